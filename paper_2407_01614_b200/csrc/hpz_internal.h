@@ -1,0 +1,115 @@
+// Internal interface between the host runtime (hpz_runtime.cpp) and the sm_100a
+// kernels (hpz_kernels.cu).  Not part of the C ABI.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/hpz.h"
+
+namespace hpz {
+
+constexpr int kMaxWorld = HPZ_MAX_WORLD;
+
+// Device-side error/timeout plumbing shared by every waiting kernel.
+struct SyncCommon {
+  uint64_t timeout_ns;                 // per-wait timeout
+  uint32_t* abort_flag;                // local arena: set after the first timeout -> later waits skip
+  unsigned long long* timeouts;        // local arena counter
+  volatile uint32_t* host_err;         // host-mapped pinned word polled by the runtime
+};
+
+// A list of flags to release (st.release.sys of `value`), possibly in peer arenas.
+struct ReleaseList {
+  uint32_t* ptr[2 * kMaxWorld];
+  int n;
+  uint32_t value;
+};
+
+// A list of local flags to acquire (ld.acquire.sys until >= target).
+struct WaitList {
+  const uint32_t* ptr[2 * kMaxWorld];
+  int n;
+  uint32_t target;
+};
+
+// Forward / backward gather (a2 / a4): out[j*src_bytes ...] = src[j][...] for j < n_src.
+struct GatherParams {
+  const char* src[kMaxWorld];          // source shards (peer-mapped), in output order
+  const uint32_t* src_flag[kMaxWorld]; // local flag acquired before reading src[j] (nullptr: none)
+  uint32_t src_target;
+  int n_src;
+  int64_t src_bytes;                   // multiple of 16
+  char* out;
+  // fused secondary store (a2): sources [sec_lo, sec_hi) also go to sec + (j-sec_lo)*src_bytes
+  char* sec;
+  int sec_lo, sec_hi;
+  WaitList war;                        // acquired before the first secondary store (E4)
+  // verification (a7)
+  unsigned long long* fp_acc;          // fingerprint accumulator (nullptr: off)
+  const char* prim[kMaxWorld];         // EXACT: primaries of all ranks
+  int64_t prim_bytes;                  // EXACT: bytes per primary shard
+  int64_t valid_bytes;                 // numel * elem_bytes: elements past it are padding
+  int elem_bytes;                      // 2 (bf16) or 4 (f32)
+  unsigned long long* mism;            // EXACT counters
+  unsigned long long* nans;
+  // completion
+  uint32_t* done_ctr;
+  ReleaseList rel;
+  // post-completion fingerprint compare (backward): waits cmp_wait, compares a vs b, zeroes both
+  unsigned long long* fp_a;
+  unsigned long long* fp_b;
+  WaitList cmp_wait;
+  unsigned long long* fp_mism;
+  unsigned long long* fp_checked;
+  SyncCommon sync;
+};
+
+// Reduce-scatter (a5).
+struct RSParams {
+  const float* src[kMaxWorld];         // src[j] = rank j's gradient slot + r*shard (peer-mapped)
+  float* out;                          // local gradient shard
+  int64_t n_vec;                       // shard / 4
+  float inv_p;
+  ReleaseList ready;                   // E5 release (may be empty if already released)
+  WaitList ready_wait;                 // E5 acquire of every rank
+  uint32_t* done_ctr;
+  ReleaseList rel;                     // E6 release
+  SyncCommon sync;
+};
+
+// Fused Adam + primary refresh (a6).
+struct AdamParams {
+  float* w;
+  float* m;
+  float* v;
+  const float* g;
+  void* prim;
+  int prim_bf16;
+  int64_t n_vec;                       // shard / 4
+  float beta1, beta2, omb1, omb2, step_size, bc2_sqrt, eps, lr_wd;
+  WaitList wait;                       // E2 (+ backward-primary readers)
+  uint32_t* done_ctr;
+  ReleaseList rel;                     // E1 for t+1
+  SyncCommon sync;
+};
+
+// Kernel launchers (hpz_kernels.cu).  Each returns the cudaError_t of the launch.
+cudaError_t launch_gather(const GatherParams& p, int grid, cudaStream_t s);
+cudaError_t launch_reduce_scatter(const RSParams& p, int world, int grid, cudaStream_t s);
+cudaError_t launch_adam(const AdamParams& p, int grid, cudaStream_t s);
+cudaError_t launch_wait(const WaitList& w, const SyncCommon& sync, cudaStream_t s);
+cudaError_t launch_release(const ReleaseList& r, cudaStream_t s);
+cudaError_t launch_copy(void* dst, const void* src, int64_t bytes, int grid, cudaStream_t s);
+cudaError_t launch_fill_u32(void* dst, uint32_t value, int64_t bytes, int grid, cudaStream_t s);
+cudaError_t launch_delay(int us, cudaStream_t s);
+// Seeded generator; e0 = global element index of dst[0]; values for
+// e >= numel are 0.  kind 0: uniform*scale, 1: dyadic.
+cudaError_t launch_synth_f32(float* dst, int64_t n, int64_t e0, int64_t numel, uint64_t key,
+                             float scale, int kind, int grid, cudaStream_t s);
+// Master init from a generator or an fp32 source (src == nullptr: generator), m = v = 0,
+// primary = rne(master).  n = shard elements, e0 = rank*shard.
+cudaError_t launch_init_shard(float* master, float* m, float* v, void* prim, int prim_bf16,
+                              const float* src_full, int64_t n, int64_t e0, int64_t numel,
+                              uint64_t key, float scale, int grid, cudaStream_t s);
+
+}  // namespace hpz

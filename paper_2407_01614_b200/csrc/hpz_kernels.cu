@@ -1,0 +1,514 @@
+// sm_100a kernels of the hpZ hot path (arXiv 2407.01614, Algorithm 1).
+//
+// Everything here is HBM- or NVLink-bound data movement plus an elementwise fp32
+// optimizer: no dense contraction, so no tensor cores.  The kernels
+// stream 16-byte words with many loads in flight per thread, use grid-stride
+// persistent grids sized to the SM count, and order themselves against other GPUs
+// with release/acquire epoch flags at system scope.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "hpz_internal.h"
+
+namespace hpz {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kGatherUnroll = 8;                        // 8 x 16 B in flight per thread
+constexpr int kTileVec = kThreads * kGatherUnroll;      // 16-byte words per gather tile (32 KiB)
+constexpr int kRSUnroll = 2;
+constexpr int kAdamUnroll = 2;
+
+// ------------------------------------------------------------------ memory-model helpers
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// Streaming 16-byte load that does not allocate in L1 (data is read once).  Peer
+// addresses bypass the local L2 and are served by the owner's L2/HBM over NVLink.
+__device__ __forceinline__ int4 ld_stream(const int4* p) {
+  int4 r;
+  asm volatile("ld.global.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void st_v4(int4* p, const int4& v) {
+  asm volatile("st.global.v4.s32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w)
+               : "memory");
+}
+
+// Acquire one flag (>= target) with a timeout; returns false on timeout.
+__device__ bool wait_geq(const uint32_t* flag, uint32_t target, const SyncCommon& s) {
+  if (ld_acquire_sys(flag) >= target) return true;
+  if (*(volatile uint32_t*)s.abort_flag) return false;
+  const uint64_t t0 = globaltimer();
+  uint32_t spins = 0;
+  while (ld_acquire_sys(flag) < target) {
+    if ((++spins & 63u) == 0) {
+      if (*(volatile uint32_t*)s.abort_flag) return false;
+      if (globaltimer() - t0 > s.timeout_ns) {
+        atomicAdd(s.timeouts, 1ull);
+        atomicExch(s.abort_flag, 1u);
+        *s.host_err = 1u;
+        __threadfence_system();
+        return false;
+      }
+    }
+    __nanosleep(32);
+  }
+  return true;
+}
+
+__device__ void wait_all(const WaitList& w, const SyncCommon& s) {
+  for (int k = 0; k < w.n; ++k) wait_geq(w.ptr[k], w.target, s);
+}
+
+__device__ void release_all(const ReleaseList& r) {
+  for (int k = 0; k < r.n; ++k) st_release_sys(r.ptr[k], r.value);
+}
+
+// Last-CTA detection: returns true in thread 0 of the CTA that finishes last.  Every
+// CTA's global stores are made visible at system scope before it is counted, so the
+// last CTA may release flags that cover the whole grid's output.
+__device__ __forceinline__ bool last_cta(uint32_t* ctr) {
+  __syncthreads();
+  bool last = false;
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    const uint32_t prev = atomicAdd(ctr, 1u);
+    if (prev == gridDim.x - 1) {
+      *ctr = 0u;   // reset for the next launch (ordered by the stream)
+      __threadfence_system();
+      last = true;
+    }
+  }
+  return last;
+}
+
+template <typename T>
+__device__ __forceinline__ T block_sum(T v) {
+  __shared__ T red[kThreads / 32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) red[wid] = v;
+  __syncthreads();
+  T s = 0;
+  if (threadIdx.x == 0)
+    for (int k = 0; k < kThreads / 32; ++k) s += red[k];
+  return s;   // valid in thread 0
+}
+
+// Order-independent 64-bit checksum contribution of one 16-byte word at global word
+// index gi (a7).  Not cryptographic: it detects stale/garbage words, the exact mode
+// counts elements.
+__device__ __forceinline__ uint64_t fp_word(uint32_t gi, const int4& w) {
+  uint32_t h = (uint32_t)w.x * 0x85EBCA6Bu ^ (uint32_t)w.y * 0xC2B2AE35u ^
+               (uint32_t)w.z * 0x27D4EB2Fu ^ (uint32_t)w.w * 0x165667B1u ^ gi * 0x9E3779B1u;
+  h ^= h >> 15;
+  h *= 0x2C1B3C6Du;
+  h ^= h >> 12;
+  uint32_t h2 = h * 0x297A2D39u;
+  h2 ^= h2 >> 16;
+  return ((uint64_t)h2 << 32) | h;
+}
+
+// Per-element compare of a 16-byte word (EXACT mode): counts differing elements and
+// NaN elements among the first `valid` elements of the word.
+__device__ __forceinline__ void exact_word(const int4& got, const int4& want, int elem_bytes,
+                                           int valid, unsigned long long& mism,
+                                           unsigned long long& nans) {
+  const uint32_t g[4] = {(uint32_t)got.x, (uint32_t)got.y, (uint32_t)got.z, (uint32_t)got.w};
+  const uint32_t e[4] = {(uint32_t)want.x, (uint32_t)want.y, (uint32_t)want.z, (uint32_t)want.w};
+  if (elem_bytes == 2) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      if (k >= valid) break;
+      const uint32_t a = (g[k >> 1] >> ((k & 1) * 16)) & 0xFFFFu;
+      const uint32_t b = (e[k >> 1] >> ((k & 1) * 16)) & 0xFFFFu;
+      mism += (a != b);
+      nans += ((a & 0x7F80u) == 0x7F80u) && ((a & 0x007Fu) != 0u);
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (k >= valid) break;
+      mism += (g[k] != e[k]);
+      nans += ((g[k] & 0x7F800000u) == 0x7F800000u) && ((g[k] & 0x007FFFFFu) != 0u);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ gather (a2, a4)
+// Grid-stride over tiles w -> (source j = w % n_src, tile = w / n_src): consecutive CTAs
+// pull from different peers so every NVLink port is busy.  Each CTA acquires a
+// source's flag once, before its first read of that source.
+template <bool SEC, bool FP, bool EXACT>
+__global__ void __launch_bounds__(kThreads) gather_kernel(const __grid_constant__ GatherParams p) {
+  const int n_src = p.n_src;
+  const int64_t vec_per_src = p.src_bytes >> 4;
+  const int64_t tiles_per_src = (vec_per_src + kTileVec - 1) / kTileVec;
+  const int64_t n_tiles = tiles_per_src * n_src;
+  const int64_t prim_vec = p.prim_bytes >> 4;
+  const int per_vec = 16 / p.elem_bytes;
+  const int64_t valid_elems = p.valid_bytes / p.elem_bytes;
+  uint32_t waited = 0;
+  bool war_done = false;
+  uint64_t fp = 0;
+  unsigned long long mism = 0, nans = 0;
+
+  for (int64_t w = blockIdx.x; w < n_tiles; w += gridDim.x) {
+    const int j = (int)(w % n_src);
+    const int64_t tile = w / n_src;
+    if (!((waited >> j) & 1u)) {
+      if (threadIdx.x == 0 && p.src_flag[j] != nullptr) wait_geq(p.src_flag[j], p.src_target, p.sync);
+      __syncthreads();
+      waited |= 1u << j;
+    }
+    const bool to_sec = SEC && j >= p.sec_lo && j < p.sec_hi;
+    if (SEC && to_sec && !war_done) {
+      if (threadIdx.x == 0) wait_all(p.war, p.sync);
+      __syncthreads();
+      war_done = true;
+    }
+    const int4* src = reinterpret_cast<const int4*>(p.src[j]);
+    int4* out = reinterpret_cast<int4*>(p.out) + (int64_t)j * vec_per_src;
+    int4* sec = SEC ? reinterpret_cast<int4*>(p.sec) + (int64_t)(j - p.sec_lo) * vec_per_src : nullptr;
+    const int64_t v0 = tile * kTileVec + threadIdx.x;
+    int4 r[kGatherUnroll];
+#pragma unroll
+    for (int u = 0; u < kGatherUnroll; ++u) {
+      const int64_t v = v0 + (int64_t)u * kThreads;
+      if (v < vec_per_src) r[u] = ld_stream(src + v);
+    }
+#pragma unroll
+    for (int u = 0; u < kGatherUnroll; ++u) {
+      const int64_t v = v0 + (int64_t)u * kThreads;
+      if (v < vec_per_src) {
+        st_v4(out + v, r[u]);
+        if (SEC && to_sec) st_v4(sec + v, r[u]);
+        const int64_t gv = (int64_t)j * vec_per_src + v;   // word index in the full buffer
+        if (FP) fp += fp_word((uint32_t)gv, r[u]);
+        if (EXACT) {
+          const int owner = (int)(gv / prim_vec);
+          const int64_t off = gv - (int64_t)owner * prim_vec;
+          const int4 want = ld_stream(reinterpret_cast<const int4*>(p.prim[owner]) + off);
+          const int64_t e0 = gv * per_vec;
+          const int64_t valid = valid_elems - e0;
+          if (valid > 0)
+            exact_word(r[u], want, p.elem_bytes, valid >= per_vec ? per_vec : (int)valid, mism, nans);
+        }
+      }
+    }
+  }
+
+  if (FP) {
+    const uint64_t s = block_sum<unsigned long long>(fp);
+    if (threadIdx.x == 0 && s) atomicAdd(p.fp_acc, (unsigned long long)s);
+  }
+  if (EXACT) {
+    const unsigned long long sm = block_sum<unsigned long long>(mism);
+    const unsigned long long sn = block_sum<unsigned long long>(nans);
+    if (threadIdx.x == 0) {
+      if (sm) atomicAdd(p.mism, sm);
+      if (sn) atomicAdd(p.nans, sn);
+    }
+  }
+  if (last_cta(p.done_ctr)) {
+    if (p.fp_a != nullptr) {
+      wait_all(p.cmp_wait, p.sync);    // the forward checksum of this step is complete
+      const unsigned long long a = atomicExch(p.fp_a, 0ull);
+      const unsigned long long b = atomicExch(p.fp_b, 0ull);
+      atomicAdd(p.fp_checked, 1ull);
+      if (a != b) atomicAdd(p.fp_mism, 1ull);
+    }
+    release_all(p.rel);
+  }
+}
+
+// ------------------------------------------------------------------ reduce-scatter (a5)
+__device__ __forceinline__ float4 add4(const float4& a, const float4& b) {
+  return make_float4(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y), __fadd_rn(a.z, b.z),
+                     __fadd_rn(a.w, b.w));
+}
+__device__ __forceinline__ float4 ld_f4(const float* p) {
+  const int4 r = ld_stream(reinterpret_cast<const int4*>(p));
+  return make_float4(__int_as_float(r.x), __int_as_float(r.y), __int_as_float(r.z),
+                     __int_as_float(r.w));
+}
+
+// Fixed association (reading R7): adjacent rank pairs summed level by level, an odd
+// last operand carried up — for P=8: ((G0+G1)+(G2+G3))+((G4+G5)+(G6+G7)).
+template <int P>
+__device__ __forceinline__ float4 pairwise_sum(float4 (&x)[P]) {
+#pragma unroll
+  for (int n = P; n > 1; n = (n + 1) / 2) {
+#pragma unroll
+    for (int k = 0; k < n / 2; ++k) x[k] = add4(x[2 * k], x[2 * k + 1]);
+    if (n & 1) x[n / 2] = x[n - 1];
+  }
+  return x[0];
+}
+
+template <int P>
+__global__ void __launch_bounds__(kThreads) rs_kernel(const __grid_constant__ RSParams p) {
+  if (threadIdx.x == 0) {
+    if (p.ready.n) {
+      __threadfence_system();   // this rank's gradient slot (written earlier on the stream)
+      release_all(p.ready);
+    }
+    wait_all(p.ready_wait, p.sync);
+  }
+  __syncthreads();
+  const int64_t stride = (int64_t)gridDim.x * kThreads * kRSUnroll;
+  for (int64_t base = (int64_t)blockIdx.x * kThreads * kRSUnroll + threadIdx.x; base < p.n_vec;
+       base += stride) {
+    float4 x[kRSUnroll][P];
+#pragma unroll
+    for (int u = 0; u < kRSUnroll; ++u) {
+      const int64_t v = base + (int64_t)u * kThreads;
+      if (v < p.n_vec) {
+#pragma unroll
+        for (int j = 0; j < P; ++j) x[u][j] = ld_f4(p.src[j] + 4 * v);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kRSUnroll; ++u) {
+      const int64_t v = base + (int64_t)u * kThreads;
+      if (v < p.n_vec) {
+        float4 s = pairwise_sum<P>(x[u]);
+        s.x = __fmul_rn(s.x, p.inv_p);
+        s.y = __fmul_rn(s.y, p.inv_p);
+        s.z = __fmul_rn(s.z, p.inv_p);
+        s.w = __fmul_rn(s.w, p.inv_p);
+        *reinterpret_cast<float4*>(p.out + 4 * v) = s;
+      }
+    }
+  }
+  if (last_cta(p.done_ctr)) release_all(p.rel);
+}
+
+// ------------------------------------------------------------------ Adam (a6)
+struct AdamScalarsDev {
+  float beta1, beta2, omb1, omb2, step_size, bc2_sqrt, eps, lr_wd;
+};
+
+// One element, exactly the oracle's operation sequence (no contraction: every
+// operation is an explicit round-to-nearest intrinsic).
+__device__ __forceinline__ void adam1(float& w, float& m, float& v, float g, const AdamParams& p) {
+  m = __fadd_rn(__fmul_rn(p.beta1, m), __fmul_rn(p.omb1, g));
+  v = __fadd_rn(__fmul_rn(p.beta2, v), __fmul_rn(__fmul_rn(p.omb2, g), g));
+  const float d = __fadd_rn(__fdiv_rn(__fsqrt_rn(v), p.bc2_sqrt), p.eps);
+  if (p.lr_wd != 0.0f) w = __fsub_rn(w, __fmul_rn(p.lr_wd, w));
+  w = __fsub_rn(w, __fmul_rn(p.step_size, __fdiv_rn(m, d)));
+}
+
+__global__ void __launch_bounds__(kThreads) adam_kernel(const __grid_constant__ AdamParams p) {
+  if (threadIdx.x == 0) wait_all(p.wait, p.sync);   // E2: peers finished reading my primary
+  __syncthreads();
+  const int64_t stride = (int64_t)gridDim.x * kThreads * kAdamUnroll;
+  for (int64_t base = (int64_t)blockIdx.x * kThreads * kAdamUnroll + threadIdx.x; base < p.n_vec;
+       base += stride) {
+    float4 w[kAdamUnroll], m[kAdamUnroll], v[kAdamUnroll], g[kAdamUnroll];
+#pragma unroll
+    for (int u = 0; u < kAdamUnroll; ++u) {
+      const int64_t i = base + (int64_t)u * kThreads;
+      if (i < p.n_vec) {
+        g[u] = ld_f4(p.g + 4 * i);
+        w[u] = ld_f4(p.w + 4 * i);
+        m[u] = ld_f4(p.m + 4 * i);
+        v[u] = ld_f4(p.v + 4 * i);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kAdamUnroll; ++u) {
+      const int64_t i = base + (int64_t)u * kThreads;
+      if (i < p.n_vec) {
+        adam1(w[u].x, m[u].x, v[u].x, g[u].x, p);
+        adam1(w[u].y, m[u].y, v[u].y, g[u].y, p);
+        adam1(w[u].z, m[u].z, v[u].z, g[u].z, p);
+        adam1(w[u].w, m[u].w, v[u].w, g[u].w, p);
+        reinterpret_cast<float4*>(p.w)[i] = w[u];
+        reinterpret_cast<float4*>(p.m)[i] = m[u];
+        reinterpret_cast<float4*>(p.v)[i] = v[u];
+        if (p.prim_bf16) {
+          __nv_bfloat162 lo = __floats2bfloat162_rn(w[u].x, w[u].y);   // cvt.rn.bf16x2.f32
+          __nv_bfloat162 hi = __floats2bfloat162_rn(w[u].z, w[u].w);
+          uint2 pk;
+          pk.x = *reinterpret_cast<uint32_t*>(&lo);
+          pk.y = *reinterpret_cast<uint32_t*>(&hi);
+          reinterpret_cast<uint2*>(p.prim)[i] = pk;
+        } else {
+          reinterpret_cast<float4*>(p.prim)[i] = w[u];
+        }
+      }
+    }
+  }
+  if (last_cta(p.done_ctr)) release_all(p.rel);   // E1: primary of step t+1 is ready
+}
+
+// ------------------------------------------------------------------ small kernels
+__global__ void wait_kernel(const WaitList w, const SyncCommon s) {
+  if (threadIdx.x == 0) wait_all(w, s);
+}
+
+__global__ void release_kernel(const ReleaseList r) {
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    release_all(r);
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) copy_kernel(int4* dst, const int4* src, int64_t n_vec) {
+  for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n_vec;
+       i += (int64_t)gridDim.x * kThreads)
+    st_v4(dst + i, ld_stream(src + i));
+}
+
+__global__ void __launch_bounds__(kThreads) fill_kernel(uint32_t* dst, uint32_t value, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * kThreads)
+    dst[i] = value;
+}
+
+__global__ void delay_kernel(uint64_t ns) {
+  const uint64_t t0 = globaltimer();
+  while (globaltimer() - t0 < ns) __nanosleep(1000);
+}
+
+// Seeded counter-based generator, the device twin of synth/inputs.py.
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z ^= z >> 30;
+  z *= 0xBF58476D1CE4E5B9ull;
+  z ^= z >> 27;
+  z *= 0x94D049BB133111EBull;
+  z ^= z >> 31;
+  return z;
+}
+__device__ __forceinline__ float synth_value(uint64_t key, int64_t e, float scale, int kind) {
+  const uint64_t x = mix64(key + (uint64_t)(e + 1) * 0x9E3779B97F4A7C15ull);
+  if (kind == 0) {
+    const int32_t i = (int32_t)(x >> 40) - (1 << 23);
+    return __fmul_rn((float)i * 0x1p-23f, scale);   // both steps exact (24-bit int, 2^k scale)
+  }
+  const int32_t i = (int32_t)(x >> 53) - (1 << 10);
+  return (float)i * 0x1p-20f;
+}
+
+__global__ void __launch_bounds__(kThreads) synth_kernel(float* dst, int64_t n, int64_t e0,
+                                                         int64_t numel, uint64_t key, float scale,
+                                                         int kind) {
+  for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * kThreads) {
+    const int64_t e = e0 + i;
+    dst[i] = e < numel ? synth_value(key, e, scale, kind) : 0.0f;
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) init_shard_kernel(float* master, float* m, float* v,
+                                                              void* prim, int prim_bf16,
+                                                              const float* src_full, int64_t n,
+                                                              int64_t e0, int64_t numel,
+                                                              uint64_t key, float scale) {
+  for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * kThreads) {
+    const int64_t e = e0 + i;
+    float w = 0.0f;
+    if (e < numel) w = src_full ? src_full[e] : synth_value(key, e, scale, 0);
+    master[i] = w;
+    m[i] = 0.0f;
+    v[i] = 0.0f;
+    if (prim_bf16)
+      reinterpret_cast<__nv_bfloat16*>(prim)[i] = __float2bfloat16_rn(w);
+    else
+      reinterpret_cast<float*>(prim)[i] = w;
+  }
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ launchers
+cudaError_t launch_gather(const GatherParams& p, int grid, cudaStream_t s) {
+  const bool sec = p.sec != nullptr, fp = p.fp_acc != nullptr, ex = p.mism != nullptr;
+  if (sec && fp) gather_kernel<true, true, false><<<grid, kThreads, 0, s>>>(p);
+  else if (sec) gather_kernel<true, false, false><<<grid, kThreads, 0, s>>>(p);
+  else if (fp && ex) gather_kernel<false, true, true><<<grid, kThreads, 0, s>>>(p);
+  else if (fp) gather_kernel<false, true, false><<<grid, kThreads, 0, s>>>(p);
+  else if (ex) gather_kernel<false, false, true><<<grid, kThreads, 0, s>>>(p);
+  else gather_kernel<false, false, false><<<grid, kThreads, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_reduce_scatter(const RSParams& p, int world, int grid, cudaStream_t s) {
+  switch (world) {
+#define HPZ_RS_CASE(P) \
+  case P: rs_kernel<P><<<grid, kThreads, 0, s>>>(p); break;
+    HPZ_RS_CASE(1) HPZ_RS_CASE(2) HPZ_RS_CASE(3) HPZ_RS_CASE(4) HPZ_RS_CASE(5) HPZ_RS_CASE(6)
+    HPZ_RS_CASE(7) HPZ_RS_CASE(8) HPZ_RS_CASE(9) HPZ_RS_CASE(10) HPZ_RS_CASE(11) HPZ_RS_CASE(12)
+    HPZ_RS_CASE(13) HPZ_RS_CASE(14) HPZ_RS_CASE(15) HPZ_RS_CASE(16)
+#undef HPZ_RS_CASE
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_adam(const AdamParams& p, int grid, cudaStream_t s) {
+  adam_kernel<<<grid, kThreads, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_wait(const WaitList& w, const SyncCommon& sync, cudaStream_t s) {
+  wait_kernel<<<1, 32, 0, s>>>(w, sync);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_release(const ReleaseList& r, cudaStream_t s) {
+  release_kernel<<<1, 32, 0, s>>>(r);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_copy(void* dst, const void* src, int64_t bytes, int grid, cudaStream_t s) {
+  copy_kernel<<<grid, kThreads, 0, s>>>(reinterpret_cast<int4*>(dst),
+                                        reinterpret_cast<const int4*>(src), bytes >> 4);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fill_u32(void* dst, uint32_t value, int64_t bytes, int grid, cudaStream_t s) {
+  fill_kernel<<<grid, kThreads, 0, s>>>(reinterpret_cast<uint32_t*>(dst), value, bytes >> 2);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_delay(int us, cudaStream_t s) {
+  delay_kernel<<<1, 32, 0, s>>>((uint64_t)us * 1000ull);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_synth_f32(float* dst, int64_t n, int64_t e0, int64_t numel, uint64_t key,
+                             float scale, int kind, int grid, cudaStream_t s) {
+  synth_kernel<<<grid, kThreads, 0, s>>>(dst, n, e0, numel, key, scale, kind);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_init_shard(float* master, float* m, float* v, void* prim, int prim_bf16,
+                              const float* src_full, int64_t n, int64_t e0, int64_t numel,
+                              uint64_t key, float scale, int grid, cudaStream_t s) {
+  init_shard_kernel<<<grid, kThreads, 0, s>>>(master, m, v, prim, prim_bf16, src_full, n, e0,
+                                              numel, key, scale);
+  return cudaGetLastError();
+}
+
+}  // namespace hpz

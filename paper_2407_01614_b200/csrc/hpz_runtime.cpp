@@ -1,0 +1,763 @@
+// Host runtime of libhpz: layout (a1), context/epoch bookkeeping, peer mappings and
+// the C ABI declared in include/hpz.h.  Every hot-path call validates on the host,
+// builds one parameter block and enqueues kernels on the caller's stream.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "hpz_internal.h"
+
+using namespace hpz;
+
+namespace {
+
+constexpr uint64_t kBufAlign = 4096;      // every per-layer buffer starts 4 KiB-aligned
+constexpr uint64_t kCtrlAlign = 65536;
+
+uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
+
+enum FlagKind { F_PRIM_READY = 0, F_FWD_DONE, F_SEC_READY, F_BWD_DONE, F_BWDP_DONE, F_NUM_LAYER_KINDS };
+enum SlotFlagKind { S_GRAD_READY = 0, S_RS_DONE, S_NUM };
+enum CtrKind { C_FWD = 0, C_BWD, C_RS, C_ADAM, C_NUM };
+
+struct Layer {
+  int64_t numel, numel_pad, shard, sec_shard;
+  uint64_t off_primary, off_master, off_m, off_v, off_gshard, off_secondary;
+  int slot;
+  // host bookkeeping of the step t the layer's ops were issued for (-1: never)
+  int64_t fwd_t = -1, bwd_t = -1, rs_t = -1, step_t = -1;
+};
+
+}  // namespace
+
+struct hpz_ctx {
+  int world = 0, node_size = 0, rank = 0, device = 0, k = 0, sm_count = 0;
+  int dtype = HPZ_BF16, elem = 2;
+  int64_t align = 256;
+  int n_layers = 0, n_slots = 0;
+  std::vector<Layer> layers;
+  std::vector<int64_t> slot_numel;        // numel_pad capacity of each grad slot
+  std::vector<uint64_t> off_slot;
+  std::vector<uint64_t> slot_use;         // completed-or-issued reduce-scatters per slot
+  std::vector<uint8_t> slot_ready_sent;   // E5 already released for the current use
+  uint64_t off_flags = 0, off_ctr = 0, off_fp = 0, off_stats = 0, ctrl_bytes = 0, arena_bytes = 0;
+  bool registered = false, bound = false, owns_arena = false;
+  char* arena[kMaxWorld] = {};            // mapped arena base of every rank
+  bool opened[kMaxWorld] = {};            // arena[j] was opened via IPC here
+  int64_t t = 0;                          // current step
+  int order = HPZ_ORDER_FIXED, stock_delay_us = 0, stock_poison = 0;
+  int verify = HPZ_VERIFY_NONE;
+  double timeout_s = 20.0;
+  uint32_t* host_err = nullptr;           // pinned, mapped
+  uint32_t* host_err_dev = nullptr;
+  cudaStream_t side = nullptr;            // stock-mode copy stream
+  cudaEvent_t side_ev = nullptr;
+  uint64_t launches = 0;
+  std::string err;
+
+  // ---- arena addressing (identical on every rank) ----
+  uint32_t* flag(int rank_arena, int kind, int layer, int src) const {
+    const uint64_t idx = ((uint64_t)kind * n_layers + layer) * world + src;
+    return reinterpret_cast<uint32_t*>(arena[rank_arena] + off_flags) + idx;
+  }
+  uint32_t* slot_flag(int rank_arena, int kind, int slot, int src) const {
+    const uint64_t base = (uint64_t)F_NUM_LAYER_KINDS * n_layers * world;
+    const uint64_t idx = base + ((uint64_t)kind * n_slots + slot) * world + src;
+    return reinterpret_cast<uint32_t*>(arena[rank_arena] + off_flags) + idx;
+  }
+  uint32_t* ctr(int kind, int idx) const {
+    return reinterpret_cast<uint32_t*>(arena[rank] + off_ctr) + (uint64_t)kind * (n_layers + n_slots) + idx;
+  }
+  unsigned long long* fp(int layer, int parity, int which) const {
+    return reinterpret_cast<unsigned long long*>(arena[rank] + off_fp) + ((uint64_t)layer * 2 + parity) * 2 + which;
+  }
+  // stats: 0 mismatches, 1 nans, 2 fp_mism, 3 fp_checked, 4 timeouts, 5 abort flag (u32)
+  unsigned long long* stat(int i) const {
+    return reinterpret_cast<unsigned long long*>(arena[rank] + off_stats) + i;
+  }
+  SyncCommon sync() const {
+    SyncCommon s;
+    s.timeout_ns = (uint64_t)(timeout_s * 1e9);
+    s.abort_flag = reinterpret_cast<uint32_t*>(stat(5));
+    s.timeouts = stat(4);
+    s.host_err = host_err_dev;
+    return s;
+  }
+  int node_first() const { return (rank / node_size) * node_size; }
+  int local() const { return rank % node_size; }
+};
+
+namespace {
+
+int fail(hpz_ctx* c, int code, const char* fmt, ...) {
+  if (c) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    c->err = buf;
+  }
+  return code;
+}
+
+#define HPZ_CUDA(c, call)                                                              \
+  do {                                                                                 \
+    cudaError_t e_ = (call);                                                           \
+    if (e_ != cudaSuccess) return fail(c, HPZ_ECUDA, "%s: %s", #call, cudaGetErrorString(e_)); \
+  } while (0)
+
+int check_ready(hpz_ctx* c) {
+  if (!c) return HPZ_EINVAL;
+  if (!c->registered || !c->bound) return fail(c, HPZ_ESTATE, "context not registered/bound");
+  if (c->host_err && *(volatile uint32_t*)c->host_err)
+    return fail(c, HPZ_ETIMEOUT, "a device-side flag wait timed out (a peer never released)");
+  return HPZ_OK;
+}
+
+int check_layer(hpz_ctx* c, int layer) {
+  if (layer < 0 || layer >= c->n_layers) return fail(c, HPZ_EINVAL, "layer %d out of range", layer);
+  return HPZ_OK;
+}
+
+int grid_for(const hpz_ctx* c, int64_t work_items, int per_sm) {
+  int64_t g = (int64_t)c->sm_count * per_sm;
+  if (work_items < g) g = work_items;
+  return g < 1 ? 1 : (int)g;
+}
+
+uint32_t epoch(int64_t x) { return (uint32_t)x; }
+
+int do_init_shard(hpz_ctx* c, int layer, const float* src, uint64_t key, float scale, cudaStream_t s) {
+  Layer& L = c->layers[layer];
+  char* a = c->arena[c->rank];
+  if (L.fwd_t >= 0) return fail(c, HPZ_ESTATE, "layer %d already in use; load before the first gather", layer);
+  cudaError_t e = launch_init_shard(reinterpret_cast<float*>(a + L.off_master), reinterpret_cast<float*>(a + L.off_m),
+                                    reinterpret_cast<float*>(a + L.off_v), a + L.off_primary, c->dtype == HPZ_BF16,
+                                    src, L.shard, (int64_t)c->rank * L.shard, L.numel, key, scale,
+                                    grid_for(c, (L.shard + 255) / 256, 8), s);
+  if (e != cudaSuccess) return fail(c, HPZ_ECUDA, "init_shard launch: %s", cudaGetErrorString(e));
+  // E1 for step 0: PRIMARY_READY_j[layer][me] = 1 in every rank's arena
+  ReleaseList r{};
+  for (int j = 0; j < c->world; ++j) r.ptr[r.n++] = c->flag(j, F_PRIM_READY, layer, c->rank);
+  r.value = epoch(c->t + 1);
+  e = launch_release(r, s);
+  if (e != cudaSuccess) return fail(c, HPZ_ECUDA, "release launch: %s", cudaGetErrorString(e));
+  c->launches += 2;
+  return HPZ_OK;
+}
+
+// E6: wait until every rank finished reading the previous use of the layer's slot.
+int slot_acquire(hpz_ctx* c, int layer, cudaStream_t s) {
+  const int slot = c->layers[layer].slot;
+  const uint64_t use = c->slot_use[slot];
+  if (use == 0) return HPZ_OK;
+  WaitList w{};
+  for (int j = 0; j < c->world; ++j) w.ptr[w.n++] = c->slot_flag(c->rank, S_RS_DONE, slot, j);
+  w.target = epoch(use);
+  cudaError_t e = launch_wait(w, c->sync(), s);
+  if (e != cudaSuccess) return fail(c, HPZ_ECUDA, "wait launch: %s", cudaGetErrorString(e));
+  c->launches += 1;
+  return HPZ_OK;
+}
+
+ReleaseList grad_ready_list(hpz_ctx* c, int slot) {
+  ReleaseList r{};
+  for (int j = 0; j < c->world; ++j) r.ptr[r.n++] = c->slot_flag(j, S_GRAD_READY, slot, c->rank);
+  r.value = epoch(c->slot_use[slot] + 1);
+  return r;
+}
+
+}  // namespace
+
+extern "C" {
+
+int hpz_version(void) { return HPZ_VERSION; }
+
+int hpz_init(int world, int node_size, int rank, int device, hpz_ctx** out) {
+  if (!out) return HPZ_EINVAL;
+  *out = nullptr;
+  if (world < 1 || world > kMaxWorld || node_size < 1 || world % node_size != 0 || rank < 0 || rank >= world)
+    return HPZ_EINVAL;
+  if (device == -1) {   // host-only context: layout queries only (no CUDA calls)
+    hpz_ctx* c = new hpz_ctx();
+    c->world = world;
+    c->node_size = node_size;
+    c->k = world / node_size;
+    c->rank = rank;
+    c->device = -1;
+    *out = c;
+    return HPZ_OK;
+  }
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) {
+    cudaGetLastError();
+    return HPZ_EINVAL;
+  }
+  if (cudaSetDevice(device) != cudaSuccess) return HPZ_ECUDA;
+  hpz_ctx* c = new hpz_ctx();
+  c->world = world;
+  c->node_size = node_size;
+  c->k = world / node_size;
+  c->rank = rank;
+  c->device = device;
+  cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device);
+  if (cudaHostAlloc(reinterpret_cast<void**>(&c->host_err), sizeof(uint32_t), cudaHostAllocMapped) != cudaSuccess) {
+    delete c;
+    return HPZ_ECUDA;
+  }
+  *c->host_err = 0;
+  cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->host_err_dev), c->host_err, 0);
+  *out = c;
+  return HPZ_OK;
+}
+
+int hpz_register_flat_params(hpz_ctx* c, int n_layers, const int64_t* numel, int param_dtype,
+                             int64_t align_elems, int n_grad_slots, uint64_t* arena_bytes) {
+  if (!c) return HPZ_EINVAL;
+  if (c->registered) return fail(c, HPZ_ESTATE, "register_flat_params called twice");
+  if (n_layers < 1 || !numel) return fail(c, HPZ_EINVAL, "n_layers must be >= 1");
+  if (param_dtype != HPZ_BF16 && param_dtype != HPZ_F32) return fail(c, HPZ_EINVAL, "bad param dtype");
+  const int elem = param_dtype == HPZ_BF16 ? 2 : 4;
+  if (align_elems < 8 || (align_elems & (align_elems - 1)) || (align_elems * elem) % 16)
+    return fail(c, HPZ_EINVAL, "align_elems must be a power of two >= 8 covering 16 bytes");
+  if (n_grad_slots < 1 || n_grad_slots > n_layers) return fail(c, HPZ_EINVAL, "n_grad_slots must be in [1, n_layers]");
+  c->dtype = param_dtype;
+  c->elem = elem;
+  c->align = align_elems;
+  c->n_layers = n_layers;
+  c->n_slots = n_grad_slots;
+  c->layers.assign(n_layers, Layer{});
+  c->slot_numel.assign(n_grad_slots, 0);
+  c->slot_use.assign(n_grad_slots, 0);
+  c->slot_ready_sent.assign(n_grad_slots, 0);
+  const int64_t q = (int64_t)c->world * align_elems;
+  for (int i = 0; i < n_layers; ++i) {
+    if (numel[i] < 1) return fail(c, HPZ_EINVAL, "layer %d: numel must be >= 1", i);
+    Layer& L = c->layers[i];
+    L.numel = numel[i];
+    L.numel_pad = (numel[i] + q - 1) / q * q;        // Eq. (1) with padding reading R2
+    L.shard = L.numel_pad / c->world;
+    L.sec_shard = L.numel_pad / c->node_size;
+    L.slot = i % n_grad_slots;
+    if (L.numel_pad > c->slot_numel[L.slot]) c->slot_numel[L.slot] = L.numel_pad;
+  }
+  // control region: flags | completion counters | fingerprints | stats
+  const uint64_t n_flags = (uint64_t)F_NUM_LAYER_KINDS * n_layers * c->world + (uint64_t)S_NUM * n_grad_slots * c->world;
+  uint64_t off = 0;
+  c->off_flags = off;
+  off = align_up(off + n_flags * 4, 256);
+  c->off_ctr = off;
+  off = align_up(off + (uint64_t)C_NUM * (n_layers + n_grad_slots) * 4, 256);
+  c->off_fp = off;
+  off = align_up(off + (uint64_t)n_layers * 4 * 8, 256);
+  c->off_stats = off;
+  off = align_up(off + 8 * 8, 256);
+  c->ctrl_bytes = align_up(off, kCtrlAlign);
+  off = c->ctrl_bytes;
+  for (int i = 0; i < n_layers; ++i) {
+    Layer& L = c->layers[i];
+    L.off_primary = off;   off = align_up(off + (uint64_t)L.shard * elem, kBufAlign);
+    L.off_master = off;    off = align_up(off + (uint64_t)L.shard * 4, kBufAlign);
+    L.off_m = off;         off = align_up(off + (uint64_t)L.shard * 4, kBufAlign);
+    L.off_v = off;         off = align_up(off + (uint64_t)L.shard * 4, kBufAlign);
+    L.off_gshard = off;    off = align_up(off + (uint64_t)L.shard * 4, kBufAlign);
+    if (true) { L.off_secondary = off; off = align_up(off + (uint64_t)L.sec_shard * elem, kBufAlign); }
+  }
+  c->off_slot.assign(n_grad_slots, 0);
+  for (int s = 0; s < n_grad_slots; ++s) {
+    c->off_slot[s] = off;
+    off = align_up(off + (uint64_t)c->slot_numel[s] * 4, kBufAlign);
+  }
+  c->arena_bytes = off;
+  c->registered = true;
+  if (arena_bytes) *arena_bytes = off;
+  return HPZ_OK;
+}
+
+int hpz_arena_alloc(hpz_ctx* c, void* ipc_handle_out) {
+  if (!c) return HPZ_EINVAL;
+  if (!c->registered) return fail(c, HPZ_ESTATE, "arena_alloc before register");
+  if (c->device < 0) return fail(c, HPZ_ESTATE, "host-only context (device -1) has no arena");
+  if (c->arena[c->rank]) return fail(c, HPZ_ESTATE, "arena already allocated/bound");
+  HPZ_CUDA(c, cudaSetDevice(c->device));
+  void* p = nullptr;
+  cudaError_t e = cudaMalloc(&p, c->arena_bytes);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(c, HPZ_ENOMEM, "cudaMalloc(%llu bytes): %s", (unsigned long long)c->arena_bytes, cudaGetErrorString(e));
+  }
+  c->arena[c->rank] = static_cast<char*>(p);
+  c->owns_arena = true;
+  HPZ_CUDA(c, cudaMemset(p, 0, c->ctrl_bytes));
+  HPZ_CUDA(c, cudaDeviceSynchronize());
+  if (ipc_handle_out) {
+    cudaIpcMemHandle_t h;
+    HPZ_CUDA(c, cudaIpcGetMemHandle(&h, p));
+    static_assert(sizeof(h) == HPZ_IPC_HANDLE_BYTES, "IPC handle size");
+    std::memcpy(ipc_handle_out, &h, sizeof h);
+  }
+  return HPZ_OK;
+}
+
+static int finish_bind(hpz_ctx* c) {
+  HPZ_CUDA(c, cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+  HPZ_CUDA(c, cudaEventCreateWithFlags(&c->side_ev, cudaEventDisableTiming));
+  c->bound = true;
+  return HPZ_OK;
+}
+
+int hpz_arena_open(hpz_ctx* c, const void* all_handles) {
+  if (!c || !all_handles) return HPZ_EINVAL;
+  if (!c->registered || !c->arena[c->rank] || !c->owns_arena) return fail(c, HPZ_ESTATE, "arena_open needs arena_alloc first");
+  if (c->bound) return fail(c, HPZ_ESTATE, "already bound");
+  HPZ_CUDA(c, cudaSetDevice(c->device));
+  const char* hs = static_cast<const char*>(all_handles);
+  for (int j = 0; j < c->world; ++j) {
+    if (j == c->rank) continue;
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, hs + (size_t)j * HPZ_IPC_HANDLE_BYTES, sizeof h);
+    void* p = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return fail(c, HPZ_ECUDA, "cudaIpcOpenMemHandle(rank %d): %s", j, cudaGetErrorString(e));
+    }
+    c->arena[j] = static_cast<char*>(p);
+    c->opened[j] = true;
+  }
+  return finish_bind(c);
+}
+
+int hpz_bind(hpz_ctx* c, void* const* ptrs) {
+  if (!c || !ptrs) return HPZ_EINVAL;
+  if (!c->registered) return fail(c, HPZ_ESTATE, "bind before register");
+  if (c->device < 0) return fail(c, HPZ_ESTATE, "host-only context (device -1) cannot bind");
+  if (c->bound) return fail(c, HPZ_ESTATE, "already bound");
+  for (int j = 0; j < c->world; ++j) {
+    if (!ptrs[j] || (reinterpret_cast<uintptr_t>(ptrs[j]) & 255)) return fail(c, HPZ_EINVAL, "arena_ptrs[%d] null or not 256-byte aligned", j);
+  }
+  if (c->arena[c->rank] && c->arena[c->rank] != ptrs[c->rank]) return fail(c, HPZ_EINVAL, "arena_ptrs[rank] differs from the allocated arena");
+  HPZ_CUDA(c, cudaSetDevice(c->device));
+  const bool zero = c->arena[c->rank] == nullptr;
+  for (int j = 0; j < c->world; ++j) c->arena[j] = static_cast<char*>(ptrs[j]);
+  if (zero) {
+    HPZ_CUDA(c, cudaMemset(c->arena[c->rank], 0, c->ctrl_bytes));
+    HPZ_CUDA(c, cudaDeviceSynchronize());
+  }
+  return finish_bind(c);
+}
+
+int hpz_finalize(hpz_ctx* c) {
+  if (!c) return HPZ_EINVAL;
+  if (c->device < 0) {
+    delete c;
+    return HPZ_OK;
+  }
+  cudaSetDevice(c->device);
+  cudaDeviceSynchronize();
+  for (int j = 0; j < c->world; ++j)
+    if (c->opened[j]) cudaIpcCloseMemHandle(c->arena[j]);
+  if (c->owns_arena && c->arena[c->rank]) cudaFree(c->arena[c->rank]);
+  if (c->side) cudaStreamDestroy(c->side);
+  if (c->side_ev) cudaEventDestroy(c->side_ev);
+  if (c->host_err) cudaFreeHost(c->host_err);
+  delete c;
+  return HPZ_OK;
+}
+
+int hpz_layer_info(const hpz_ctx* cc, int layer, hpz_layer_info_t* out) {
+  hpz_ctx* c = const_cast<hpz_ctx*>(cc);
+  if (!c || !out) return HPZ_EINVAL;
+  if (!c->registered) return fail(c, HPZ_ESTATE, "not registered");
+  if (int rc = check_layer(c, layer)) return rc;
+  const Layer& L = c->layers[layer];
+  out->numel = L.numel;
+  out->numel_pad = L.numel_pad;
+  out->shard = L.shard;
+  out->sec_shard = L.sec_shard;
+  out->off_primary = L.off_primary;
+  out->off_master = L.off_master;
+  out->off_m = L.off_m;
+  out->off_v = L.off_v;
+  out->off_grad_shard = L.off_gshard;
+  out->off_secondary = L.off_secondary;
+  out->off_grad_slot = c->off_slot[L.slot];
+  out->grad_slot = L.slot;
+  out->_pad = 0;
+  return HPZ_OK;
+}
+
+int hpz_arena_ptr(const hpz_ctx* cc, int rank, void** out) {
+  hpz_ctx* c = const_cast<hpz_ctx*>(cc);
+  if (!c || !out || rank < 0 || rank >= c->world) return HPZ_EINVAL;
+  if (!c->arena[rank]) return fail(c, HPZ_ESTATE, "arena of rank %d not mapped", rank);
+  *out = c->arena[rank];
+  return HPZ_OK;
+}
+
+int hpz_buffer(const hpz_ctx* cc, int layer, int kind, void** ptr, int64_t* n) {
+  hpz_ctx* c = const_cast<hpz_ctx*>(cc);
+  if (!c || !ptr) return HPZ_EINVAL;
+  if (!c->registered || !c->arena[c->rank]) return fail(c, HPZ_ESTATE, "arena not allocated/bound");
+  if (int rc = check_layer(c, layer)) return rc;
+  const Layer& L = c->layers[layer];
+  char* a = c->arena[c->rank];
+  int64_t cnt = L.shard;
+  switch (kind) {
+    case HPZ_BUF_PRIMARY: *ptr = a + L.off_primary; break;
+    case HPZ_BUF_MASTER: *ptr = a + L.off_master; break;
+    case HPZ_BUF_ADAM_M: *ptr = a + L.off_m; break;
+    case HPZ_BUF_ADAM_V: *ptr = a + L.off_v; break;
+    case HPZ_BUF_GRAD_SHARD: *ptr = a + L.off_gshard; break;
+    case HPZ_BUF_SECONDARY: *ptr = a + L.off_secondary; cnt = L.sec_shard; break;
+    case HPZ_BUF_GRAD_SLOT: *ptr = a + c->off_slot[L.slot]; cnt = L.numel_pad; break;
+    default: return fail(c, HPZ_EINVAL, "bad buffer kind %d", kind);
+  }
+  if (n) *n = cnt;
+  return HPZ_OK;
+}
+
+int hpz_current_step(const hpz_ctx* c, int64_t* t) {
+  if (!c || !t) return HPZ_EINVAL;
+  *t = c->t;
+  return HPZ_OK;
+}
+
+int hpz_counters(hpz_ctx* c, hpz_counters_t* out, int reset) {
+  if (!c || !out) return HPZ_EINVAL;
+  if (c->device < 0) return fail(c, HPZ_ESTATE, "host-only context has no counters");
+  if (!c->registered || !c->arena[c->rank]) return fail(c, HPZ_ESTATE, "arena not allocated/bound");
+  HPZ_CUDA(c, cudaSetDevice(c->device));
+  HPZ_CUDA(c, cudaDeviceSynchronize());
+  unsigned long long s[5];
+  HPZ_CUDA(c, cudaMemcpy(s, c->stat(0), sizeof s, cudaMemcpyDeviceToHost));
+  out->mismatches = s[0];
+  out->nan_reads = s[1];
+  out->fp_mismatches = s[2];
+  out->fp_checked = s[3];
+  out->timeouts = s[4];
+  out->launches = c->launches;
+  if (reset) HPZ_CUDA(c, cudaMemset(c->stat(0), 0, 4 * sizeof(unsigned long long)));
+  return HPZ_OK;
+}
+
+const char* hpz_last_error(const hpz_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+int hpz_set_order(hpz_ctx* c, int order, int stock_delay_us, int stock_poison) {
+  if (!c) return HPZ_EINVAL;
+  if (order < HPZ_ORDER_FIXED || order > HPZ_ORDER_OFF || stock_delay_us < 0) return fail(c, HPZ_EINVAL, "bad order");
+  c->order = order;
+  c->stock_delay_us = stock_delay_us;
+  c->stock_poison = stock_poison;
+  return HPZ_OK;
+}
+
+int hpz_set_verify(hpz_ctx* c, int mode) {
+  if (!c) return HPZ_EINVAL;
+  if (mode < HPZ_VERIFY_NONE || mode > HPZ_VERIFY_EXACT) return fail(c, HPZ_EINVAL, "bad verify mode");
+  c->verify = mode;
+  return HPZ_OK;
+}
+
+int hpz_set_timeout(hpz_ctx* c, double seconds) {
+  if (!c || !(seconds > 0)) return HPZ_EINVAL;
+  c->timeout_s = seconds;
+  return HPZ_OK;
+}
+
+int hpz_load_master(hpz_ctx* c, int layer, const float* full, void* stream) {
+  if (int rc = check_ready(c)) return rc;
+  if (int rc = check_layer(c, layer)) return rc;
+  if (!full) return fail(c, HPZ_EINVAL, "null source");
+  return do_init_shard(c, layer, full, 0, 0.f, static_cast<cudaStream_t>(stream));
+}
+
+int hpz_synth_master(hpz_ctx* c, int layer, uint64_t key, float scale, void* stream) {
+  if (int rc = check_ready(c)) return rc;
+  if (int rc = check_layer(c, layer)) return rc;
+  return do_init_shard(c, layer, nullptr, key, scale, static_cast<cudaStream_t>(stream));
+}
+
+int hpz_fwd_gather(hpz_ctx* c, int layer, void* full_out, void* stream) {
+  if (int rc = check_ready(c)) return rc;
+  if (int rc = check_layer(c, layer)) return rc;
+  if (!full_out || (reinterpret_cast<uintptr_t>(full_out) & 15)) return fail(c, HPZ_EINVAL, "full_out null or not 16-byte aligned");
+  Layer& L = c->layers[layer];
+  if (L.fwd_t == c->t) return fail(c, HPZ_ESTATE, "layer %d already forward-gathered at step %lld", layer, (long long)c->t);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const uint32_t t1 = epoch(c->t + 1);
+  GatherParams p{};
+  p.n_src = c->world;
+  p.src_bytes = L.shard * c->elem;
+  for (int j = 0; j < c->world; ++j) {
+    p.src[j] = c->arena[j] + L.off_primary;
+    p.src_flag[j] = c->flag(c->rank, F_PRIM_READY, layer, j);    // E1
+  }
+  p.src_target = t1;
+  p.out = static_cast<char*>(full_out);
+  p.elem_bytes = c->elem;
+  p.valid_bytes = L.numel * c->elem;
+  const int l = c->local();
+  const int nf = c->node_first();
+  if (c->order == HPZ_ORDER_FIXED) {
+    // fused secondary store: my secondary slice l holds primaries l*k .. l*k+k-1 (R2 nesting)
+    p.sec = c->arena[c->rank] + L.off_secondary;
+    p.sec_lo = l * c->k;
+    p.sec_hi = (l + 1) * c->k;
+    for (int q = 0; q < c->node_size; ++q) p.war.ptr[p.war.n++] = c->flag(c->rank, F_BWD_DONE, layer, nf + q);   // E4
+    p.war.target = epoch(c->t);
+  }
+  if (c->verify != HPZ_VERIFY_NONE) p.fp_acc = c->fp(layer, (int)(c->t & 1), 0);
+  p.done_ctr = c->ctr(C_FWD, layer);
+  if (c->order == HPZ_ORDER_FIXED)
+    for (int q = 0; q < c->node_size; ++q) p.rel.ptr[p.rel.n++] = c->flag(nf + q, F_SEC_READY, layer, c->rank);   // E3
+  for (int j = 0; j < c->world; ++j) p.rel.ptr[p.rel.n++] = c->flag(j, F_FWD_DONE, layer, c->rank);            // E2
+  p.rel.value = t1;
+  p.sync = c->sync();
+  const int64_t tiles = (p.src_bytes / 16 + 2047) / 2048 * c->world;
+  cudaError_t e = launch_gather(p, grid_for(c, tiles, 4), s);
+  if (e != cudaSuccess) return fail(c, HPZ_ECUDA, "fwd gather launch: %s", cudaGetErrorString(e));
+  c->launches += 1;
+  if (c->order == HPZ_ORDER_STOCK) {
+    // stock ZeRO++: L_i,second <- empty(); async MemcpyD2D on another stream, no edge to the
+    // backward AllGather
+    char* sec = c->arena[c->rank] + L.off_secondary;
+    const int64_t sec_bytes = L.sec_shard * c->elem;
+    HPZ_CUDA(c, cudaEventRecord(c->side_ev, s));
+    HPZ_CUDA(c, cudaStreamWaitEvent(c->side, c->side_ev, 0));
+    if (c->stock_poison) {
+      e = launch_fill_u32(sec, c->elem == 2 ? 0x7FC07FC0u : 0x7FC00000u, sec_bytes, grid_for(c, sec_bytes / 4096 + 1, 4), c->side);
+      if (e != cudaSuccess) return fail(c, HPZ_ECUDA, "poison launch: %s", cudaGetErrorString(e));
+      c->launches += 1;
+    }
+    if (c->stock_delay_us > 0) {
+      e = launch_delay(c->stock_delay_us, c->side);
+      if (e != cudaSuccess) return fail(c, HPZ_ECUDA, "delay launch: %s", cudaGetErrorString(e));
+      c->launches += 1;
+    }
+    e = launch_copy(sec, p.out + (int64_t)l * sec_bytes, sec_bytes, grid_for(c, sec_bytes / 4096 + 1, 4), c->side);
+    if (e != cudaSuccess) return fail(c, HPZ_ECUDA, "stock copy launch: %s", cudaGetErrorString(e));
+    c->launches += 1;
+  }
+  L.fwd_t = c->t;
+  return HPZ_OK;
+}
+
+int hpz_bwd_gather(hpz_ctx* c, int layer, void* full_out, void* stream) {
+  if (int rc = check_ready(c)) return rc;
+  if (int rc = check_layer(c, layer)) return rc;
+  if (!full_out || (reinterpret_cast<uintptr_t>(full_out) & 15)) return fail(c, HPZ_EINVAL, "full_out null or not 16-byte aligned");
+  Layer& L = c->layers[layer];
+  if (L.fwd_t != c->t) return fail(c, HPZ_ESTATE, "layer %d: backward gather without its forward gather at step %lld", layer, (long long)c->t);
+  if (L.bwd_t == c->t) return fail(c, HPZ_ESTATE, "layer %d already backward-gathered at step %lld", layer, (long long)c->t);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const uint32_t t1 = epoch(c->t + 1);
+  const int nf = c->node_first();
+  const bool reads_prim = c->order == HPZ_ORDER_OFF || c->verify == HPZ_VERIFY_EXACT;
+  GatherParams p{};
+  if (c->order == HPZ_ORDER_OFF) {
+    // no hpZ: AllGather(L_i, P) from the primaries again (ZeRO-3 backward)
+    p.n_src = c->world;
+    p.src_bytes = L.shard * c->elem;
+    for (int j = 0; j < c->world; ++j) {
+      p.src[j] = c->arena[j] + L.off_primary;
+      p.src_flag[j] = c->flag(c->rank, F_PRIM_READY, layer, j);
+    }
+  } else {
+    // hpZ: AllGather(L_i, P') over the node's secondaries
+    p.n_src = c->node_size;
+    p.src_bytes = L.sec_shard * c->elem;
+    for (int q = 0; q < c->node_size; ++q) {
+      p.src[q] = c->arena[nf + q] + L.off_secondary;
+      // THE FIX: acquire SEC_READY of the owner for step t.
+      // STOCK reproduces the bug: no wait.
+      p.src_flag[q] = c->order == HPZ_ORDER_FIXED ? c->flag(c->rank, F_SEC_READY, layer, nf + q) : nullptr;
+    }
+  }
+  p.src_target = t1;
+  p.out = static_cast<char*>(full_out);
+  p.elem_bytes = c->elem;
+  p.valid_bytes = L.numel * c->elem;
+  if (c->verify == HPZ_VERIFY_EXACT) {
+    for (int j = 0; j < c->world; ++j) p.prim[j] = c->arena[j] + L.off_primary;
+    p.prim_bytes = L.shard * c->elem;
+    p.mism = c->stat(0);
+    p.nans = c->stat(1);
+  }
+  if (c->verify != HPZ_VERIFY_NONE) {
+    const int par = (int)(c->t & 1);
+    p.fp_acc = c->fp(layer, par, 1);
+    p.fp_a = c->fp(layer, par, 0);
+    p.fp_b = c->fp(layer, par, 1);
+    p.cmp_wait.ptr[p.cmp_wait.n++] = c->flag(c->rank, F_FWD_DONE, layer, c->rank);   // my forward finished
+    p.cmp_wait.target = t1;
+    p.fp_mism = c->stat(2);
+    p.fp_checked = c->stat(3);
+  }
+  p.done_ctr = c->ctr(C_BWD, layer);
+  if (c->order != HPZ_ORDER_OFF)
+    for (int q = 0; q < c->node_size; ++q) p.rel.ptr[p.rel.n++] = c->flag(nf + q, F_BWD_DONE, layer, c->rank);   // E4
+  if (reads_prim)
+    for (int j = 0; j < c->world; ++j) p.rel.ptr[p.rel.n++] = c->flag(j, F_BWDP_DONE, layer, c->rank);
+  p.rel.value = t1;
+  p.sync = c->sync();
+  if (reads_prim) {
+    // the primaries read here must still be W_t: they are, because Adam(t) waits for BWDP_DONE
+    // and the sources' PRIMARY_READY >= t+1 is acquired per source (OFF) or below (EXACT)
+    if (c->order != HPZ_ORDER_OFF) {
+      WaitList w{};
+      for (int j = 0; j < c->world; ++j) w.ptr[w.n++] = c->flag(c->rank, F_PRIM_READY, layer, j);
+      w.target = t1;
+      cudaError_t e = launch_wait(w, c->sync(), s);
+      if (e != cudaSuccess) return fail(c, HPZ_ECUDA, "wait launch: %s", cudaGetErrorString(e));
+      c->launches += 1;
+    }
+  }
+  const int64_t tiles = (p.src_bytes / 16 + 2047) / 2048 * p.n_src;
+  cudaError_t e = launch_gather(p, grid_for(c, tiles, 4), s);
+  if (e != cudaSuccess) return fail(c, HPZ_ECUDA, "bwd gather launch: %s", cudaGetErrorString(e));
+  c->launches += 1;
+  L.bwd_t = c->t;
+  return HPZ_OK;
+}
+
+int hpz_grad_buffer(hpz_ctx* c, int layer, float** slot_ptr, void* stream) {
+  if (int rc = check_ready(c)) return rc;
+  if (int rc = check_layer(c, layer)) return rc;
+  if (int rc = slot_acquire(c, layer, static_cast<cudaStream_t>(stream))) return rc;
+  if (slot_ptr) *slot_ptr = reinterpret_cast<float*>(c->arena[c->rank] + c->off_slot[c->layers[layer].slot]);
+  return HPZ_OK;
+}
+
+int hpz_grad_upload(hpz_ctx* c, int layer, const float* src, int64_t n, void* stream) {
+  float* slot = nullptr;
+  if (int rc = hpz_grad_buffer(c, layer, &slot, stream)) return rc;
+  const Layer& L = c->layers[layer];
+  if (!src || n < 0 || n > L.numel) return fail(c, HPZ_EINVAL, "bad gradient source or length");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  HPZ_CUDA(c, cudaMemcpyAsync(slot, src, (size_t)n * 4, cudaMemcpyDefault, s));
+  if (n < L.numel_pad) HPZ_CUDA(c, cudaMemsetAsync(slot + n, 0, (size_t)(L.numel_pad - n) * 4, s));
+  return HPZ_OK;
+}
+
+int hpz_synth_grads(hpz_ctx* c, int layer, uint64_t key, float scale, int kind, void* stream) {
+  float* slot = nullptr;
+  if (int rc = hpz_grad_buffer(c, layer, &slot, stream)) return rc;
+  if (kind != 0 && kind != 1) return fail(c, HPZ_EINVAL, "bad generator kind");
+  const Layer& L = c->layers[layer];
+  cudaError_t e = launch_synth_f32(slot, L.numel_pad, 0, L.numel, key, scale, kind,
+                                   grid_for(c, (L.numel_pad + 255) / 256, 8), static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return fail(c, HPZ_ECUDA, "synth launch: %s", cudaGetErrorString(e));
+  c->launches += 1;
+  return HPZ_OK;
+}
+
+int hpz_grads_ready(hpz_ctx* c, int layer, void* stream) {
+  if (int rc = check_ready(c)) return rc;
+  if (int rc = check_layer(c, layer)) return rc;
+  const int slot = c->layers[layer].slot;
+  if (c->slot_ready_sent[slot]) return fail(c, HPZ_ESTATE, "grads_ready already published for this use of the slot");
+  cudaError_t e = launch_release(grad_ready_list(c, slot), static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return fail(c, HPZ_ECUDA, "release launch: %s", cudaGetErrorString(e));
+  c->launches += 1;
+  c->slot_ready_sent[slot] = 1;
+  return HPZ_OK;
+}
+
+int hpz_reduce_scatter(hpz_ctx* c, int layer, void* stream) {
+  if (int rc = check_ready(c)) return rc;
+  if (int rc = check_layer(c, layer)) return rc;
+  Layer& L = c->layers[layer];
+  if (L.rs_t == c->t) return fail(c, HPZ_ESTATE, "layer %d already reduce-scattered at step %lld", layer, (long long)c->t);
+  const int slot = L.slot;
+  const uint32_t u1 = epoch(c->slot_use[slot] + 1);
+  RSParams p{};
+  for (int j = 0; j < c->world; ++j)
+    p.src[j] = reinterpret_cast<const float*>(c->arena[j] + c->off_slot[slot]) + (int64_t)c->rank * L.shard;
+  p.out = reinterpret_cast<float*>(c->arena[c->rank] + L.off_gshard);
+  p.n_vec = L.shard / 4;
+  p.inv_p = (float)(1.0 / c->world);
+  if (!c->slot_ready_sent[slot]) p.ready = grad_ready_list(c, slot);   // E5 release
+  for (int j = 0; j < c->world; ++j) p.ready_wait.ptr[p.ready_wait.n++] = c->slot_flag(c->rank, S_GRAD_READY, slot, j);
+  p.ready_wait.target = u1;
+  p.done_ctr = c->ctr(C_RS, c->n_layers + slot);
+  for (int j = 0; j < c->world; ++j) p.rel.ptr[p.rel.n++] = c->slot_flag(j, S_RS_DONE, slot, c->rank);   // E6
+  p.rel.value = u1;
+  p.sync = c->sync();
+  cudaError_t e = launch_reduce_scatter(p, c->world, grid_for(c, (p.n_vec + 511) / 512, 4), static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return fail(c, HPZ_ECUDA, "reduce-scatter launch: %s", cudaGetErrorString(e));
+  c->launches += 1;
+  c->slot_use[slot] += 1;
+  c->slot_ready_sent[slot] = 0;
+  L.rs_t = c->t;
+  return HPZ_OK;
+}
+
+static int step_one(hpz_ctx* c, int layer, const hpz_adam* a, cudaStream_t s) {
+  Layer& L = c->layers[layer];
+  if (L.rs_t != c->t) return fail(c, HPZ_ESTATE, "layer %d: step without its reduce-scatter at step %lld", layer, (long long)c->t);
+  if (L.step_t == c->t) return fail(c, HPZ_ESTATE, "layer %d already stepped at step %lld", layer, (long long)c->t);
+  const int64_t tad = a->step > 0 ? a->step : c->t + 1;    // 1-based Adam count (R24)
+  const double bc1 = 1.0 - std::pow(a->beta1, (double)tad);
+  const double bc2 = 1.0 - std::pow(a->beta2, (double)tad);
+  char* ar = c->arena[c->rank];
+  AdamParams p{};
+  p.w = reinterpret_cast<float*>(ar + L.off_master);
+  p.m = reinterpret_cast<float*>(ar + L.off_m);
+  p.v = reinterpret_cast<float*>(ar + L.off_v);
+  p.g = reinterpret_cast<const float*>(ar + L.off_gshard);
+  p.prim = ar + L.off_primary;
+  p.prim_bf16 = c->dtype == HPZ_BF16;
+  p.n_vec = L.shard / 4;
+  p.beta1 = (float)a->beta1;
+  p.beta2 = (float)a->beta2;
+  p.omb1 = (float)(1.0 - a->beta1);
+  p.omb2 = (float)(1.0 - a->beta2);
+  p.step_size = (float)(a->lr / bc1);
+  p.bc2_sqrt = (float)std::sqrt(bc2);
+  p.eps = (float)a->eps;
+  p.lr_wd = (float)(a->lr * a->weight_decay);
+  const uint32_t t1 = epoch(c->t + 1);
+  for (int j = 0; j < c->world; ++j) p.wait.ptr[p.wait.n++] = c->flag(c->rank, F_FWD_DONE, layer, j);   // E2
+  if (c->order == HPZ_ORDER_OFF || c->verify == HPZ_VERIFY_EXACT)
+    for (int j = 0; j < c->world; ++j) p.wait.ptr[p.wait.n++] = c->flag(c->rank, F_BWDP_DONE, layer, j);
+  p.wait.target = t1;
+  p.done_ctr = c->ctr(C_ADAM, layer);
+  for (int j = 0; j < c->world; ++j) p.rel.ptr[p.rel.n++] = c->flag(j, F_PRIM_READY, layer, c->rank);   // E1
+  p.rel.value = epoch(c->t + 2);
+  p.sync = c->sync();
+  cudaError_t e = launch_adam(p, grid_for(c, (p.n_vec + 511) / 512, 4), s);
+  if (e != cudaSuccess) return fail(c, HPZ_ECUDA, "adam launch: %s", cudaGetErrorString(e));
+  c->launches += 1;
+  L.step_t = c->t;
+  return HPZ_OK;
+}
+
+int hpz_step(hpz_ctx* c, int layer, const hpz_adam* a, void* stream) {
+  if (int rc = check_ready(c)) return rc;
+  if (!a) return fail(c, HPZ_EINVAL, "null adam");
+  if (!(a->lr >= 0) || !(a->beta1 >= 0 && a->beta1 < 1) || !(a->beta2 >= 0 && a->beta2 < 1) || !(a->eps > 0))
+    return fail(c, HPZ_EINVAL, "bad Adam hyper-parameters");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (layer == -1) {
+    for (int i = 0; i < c->n_layers; ++i)
+      if (c->layers[i].rs_t != c->t) return fail(c, HPZ_ESTATE, "layer %d not reduce-scattered at step %lld", i, (long long)c->t);
+    for (int i = 0; i < c->n_layers; ++i)
+      if (int rc = step_one(c, i, a, s)) return rc;
+  } else {
+    if (int rc = check_layer(c, layer)) return rc;
+    if (int rc = step_one(c, layer, a, s)) return rc;
+  }
+  bool all = true;
+  for (int i = 0; i < c->n_layers; ++i) all = all && c->layers[i].step_t == c->t;
+  if (all) c->t += 1;
+  return HPZ_OK;
+}
+
+}  // extern "C"

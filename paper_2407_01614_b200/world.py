@@ -1,0 +1,168 @@
+"""Process/GPU plumbing around libhpz: one context per rank.
+
+Two ways to build a world, both ending in the same C-ABI calls:
+
+* ``DistWorld`` — the production path: one process per GPU (torchrun), every rank
+  allocates its arena in libhpz, exchanges CUDA IPC handles through
+  ``torch.distributed`` (``all_gather_object``; control plane only) and opens its
+  peers' arenas as NVLink mappings.  No data ever moves through torch.distributed.
+* ``EmulatedWorld`` — P ranks as P contexts in ONE process on ONE GPU, arenas bound
+  to each other directly.  Every rank's operation is issued on one stream in SPMD
+  round-robin order, so no kernel ever waits for a kernel that is not already ahead
+  of it in the stream (B200_PROFILING.md: never run mutually-waiting kernels as
+  separate launches on one GPU).  Used by the single-GPU parity tests.
+
+``run_step`` drives one training step of Algorithm 1 for the
+ranks a process owns.
+"""
+from __future__ import annotations
+
+import os
+from dataclasses import dataclass, field
+
+import torch
+
+from . import hpz as H
+from .shapes import PARAM_DTYPE
+
+DTYPES = {"bf16": (H.HPZ_BF16, torch.bfloat16, 2), "f32": (H.HPZ_F32, torch.float32, 4)}
+
+
+@dataclass
+class RankCtx:
+    ctx: object
+    rank: int
+    world: int
+    node_size: int
+    numels: list[int]
+    infos: list = field(default_factory=list)
+
+    def layer(self, i):
+        return self.infos[i]
+
+
+def _register(ctx, numels, dtype, align, n_grad_slots):
+    code = DTYPES[dtype][0]
+    nbytes = H.hpz_register_flat_params(ctx, numels, code, align, n_grad_slots)
+    return nbytes
+
+
+class EmulatedWorld:
+    """P ranks on one GPU in one process (test harness for the multi-rank protocol)."""
+
+    def __init__(self, numels, world, node_size, dtype="bf16", align=256, n_grad_slots=None,
+                 device=0, timeout_s=20.0):
+        self.world, self.node_size, self.dtype = world, node_size, dtype
+        self.numels = list(numels)
+        self.ranks: list[RankCtx] = []
+        for r in range(world):
+            ctx = H.hpz_init(world, node_size, r, device)
+            _register(ctx, self.numels, dtype, align, n_grad_slots)
+            H.hpz_arena_alloc(ctx)
+            H.hpz_set_timeout(ctx, timeout_s)
+            self.ranks.append(RankCtx(ctx, r, world, node_size, self.numels))
+        ptrs = [H.hpz_arena_ptr(rc.ctx, rc.rank) for rc in self.ranks]
+        for rc in self.ranks:
+            H.hpz_bind(rc.ctx, ptrs)
+            rc.infos = [H.hpz_layer_info(rc.ctx, i) for i in range(len(self.numels))]
+        torch.cuda.synchronize()
+
+    def close(self):
+        for rc in self.ranks:
+            H.hpz_finalize(rc.ctx)
+        self.ranks = []
+
+
+class DistWorld:
+    """This process's single rank of a torch.distributed world (one GPU per process)."""
+
+    def __init__(self, numels, node_size, dtype="bf16", align=256, n_grad_slots=None, device=None,
+                 group=None, timeout_s=20.0):
+        import torch.distributed as dist
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.node_size = node_size
+        self.dtype = dtype
+        self.numels = list(numels)
+        dev = torch.cuda.current_device() if device is None else device
+        ctx = H.hpz_init(self.world, node_size, self.rank, dev)
+        self.arena_bytes = _register(ctx, self.numels, dtype, align, n_grad_slots)
+        handle = H.hpz_arena_alloc(ctx)
+        H.hpz_set_timeout(ctx, timeout_s)
+        handles = [None] * self.world
+        dist.all_gather_object(handles, handle, group=group)
+        H.hpz_arena_open(ctx, handles)
+        torch.cuda.synchronize()
+        dist.barrier(group=group)          # every arena's flags are zero before any release
+        rc = RankCtx(ctx, self.rank, self.world, node_size, self.numels)
+        rc.infos = [H.hpz_layer_info(ctx, i) for i in range(len(self.numels))]
+        self.ranks = [rc]
+
+    def close(self):
+        for rc in self.ranks:
+            H.hpz_finalize(rc.ctx)
+        self.ranks = []
+
+
+def full_buffers(world_obj, n_bufs: int = 1, device=None):
+    """Caller-owned full-parameter buffers (N̂_max elements of the param dtype) per rank."""
+    tdt = DTYPES[world_obj.dtype][1]
+    nmax = max(rc.infos[i].numel_pad for rc in world_obj.ranks for i in range(len(rc.numels)))
+    dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+    return [[torch.empty(nmax, dtype=tdt, device=dev) for _ in range(n_bufs)] for _ in world_obj.ranks]
+
+
+def run_step(ranks: list[RankCtx], fwd_out, bwd_out, adam, stream=None, grad_fn=None,
+             emulated: bool = False, layer_hook=None):
+    """One step of Algorithm 1 for the given ranks (all P in emulation, or this process's one).
+
+    fwd_out[r](i) / bwd_out[r](i) return the device pointer of the caller-owned full buffer
+    for rank r, layer i.  grad_fn(rank_ctx, i) fills the rank's gradient slot (or None:
+    gradients already resident).  In emulation every phase is issued for all ranks before
+    the next phase, in the SPMD order of the real world."""
+    L = len(ranks[0].numels)
+    for i in range(L):                                      # forward, i = 1..N
+        for rc in ranks:
+            H.hpz_fwd_gather(rc.ctx, i, fwd_out[rc.rank](i), stream)
+        if layer_hook:
+            layer_hook("fwd", i)
+    for i in reversed(range(L)):                            # backward, i = N..1
+        for rc in ranks:
+            H.hpz_bwd_gather(rc.ctx, i, bwd_out[rc.rank](i), stream)
+        if layer_hook:
+            layer_hook("bwd", i)
+        if grad_fn is not None:
+            for rc in ranks:
+                grad_fn(rc, i)
+        if emulated:
+            for rc in ranks:
+                H.hpz_grads_ready(rc.ctx, i, stream)
+        for rc in ranks:
+            H.hpz_reduce_scatter(rc.ctx, i, stream)
+        if layer_hook:
+            layer_hook("rs", i)
+    for rc in ranks:                                        # optimizer.step()
+        H.hpz_step(rc.ctx, -1, adam, stream)
+
+
+class _CAI:
+    def __init__(self, ptr: int, n: int, typestr: str):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (int(ptr), False),
+                                         "version": 3, "strides": None}
+
+
+def device_view(ptr: int, n: int, dtype: str) -> torch.Tensor:
+    """Zero-copy torch view of n elements at a device address in an arena.
+    dtype: 'f32' -> float32, 'bf16' -> int16 bits viewed as bfloat16, 'u16'/'u32' bit views."""
+    ts = {"f32": "<f4", "bf16": "<i2", "u16": "<i2", "u32": "<i4"}[dtype]
+    t = torch.as_tensor(_CAI(ptr, n, ts), device="cuda")
+    return t.view(torch.bfloat16) if dtype == "bf16" else t
+
+
+def buffer_view(rc: RankCtx, layer: int, kind: str, dtype: str) -> torch.Tensor:
+    ptr, n = H.hpz_buffer(rc.ctx, layer, kind)
+    if kind in ("primary", "secondary") and dtype == "bf16":
+        return device_view(ptr, n, "u16")
+    if kind in ("primary", "secondary"):
+        return device_view(ptr, n, "u32")
+    return device_view(ptr, n, "f32")

@@ -1,0 +1,81 @@
+"""Helpers shared by the -m gpu tests (test infrastructure: may use the oracle)."""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from oracle import hpz_oracle as O
+from synth import inputs as S
+
+
+def gpu_ok() -> bool:
+    return torch.cuda.is_available()
+
+
+def bits_np(t: torch.Tensor, dtype: str) -> np.ndarray:
+    a = t.detach().cpu()
+    if dtype == "bf16":
+        return a.view(torch.int16).numpy().view(np.uint16)
+    return a.view(torch.int32).numpy().view(np.uint32) if a.dtype == torch.float32 else a.numpy().view(np.uint32)
+
+
+def oracle_prim_bits(x: np.ndarray, dtype: str) -> np.ndarray:
+    return O.param_bits(x, dtype)
+
+
+class ParityRun:
+    """Drive an EmulatedWorld and an HpzOracle side by side on the same seeded inputs."""
+
+    def __init__(self, numels, world, node_size, dtype="bf16", align=256, order="fixed",
+                 verify="exact", grad_kind="uniform", n_grad_slots=None, stock_schedule="program"):
+        from paper_2407_01614_b200 import hpz as H
+        from paper_2407_01614_b200.world import EmulatedWorld
+        self.H = H
+        self.numels, self.P, self.Pp, self.dtype = list(numels), world, node_size, dtype
+        self.grad_kind = grad_kind
+        self.w = EmulatedWorld(numels, world, node_size, dtype=dtype, align=align, n_grad_slots=n_grad_slots,
+                               timeout_s=10.0)
+        self.o = O.HpzOracle(self.numels, world, node_size, align=align, param_dtype=dtype, order=order,
+                             stock_schedule=stock_schedule, grad_kind=grad_kind)
+        self.stream = torch.cuda.current_stream()
+        for rc in self.w.ranks:
+            H.hpz_set_order(rc.ctx, order)
+            H.hpz_set_verify(rc.ctx, verify)
+        tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
+        L = len(self.numels)
+        self.fwd = [[torch.zeros(rc.infos[i].numel_pad, dtype=tdt, device="cuda") for i in range(L)] for rc in self.w.ranks]
+        self.bwd = [[torch.zeros(rc.infos[i].numel_pad, dtype=tdt, device="cuda") for i in range(L)] for rc in self.w.ranks]
+        for i, n in enumerate(self.numels):
+            w0 = torch.from_numpy(S.layer_params(i, n)).cuda()
+            for rc in self.w.ranks:
+                H.hpz_load_master(rc.ctx, i, w0.data_ptr(), self.stream)
+        self.adam = H.make_adam()
+        self.t = 0
+
+    def grad_fn(self, rc, i):
+        lay = self.o.layouts[i]
+        g = torch.from_numpy(S.layer_grads(i, self.t, rc.rank, lay.numel, kind=self.grad_kind)).cuda()
+        self.H.hpz_grad_upload(rc.ctx, i, g.data_ptr(), lay.numel, self.stream)
+        self._keep.append(g)
+
+    def step(self):
+        from paper_2407_01614_b200.world import run_step
+        self._keep = []
+        run_step(self.w.ranks, [lambda i, r=r: self.fwd[r][i].data_ptr() for r in range(self.P)],
+                 [lambda i, r=r: self.bwd[r][i].data_ptr() for r in range(self.P)], self.adam,
+                 stream=self.stream, grad_fn=self.grad_fn, emulated=True)
+        torch.cuda.synchronize()
+        rec = self.o.step()
+        self.t += 1
+        return rec
+
+    def counters(self, reset=True):
+        tot = {}
+        for rc in self.w.ranks:
+            c = self.H.hpz_counters(rc.ctx, reset=reset)
+            for k, v in c.items():
+                tot[k] = tot.get(k, 0) + v
+        return tot
+
+    def close(self):
+        self.w.close()

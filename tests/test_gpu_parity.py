@@ -1,0 +1,190 @@
+"""GPU parity: the CUDA path through the C ABI vs the CPU oracle, element by element.
+
+Ranks are emulated in one process on one GPU (paper_2407_01614_b200.world.EmulatedWorld),
+so every (P, P') of BASELINE.json's sweep is covered on a single B200; the real
+multi-process NVLink path is covered by tests/test_gpu_multiproc.py when >= 2 GPUs exist.
+Bars (north_star): gathers, secondaries, shard indexing and the fp32 reduce-scatter
+bit-exact; Adam within 1e-6 relative (the kernel matches the oracle's op sequence, so
+the test asserts bit-exactness and reports the max relative error on failure).
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle import hpz_oracle as O
+from synth import inputs as S
+
+from .gpu_util import ParityRun, bits_np, gpu_ok
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not gpu_ok(), reason="needs a GPU")]
+
+# several 32 KiB gather tiles per shard plus ragged tails; one layer smaller than P*A
+NUMELS = [300_007, 65_536, 4_099, 77]
+TOPOS = [(1, 1), (2, 1), (2, 2), (4, 1), (4, 2), (4, 4), (8, 1), (8, 2), (8, 4), (8, 8)]
+
+
+def _check_step(run: ParityRun, rec, check_all=True):
+    P, dtype = run.P, run.dtype
+    for i, lay in enumerate(run.o.layouts):
+        W = O.param_bits(rec.W[i], dtype)
+        for r, rc in enumerate(run.w.ranks):
+            # a2: forward gather == W_t bitwise (incl. zero padding)
+            assert np.array_equal(bits_np(run.fwd[r][i], dtype), W), f"fwd layer {i} rank {r}"
+            # a4: backward gather == W_t bitwise
+            assert np.array_equal(bits_np(run.bwd[r][i], dtype), W), f"bwd layer {i} rank {r}"
+        if not check_all:
+            continue
+        from paper_2407_01614_b200.world import buffer_view
+        grads = [S.layer_grads(i, run.t - 1, j, lay.numel, lay.numel_pad, kind=run.grad_kind) for j in range(P)]
+        for r, rc in enumerate(run.w.ranks):
+            st = run.o.state[i][r]
+            # a2 secondary store == oracle's Eq. (1) slice
+            if run.o.order == "fixed":
+                sec = bits_np(buffer_view(rc, i, "secondary", dtype), dtype)
+                assert np.array_equal(sec, O.param_bits(st.sec, dtype)), f"secondary layer {i} rank {r}"
+            # a5 reduce-scatter bit-exact in the fixed order
+            g_gpu = buffer_view(rc, i, "grad_shard", "f32").cpu().numpy()
+            g_ref = O.reduce_scatter(grads, lay, r)
+            assert np.array_equal(g_gpu.view(np.uint32), g_ref.view(np.uint32)), f"RS layer {i} rank {r}"
+            # a6 Adam + bf16 refresh
+            for kind, ref in (("master", st.master), ("m", st.m), ("v", st.v)):
+                got = buffer_view(rc, i, kind, "f32").cpu().numpy()
+                if not np.array_equal(got.view(np.uint32), ref.view(np.uint32)):
+                    rel = np.max(np.abs(got - ref) / np.maximum(np.abs(ref), 1e-30))
+                    pytest.fail(f"{kind} layer {i} rank {r}: max rel err {rel:.3g}")
+            prim = bits_np(buffer_view(rc, i, "primary", dtype), dtype)
+            assert np.array_equal(prim, O.param_bits(st.prim, dtype)), f"primary layer {i} rank {r}"
+
+
+@pytest.mark.parametrize("P,Pp", TOPOS)
+def test_parity_fixed(P, Pp):
+    run = ParityRun(NUMELS, P, Pp)
+    try:
+        for _ in range(3):
+            rec = run.step()
+            _check_step(run, rec)
+        c = run.counters()
+        assert c["mismatches"] == 0 and c["nan_reads"] == 0 and c["timeouts"] == 0
+        assert c["fp_mismatches"] == 0 and c["fp_checked"] == 3 * len(NUMELS) * P
+    finally:
+        run.close()
+
+
+@pytest.mark.parametrize("P,Pp", [(8, 4), (4, 2)])
+def test_parity_off_equals_fixed(P, Pp):
+    """ORDER_OFF (plain ZeRO-3 backward over P) gives the same bits (PAPER.md:207 / SPEC.md:352)."""
+    run = ParityRun(NUMELS, P, Pp, order="off")
+    try:
+        for _ in range(2):
+            _check_step(run, run.step())
+        assert run.counters()["mismatches"] == 0
+    finally:
+        run.close()
+
+
+def test_parity_fp32_params_toy_shapes():
+    """Config C1 shapes with fp32 parameters (primary == master copy)."""
+    run = ParityRun(O.toy_layer_numels(), 8, 4, dtype="f32")
+    try:
+        for _ in range(2):
+            _check_step(run, run.step())
+    finally:
+        run.close()
+
+
+def test_parity_dyadic_rs_closed_form():
+    """Dyadic gradients: the GPU reduce-scatter equals the exact rational mean."""
+    run = ParityRun([40_000], 8, 2, grad_kind="dyadic")
+    try:
+        rec = run.step()
+        _check_step(run, rec)
+    finally:
+        run.close()
+
+
+def test_parity_shared_grad_slots():
+    """Fewer gradient slots than layers: the E6 wait orders slot reuse."""
+    run = ParityRun(NUMELS, 4, 2, n_grad_slots=2)
+    try:
+        for _ in range(2):
+            _check_step(run, run.step())
+    finally:
+        run.close()
+
+
+def test_synth_generator_matches_host():
+    """The device twin of synth/inputs.py produces the same fp32 bits."""
+    from paper_2407_01614_b200 import hpz as H
+    from paper_2407_01614_b200.world import EmulatedWorld, buffer_view
+    n = 123_457
+    w = EmulatedWorld([n], 2, 1)
+    try:
+        s = torch.cuda.current_stream()
+        for rc in w.ranks:
+            H.hpz_synth_master(rc.ctx, 0, S.stream_key(S.SEED_PARAMS, 0, 0, 0), S.PARAM_SCALE, s)
+            H.hpz_synth_grads(rc.ctx, 0, S.stream_key(S.SEED_GRADS, 0, 5, rc.rank), S.GRAD_SCALE, 0, s)
+        torch.cuda.synchronize()
+        full = S.layer_params(0, n, w.ranks[0].infos[0].numel_pad)
+        for rc in w.ranks:
+            info = rc.infos[0]
+            m = buffer_view(rc, 0, "master", "f32").cpu().numpy()
+            assert np.array_equal(m.view(np.uint32), full[rc.rank * info.shard:(rc.rank + 1) * info.shard].view(np.uint32))
+            g = buffer_view(rc, 0, "grad_slot", "f32").cpu().numpy()
+            ref = S.layer_grads(0, 5, rc.rank, n, info.numel_pad)
+            assert np.array_equal(g.view(np.uint32), ref.view(np.uint32))
+            # bf16 primary = RNE(master)
+            p = bits_np(buffer_view(rc, 0, "primary", "bf16"), "bf16")
+            assert np.array_equal(p, O.bf16_rne(m))
+    finally:
+        w.close()
+
+
+def test_stock_ordering_shows_stale_reads():
+    """Negative control (Table 1 ×): stock ordering with a delayed,
+    poisoned side-stream secondary copy makes backward gathers read stale or NaN
+    weights; the exact detector counts them (> 0; the count itself is a hardware race)."""
+    from paper_2407_01614_b200 import hpz as H
+    run = ParityRun(NUMELS, 8, 4, order="stock", verify="exact")
+    try:
+        for rc in run.w.ranks:
+            H.hpz_set_order(rc.ctx, "stock", stock_delay_us=2000, stock_poison=True)
+        for _ in range(3):
+            run.step()
+        c = run.counters()
+        assert c["mismatches"] > 0
+        assert c["timeouts"] == 0
+    finally:
+        run.close()
+
+
+def test_api_errors():
+    from paper_2407_01614_b200 import hpz as H
+    with pytest.raises(H.HpzError) as e:
+        H.hpz_init(8, 3, 0, 0)
+    assert e.value.code == H.HPZ_EINVAL
+    ctx = H.hpz_init(2, 2, 0, 0)
+    try:
+        with pytest.raises(H.HpzError) as e:
+            H.hpz_fwd_gather(ctx, 0, 0)
+        assert e.value.code == H.HPZ_ESTATE
+        H.hpz_register_flat_params(ctx, [1000])
+        with pytest.raises(H.HpzError) as e:
+            H.hpz_register_flat_params(ctx, [1000])
+        assert e.value.code == H.HPZ_ESTATE
+    finally:
+        H.hpz_finalize(ctx)
+    from paper_2407_01614_b200.world import EmulatedWorld
+    w = EmulatedWorld([5000], 2, 2)
+    try:
+        buf = torch.empty(w.ranks[0].infos[0].numel_pad, dtype=torch.bfloat16, device="cuda")
+        with pytest.raises(H.HpzError) as e:   # backward before forward
+            H.hpz_bwd_gather(w.ranks[0].ctx, 0, buf.data_ptr())
+        assert e.value.code == H.HPZ_ESTATE
+        with pytest.raises(H.HpzError) as e:   # misaligned output
+            H.hpz_fwd_gather(w.ranks[0].ctx, 0, buf.data_ptr() + 2)
+        assert e.value.code == H.HPZ_EINVAL
+        with pytest.raises(H.HpzError) as e:   # step before reduce-scatter
+            H.hpz_step(w.ranks[0].ctx, 0, H.make_adam())
+        assert e.value.code == H.HPZ_ESTATE
+    finally:
+        w.close()
