@@ -1,0 +1,482 @@
+#!/usr/bin/env python
+"""Benchmark of the hpZ hot path (arXiv 2407.01614, Algorithm 1) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--model falcon7b] [--impl hpz|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+One step = one pass of the whole hot path over the model's flat layer buffers:
+forward gather (+ fused secondary write) of every layer, backward gather +
+reduce-scatter of every layer in reverse order, partitioned Adam of every layer
+(DESIGN.md §7).  Inputs (parameters, optimizer state, gradients) are resident in HBM
+before the timed region; gradients are synthetic (the model's backward compute is out
+of scope).  The N GPUs form a world of P = N ranks split into 2 virtual nodes of
+P' = N/2 (P' = 1 at N = 1).
+
+Rank 0 prints ONE JSON line.  `value` = whole-job gather+reduce-scatter bandwidth:
+Σ over ranks of the collectives' algorithmic bytes (AllGather output bytes of the
+forward and backward gathers + ReduceScatter input bytes, the nccl-tests "algbw"
+convention) ÷ the max over ranks of the collectives' device time per step.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "hpZ gather+reduce-scatter NVLink GB/s per step; stale-param mismatches (must be 0)"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=None)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--model", default="falcon7b")
+    ap.add_argument("--node-size", type=int, default=None)
+    ap.add_argument("--impl", default="hpz", choices=["hpz", "reference"])
+    ap.add_argument("--order", default="fixed", choices=["fixed", "stock", "off"])
+    ap.add_argument("--verify", default="fingerprint", choices=["none", "fingerprint", "exact"])
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-nccl", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle sample time")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------- helpers
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpus):
+        self.gpus = gpus
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                       "-lms", "200", "-i", ",".join(str(g) for g in self.gpus)],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        time.sleep(0.25)
+        self.p.terminate()
+        try:
+            out, _ = self.p.communicate(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.p.kill()
+            out, _ = self.p.communicate()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+def ncu_traffic():
+    """Per-element DRAM traffic of each kernel from a committed `ncu --set full` capture
+    (profiles/ncu_traffic.json), or {}."""
+    try:
+        return json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+    except Exception:
+        return {}
+
+
+def host_cores():
+    return os.cpu_count()
+
+
+# ----------------------------------------------------------------------------- oracle legs
+def oracle_sample(world, node_size, dtype, target_s):
+    """Time the CPU oracle (as it stands) on a bounded sample of the workload: one flat
+    layer of S elements, all P ranks simulated, one full step (both gathers, RS, Adam).
+    S is grown until a step takes >= target_s/4, then one more timed step is run.
+    Returns (GB/s by the same byte accounting, seconds, S)."""
+    from oracle import hpz_oracle as O
+    e = 2 if dtype == "bf16" else 4
+    S = 1 << 18
+    while True:
+        o = O.HpzOracle([S], world, node_size, align=256, param_dtype=dtype)
+        t0 = time.perf_counter()
+        o.step()
+        dt = time.perf_counter() - t0
+        if dt >= target_s / 4 or S >= (1 << 27):
+            break
+        S = int(S * min(8.0, max(2.0, (target_s / 4) / max(dt, 1e-3))))
+    lay = o.layouts[0]
+    t0 = time.perf_counter()
+    o.step()
+    dt = time.perf_counter() - t0
+    bytes_ = world * (2 * lay.numel_pad * e + 4 * lay.numel_pad)
+    return bytes_ / dt / 1e9, dt, S
+
+
+# ----------------------------------------------------------------------------- main arm
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    n_gpus = args.gpus if args.gpus is not None else world
+    if n_gpus != world:
+        if world == 1 and n_gpus > 1:
+            sys.exit(f"--gpus {n_gpus} needs torchrun --nproc-per-node {n_gpus}")
+    node_size = args.node_size or (world // 2 if world >= 2 else 1)
+
+    if args.impl == "reference":
+        return reference_arm(args, world, rank, node_size)
+
+    import torch
+    import torch.distributed as dist
+    from paper_2407_01614_b200 import hpz as H
+    from paper_2407_01614_b200 import shapes
+    from paper_2407_01614_b200.world import DistWorld, EmulatedWorld
+    from synth import inputs as S
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    numels = shapes.numels(args.model)
+    dtype = shapes.PARAM_DTYPE.get(args.model, "bf16")
+    e = 2 if dtype == "bf16" else 4
+    L = len(numels)
+
+    if world > 1:
+        W = DistWorld(numels, node_size, dtype=dtype, n_grad_slots=L, device=local_rank, timeout_s=60.0)
+    else:
+        W = EmulatedWorld(numels, 1, 1, dtype=dtype, n_grad_slots=L, device=local_rank, timeout_s=60.0)
+    rc = W.ranks[0]
+    ctx = rc.ctx
+    H.hpz_set_order(ctx, args.order)
+    H.hpz_set_verify(ctx, args.verify)
+    stream = torch.cuda.current_stream()
+    infos = rc.infos
+    # resident inputs: initial params (device generator) and this rank's gradients
+    for i in range(L):
+        H.hpz_synth_master(ctx, i, S.stream_key(S.SEED_PARAMS, i, 0, 0), S.PARAM_SCALE, stream)
+        H.hpz_synth_grads(ctx, i, S.stream_key(S.SEED_GRADS, i, 0, rank), S.GRAD_SCALE, 0, stream)
+    tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    nmax = max(x.numel_pad for x in infos)
+    fwd_buf = torch.empty(nmax, dtype=tdt, device=dev)     # caller-owned full buffers, reused
+    bwd_buf = torch.empty(nmax, dtype=tdt, device=dev)     # per layer (repartition)
+    adam = H.make_adam()
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def one_step(ev=None, grads_from=None):
+        """ev: dict of per-call event lists (or None).  grads_from: pinned host buffer
+        uploaded into every layer's gradient slot (end-to-end arm)."""
+        def rec(k):
+            if ev is not None:
+                x = torch.cuda.Event(enable_timing=True)
+                x.record(stream)
+                ev[k].append(x)
+        for i in range(L):
+            rec("fwd0")
+            H.hpz_fwd_gather(ctx, i, fwd_buf.data_ptr(), stream)
+            rec("fwd1")
+        for i in reversed(range(L)):
+            rec("bwd0")
+            H.hpz_bwd_gather(ctx, i, bwd_buf.data_ptr(), stream)
+            rec("bwd1")
+            if grads_from is not None:
+                H.hpz_grad_upload(ctx, i, grads_from.data_ptr(), infos[i].numel, stream)
+            rec("rs0")
+            H.hpz_reduce_scatter(ctx, i, stream)
+            rec("rs1")
+        for i in range(L):
+            rec("adam0")
+            H.hpz_step(ctx, i, adam, stream)
+            rec("adam1")
+
+    for _ in range(args.warmup):
+        one_step()
+    H.hpz_counters(ctx, reset=True)
+    launches0 = H.hpz_counters(ctx)["launches"]
+    clocks = ClockSampler(list(range(world)) if rank == 0 else [])
+    barrier()
+    if rank == 0:
+        clocks.start()
+    evs = {k: [] for k in ("fwd0", "fwd1", "bwd0", "bwd1", "rs0", "rs1", "adam0", "adam1")}
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    t_start.record(stream)
+    for _ in range(args.steps):
+        one_step(evs)
+    t_end.record(stream)
+    barrier()
+    clk = clocks.stop() if rank == 0 else None
+    cnt = H.hpz_counters(ctx)
+    launches = cnt["launches"] - launches0
+
+    K = args.steps
+    step_ms = t_start.elapsed_time(t_end) / K
+    tot = {k: sum(a.elapsed_time(b) for a, b in zip(evs[k + "0"], evs[k + "1"])) / K
+           for k in ("fwd", "bwd", "rs", "adam")}
+    # bytes per rank per step (algbw: AG output bytes, RS input bytes)
+    ag_bytes = sum(x.numel_pad for x in infos) * e
+    rs_bytes = sum(x.numel_pad for x in infos) * 4
+    coll_bytes = 2 * ag_bytes + rs_bytes
+    # NVLink ingress per rank per step (busbw convention)
+    P, Pp = world, node_size
+    ingress = ag_bytes * (P - 1) / P + ag_bytes * (Pp - 1) / Pp + rs_bytes * (P - 1) / P
+    adam_bytes = sum(x.shard for x in infos) * (30 if dtype == "bf16" else 32)
+
+    vals = torch.tensor([step_ms, tot["fwd"], tot["bwd"], tot["rs"], tot["adam"],
+                         tot["fwd"] + tot["bwd"] + tot["rs"]], dtype=torch.float64, device=dev)
+    stats = torch.tensor([cnt["fp_mismatches"], cnt["mismatches"], cnt["nan_reads"], cnt["timeouts"],
+                          cnt["fp_checked"], launches], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(vals, op=dist.ReduceOp.MAX)
+        dist.all_reduce(stats, op=dist.ReduceOp.SUM)
+    vals = vals.tolist()
+    stats = stats.tolist()
+    step_ms, fwd_ms, bwd_ms, rs_ms, adam_ms, coll_ms = vals
+    value = world * coll_bytes / (coll_ms * 1e-3) / 1e9
+
+    # ------------------------------------------------ roofline of the dominant kernel
+    pk = peaks()
+    hbm_peak = pk.get("hbm_gbs", 6650.0)
+    share = {"fwd_gather": fwd_ms, "bwd_gather": bwd_ms, "reduce_scatter": rs_ms, "adam": adam_ms}
+    dom = max(share, key=share.get)
+    if world == 1:
+        hbm_alg = {"fwd_gather": 3 * ag_bytes,     # read primary, write full out + secondary (P'=1)
+                   "bwd_gather": 2 * ag_bytes, "reduce_scatter": 2 * rs_bytes, "adam": adam_bytes}
+        alg = hbm_alg[dom]
+        bound, peak, unit = "hbm", hbm_peak, "GB/s"
+    else:
+        nv_alg = {"fwd_gather": ag_bytes * (P - 1) / P, "bwd_gather": ag_bytes * (Pp - 1) / Pp,
+                  "reduce_scatter": rs_bytes * (P - 1) / P, "adam": adam_bytes}
+        alg = nv_alg[dom]
+        if dom == "adam":
+            bound, peak, unit = "hbm", hbm_peak, "GB/s"
+        else:
+            bound, peak, unit = "nvlink", 770.0, "GB/s"
+    achieved = alg / (share[dom] * 1e-3) / 1e9          # per-launch bytes / per-launch time, summed over L launches
+    traffic = None
+    tr = ncu_traffic().get(f"{args.model}_P{world}_{dom}")
+    if tr:
+        traffic = tr.get("dram_bytes_per_launch")
+    roofline = {"bound": bound, "kernel": dom, "achieved": round(achieved, 1), "peak": peak, "unit": unit,
+                "frac": round(achieved / peak, 4), "traffic": traffic,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if bound == "hbm" else
+                "B200_PROFILING.md measured peer copy 770 GB/s per direction (900 nominal)",
+                "alg_bytes_per_step": alg, "launches_per_step": L, "ms_per_step": round(share[dom], 4),
+                "share_of_step": round(share[dom] / step_ms, 4)}
+
+    # ------------------------------------------------ end-to-end arm (host buffers)
+    e2e = None
+    if not args.no_e2e and args.e2e_steps > 0:
+        host = torch.empty(max(x.numel for x in infos), dtype=torch.float32, pin_memory=True)
+        H.hpz_synth_grads(ctx, 0, S.stream_key(S.SEED_GRADS, 0, 0, rank), S.GRAD_SCALE, 0, stream)
+        # fill the pinned buffer with this rank's synthetic gradient values (device generator)
+        from paper_2407_01614_b200.world import buffer_view
+        src = buffer_view(rc, 0, "grad_slot", "f32")
+        host[: infos[0].numel].copy_(src[: infos[0].numel])
+        one_step(grads_from=host)          # warm-up of the e2e path
+        barrier()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(args.e2e_steps):
+            one_step(grads_from=host)
+            res = torch.empty(6, dtype=torch.int64)   # the step's result: detection counters, D2H
+            c = H.hpz_counters(ctx)
+            res[:] = torch.tensor([c["fp_mismatches"], c["mismatches"], c["nan_reads"], c["timeouts"],
+                                   c["fp_checked"], c["launches"]])
+        b.record(stream)
+        barrier()
+        e2e_ms = torch.tensor([a.elapsed_time(b) / args.e2e_steps], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
+        e2e_ms = e2e_ms.item()
+        e2e = {"value": round(world * coll_bytes / (e2e_ms * 1e-3) / 1e9, 2), "unit": "GB/s",
+               "h2d_bytes_per_step": sum(x.numel for x in infos) * 4, "d2h_bytes_per_step": 5 * 8,
+               "ms_per_step": round(e2e_ms, 3),
+               "note": "through the C ABI: every layer's fp32 gradient uploaded from pinned host memory "
+                       "(hpz_grad_upload) inside the timed step; counters read back (hpz_counters)"}
+
+    # ------------------------------------------------ NCCL baseline (same collectives, same sizes)
+    nccl = None
+    if world > 1 and not args.no_nccl:
+        nccl = nccl_baseline(infos, e, node_size, dev, tdt, args)
+
+    W.close()
+    if rank == 0:
+        cpu = None
+        if not args.no_cpu_baseline:
+            gbs, dt, Ssz = oracle_sample(world, node_size, dtype, args.cpu_seconds)
+            cpu = {"value": round(gbs, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
+                   "sample": f"oracle/hpz_oracle.py HpzOracle: one step (fwd gather+secondary, bwd gather, "
+                             f"RS, Adam) of ONE flat layer of {Ssz} elements, all {world} rank(s) simulated "
+                             f"(P={world}, P'={node_size}), {dt:.2f} s; same algbw byte accounting; numpy, "
+                             f"single thread (host has {host_cores()} cores)"}
+        out = {
+            "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world,
+            "steps": K, "warmup": args.warmup, "ms_per_step": round(step_ms, 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "bf16 gathers / f32 reduce-scatter+Adam", "data": "synthetic",
+            "config": {"workload": f"{args.model}-shaped flat parameter buffers ({L} layers, "
+                                   f"{sum(x.numel for x in infos)} params), bf16 params + fp32 master/Adam",
+                       "world": world, "node_size": node_size, "virtual_nodes": world // node_size,
+                       "parallelism": f"hpZ dp{world} (P={world}, P'={node_size})", "order": args.order,
+                       "verify": args.verify,
+                       "l2": "no flush: per-step working set >> 126 MB L2 (every layer buffer is "
+                             "touched once per phase)",
+                       "value_def": "sum over ranks of AllGather output bytes (fwd+bwd) + ReduceScatter "
+                                    "input bytes, / max-over-ranks collective device time per step (algbw)"},
+            "stale_param_mismatches": {"fingerprint_layers": int(stats[0]), "exact_elements": int(stats[1]),
+                                       "nan_reads": int(stats[2]), "timeouts": int(stats[3]),
+                                       "layers_checked": int(stats[4])},
+            "breakdown_ms_per_step": {"fwd_gather": round(fwd_ms, 3), "bwd_gather": round(bwd_ms, 3),
+                                      "reduce_scatter": round(rs_ms, 3), "adam": round(adam_ms, 3),
+                                      "collectives": round(coll_ms, 3)},
+            "nvlink_ingress_GBps_per_gpu": round(ingress / (coll_ms * 1e-3) / 1e9, 2) if world > 1 else None,
+            "nvlink_frac_of_900": round(ingress / (coll_ms * 1e-3) / 1e9 / 900, 4) if world > 1 else None,
+            "step_GBps_incl_adam": round(world * coll_bytes / (step_ms * 1e-3) / 1e9, 2),
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "nccl_baseline": nccl,
+            "e2e": e2e,
+            "gpu_launches": int(stats[5]),
+            "clocks": clk,
+        }
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def nccl_baseline(infos, e, node_size, dev, tdt, args):
+    """NCCL (torch.distributed, NCCL 2.28) on the same message sizes: AllGather over P into
+    a full buffer + copy of the secondary slice; AllGather over the virtual-node group;
+    fp32 ReduceScatter(AVG).  Timed with CUDA events, max over ranks."""
+    import torch
+    import torch.distributed as dist
+    P = dist.get_world_size()
+    r = dist.get_rank()
+    groups = [dist.new_group(list(range(n * node_size, (n + 1) * node_size))) for n in range(P // node_size)]
+    my_group = groups[r // node_size]
+    nmax = max(x.numel_pad for x in infos)
+    smax = max(x.shard for x in infos)
+    full = torch.empty(nmax, dtype=tdt, device=dev)
+    prim = torch.ones(smax, dtype=tdt, device=dev)
+    sec = torch.empty(nmax // node_size, dtype=tdt, device=dev)
+    grad = torch.ones(nmax, dtype=torch.float32, device=dev)
+    gsh = torch.empty(smax, dtype=torch.float32, device=dev)
+    l = r % node_size
+
+    def step(ev=None):
+        t = {"fwd": 0.0, "bwd": 0.0, "rs": 0.0}
+        marks = []
+        for x in infos:
+            a = torch.cuda.Event(enable_timing=True); a.record()
+            dist.all_gather_into_tensor(full[: x.numel_pad], prim[: x.shard])
+            sec[: x.sec_shard].copy_(full[l * x.sec_shard:(l + 1) * x.sec_shard])
+            b = torch.cuda.Event(enable_timing=True); b.record()
+            marks.append(("fwd", a, b))
+        for x in reversed(infos):
+            a = torch.cuda.Event(enable_timing=True); a.record()
+            dist.all_gather_into_tensor(full[: x.numel_pad], sec[: x.sec_shard], group=my_group)
+            b = torch.cuda.Event(enable_timing=True); b.record()
+            dist.reduce_scatter_tensor(gsh[: x.shard], grad[: x.numel_pad], op=dist.ReduceOp.AVG)
+            c = torch.cuda.Event(enable_timing=True); c.record()
+            marks.append(("bwd", a, b))
+            marks.append(("rs", b, c))
+        return marks
+
+    for _ in range(2):
+        step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    K = max(1, min(args.steps, 5))
+    allm = []
+    for _ in range(K):
+        allm += step()
+    torch.cuda.synchronize()
+    t = {"fwd": 0.0, "bwd": 0.0, "rs": 0.0}
+    for k, a, b in allm:
+        t[k] += a.elapsed_time(b) / K
+    v = torch.tensor([t["fwd"], t["bwd"], t["rs"]], dtype=torch.float64, device=dev)
+    dist.all_reduce(v, op=dist.ReduceOp.MAX)
+    fwd, bwd, rs = v.tolist()
+    ag = sum(x.numel_pad for x in infos) * e
+    rsb = sum(x.numel_pad for x in infos) * 4
+    coll = fwd + bwd + rs
+    return {"value": round(P * (2 * ag + rsb) / (coll * 1e-3) / 1e9, 2), "unit": "GB/s",
+            "ms_per_step": {"fwd_gather+copy": round(fwd, 3), "bwd_gather": round(bwd, 3),
+                            "reduce_scatter": round(rs, 3)},
+            "steps": K, "impl": f"torch.distributed NCCL {'.'.join(map(str, torch.cuda.nccl.version()))}"}
+
+
+def reference_arm(args, world, rank, node_size):
+    """--impl reference: the CPU oracle as it stands, on this arm's config/metric/unit, each
+    step a bounded sample of the workload.  Under torchrun only rank 0 runs."""
+    if rank != 0:
+        return
+    from paper_2407_01614_b200 import shapes
+    dtype = shapes.PARAM_DTYPE.get(args.model, "bf16")
+    target = max(2.0, min(args.cpu_seconds, 60.0 / max(1, args.steps + args.warmup)))
+    vals = []
+    Ssz = dt = None
+    for k in range(args.warmup + args.steps):
+        gbs, dt, Ssz = oracle_sample(world, node_size, dtype, target)
+        if k >= args.warmup:
+            vals.append((gbs, dt))
+    value = statistics.median(v for v, _ in vals)
+    ms = statistics.median(d for _, d in vals) * 1e3
+    sample = (f"oracle/hpz_oracle.py HpzOracle: one step of ONE flat layer of {Ssz} elements, all {world} "
+              f"rank(s) simulated (P={world}, P'={node_size}); numpy single thread")
+    out = {"metric": METRIC, "value": round(value, 4), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": round(ms, 1), "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "bf16 gathers / f32 reduce-scatter+Adam", "data": "synthetic",
+           "impl": "reference",
+           "config": {"workload": f"{args.model}-shaped flat parameter buffers (bounded per-step sample)",
+                      "world": world, "node_size": node_size},
+           "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "kind": "oracle", "cores": 1, "sample": sample},
+           "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()
