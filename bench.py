@@ -165,7 +165,7 @@ def main():
     import torch.distributed as dist
     from paper_2407_01614_b200 import hpz as H
     from paper_2407_01614_b200 import shapes
-    from paper_2407_01614_b200.world import DistWorld, EmulatedWorld
+    from paper_2407_01614_b200.world import DistWorld, EmulatedWorld, max_over_ranks, sum_over_ranks
     from synth import inputs as S
 
     torch.cuda.set_device(local_rank)
@@ -262,15 +262,10 @@ def main():
     ingress = ag_bytes * (P - 1) / P + ag_bytes * (Pp - 1) / Pp + rs_bytes * (P - 1) / P
     adam_bytes = sum(x.shard for x in infos) * (30 if dtype == "bf16" else 32)
 
-    vals = torch.tensor([step_ms, tot["fwd"], tot["bwd"], tot["rs"], tot["adam"],
-                         tot["fwd"] + tot["bwd"] + tot["rs"]], dtype=torch.float64, device=dev)
-    stats = torch.tensor([cnt["fp_mismatches"], cnt["mismatches"], cnt["nan_reads"], cnt["timeouts"],
-                          cnt["fp_checked"], launches], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(vals, op=dist.ReduceOp.MAX)
-        dist.all_reduce(stats, op=dist.ReduceOp.SUM)
-    vals = vals.tolist()
-    stats = stats.tolist()
+    vals = max_over_ranks([step_ms, tot["fwd"], tot["bwd"], tot["rs"], tot["adam"],
+                           tot["fwd"] + tot["bwd"] + tot["rs"]], device=dev)
+    stats = sum_over_ranks([cnt["fp_mismatches"], cnt["mismatches"], cnt["nan_reads"], cnt["timeouts"],
+                            cnt["fp_checked"], launches], device=dev)
     step_ms, fwd_ms, bwd_ms, rs_ms, adam_ms, coll_ms = vals
     value = world * coll_bytes / (coll_ms * 1e-3) / 1e9
 
@@ -326,10 +321,7 @@ def main():
                                    c["fp_checked"], c["launches"]])
         b.record(stream)
         barrier()
-        e2e_ms = torch.tensor([a.elapsed_time(b) / args.e2e_steps], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
-        e2e_ms = e2e_ms.item()
+        e2e_ms = max_over_ranks([a.elapsed_time(b) / args.e2e_steps], device=dev)[0]
         e2e = {"value": round(world * coll_bytes / (e2e_ms * 1e-3) / 1e9, 2), "unit": "GB/s",
                "h2d_bytes_per_step": sum(x.numel for x in infos) * 4, "d2h_bytes_per_step": 5 * 8,
                "ms_per_step": round(e2e_ms, 3),
@@ -395,7 +387,8 @@ def nccl_baseline(infos, e, node_size, dev, tdt, args):
     import torch.distributed as dist
     P = dist.get_world_size()
     r = dist.get_rank()
-    groups = [dist.new_group(list(range(n * node_size, (n + 1) * node_size))) for n in range(P // node_size)]
+    from paper_2407_01614_b200.world import virtual_nodes
+    groups = [dist.new_group(g) for g in virtual_nodes(P, node_size)]
     my_group = groups[r // node_size]
     nmax = max(x.numel_pad for x in infos)
     smax = max(x.shard for x in infos)

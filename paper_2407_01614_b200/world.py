@@ -41,6 +41,42 @@ class RankCtx:
         return self.infos[i]
 
 
+def virtual_nodes(world: int, node_size: int) -> list[list[int]]:
+    """Consecutive ranks form a virtual node (readings R3/R4): 2x4 = [[0..3], [4..7]]."""
+    if world < 1 or node_size < 1 or world % node_size:
+        raise ValueError(f"node_size {node_size} must divide world {world}")
+    return [list(range(n * node_size, (n + 1) * node_size)) for n in range(world // node_size)]
+
+
+def exchange_handles(handle: bytes, group=None) -> list[bytes]:
+    """All ranks' CUDA IPC handles in rank order (control plane only; works on gloo or nccl)."""
+    import torch.distributed as dist
+    handles = [None] * dist.get_world_size(group)
+    dist.all_gather_object(handles, handle, group=group)
+    if any(not isinstance(h, (bytes, bytearray)) or len(h) != H.IPC_HANDLE_BYTES for h in handles):
+        raise RuntimeError("malformed IPC handle from a peer")
+    return [bytes(h) for h in handles]
+
+
+def max_over_ranks(values: list[float], device=None) -> list[float]:
+    """Element-wise max over all ranks (timing rule: max over ranks); identity without a PG."""
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return list(values)
+    t = torch.tensor(values, dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return t.tolist()
+
+
+def sum_over_ranks(values: list[float], device=None) -> list[float]:
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return list(values)
+    t = torch.tensor(values, dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return t.tolist()
+
+
 def _register(ctx, numels, dtype, align, n_grad_slots):
     code = DTYPES[dtype][0]
     nbytes = H.hpz_register_flat_params(ctx, numels, code, align, n_grad_slots)
@@ -89,9 +125,8 @@ class DistWorld:
         self.arena_bytes = _register(ctx, self.numels, dtype, align, n_grad_slots)
         handle = H.hpz_arena_alloc(ctx)
         H.hpz_set_timeout(ctx, timeout_s)
-        handles = [None] * self.world
-        dist.all_gather_object(handles, handle, group=group)
-        H.hpz_arena_open(ctx, handles)
+        virtual_nodes(self.world, node_size)         # validates the topology early
+        H.hpz_arena_open(ctx, exchange_handles(handle, group))
         torch.cuda.synchronize()
         dist.barrier(group=group)          # every arena's flags are zero before any release
         rc = RankCtx(ctx, self.rank, self.world, node_size, self.numels)

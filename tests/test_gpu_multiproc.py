@@ -1,0 +1,39 @@
+"""Real multi-process path: one process per GPU, CUDA IPC peer mappings, NVLink P2P
+pulls and cross-GPU release/acquire flags, checked against the oracle (tests/mp_worker.py).
+Skipped unless the box has >= 2 GPUs (gpurun --gpus 2|4)."""
+import os
+import subprocess
+import sys
+
+import pytest
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+NGPU = torch.cuda.device_count() if torch.cuda.is_available() else 0
+
+pytestmark = [pytest.mark.gpu, pytest.mark.multigpu,
+              pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")]
+
+
+def _run(n, node_size, order="fixed", extra=(), port=29611):
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}",
+           os.path.join(ROOT, "tests", "mp_worker.py"), "--node-size", str(node_size), "--order", order, *extra]
+    res = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT)
+    assert res.returncode == 0 and "MP_PARITY_OK" in res.stdout, res.stdout[-3000:] + res.stderr[-3000:]
+    return res.stdout
+
+
+@pytest.mark.parametrize("n,node", [(2, 1), (2, 2), (4, 2), (4, 1), (4, 4), (8, 4), (8, 2)])
+def test_multiproc_parity_fixed(n, node):
+    if n > NGPU:
+        pytest.skip(f"needs {n} GPUs")
+    _run(n, node, port=29611 + n * 10 + node)
+
+
+def test_multiproc_parity_off():
+    _run(2, 1, order="off", port=29681)
+
+
+def test_multiproc_stock_shows_mismatches():
+    _run(2, 2, order="stock", extra=("--stock-delay-us", "3000"), port=29691)
