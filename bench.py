@@ -44,6 +44,9 @@ def parse():
     ap.add_argument("--impl", default="hpz", choices=["hpz", "reference"])
     ap.add_argument("--order", default="fixed", choices=["fixed", "stock", "off"])
     ap.add_argument("--verify", default="fingerprint", choices=["none", "fingerprint", "exact"])
+    ap.add_argument("--unfused", action="store_true",
+                    help="separate reduce-scatter and Adam kernels (default: fused per-layer RS+Adam)")
+    ap.add_argument("--ctas-per-sm", type=int, default=None)
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -185,6 +188,10 @@ def main():
     ctx = rc.ctx
     H.hpz_set_order(ctx, args.order)
     H.hpz_set_verify(ctx, args.verify)
+    fused = not args.unfused
+    H.hpz_set_option(ctx, "store_grad_shard", 0 if fused else 1)
+    if args.ctas_per_sm:
+        H.hpz_set_option(ctx, "ctas_per_sm", args.ctas_per_sm)
     stream = torch.cuda.current_stream()
     infos = rc.infos
     # resident inputs: initial params (device generator) and this rank's gradients
@@ -222,12 +229,16 @@ def main():
             if grads_from is not None:
                 H.hpz_grad_upload(ctx, i, grads_from.data_ptr(), infos[i].numel, stream)
             rec("rs0")
-            H.hpz_reduce_scatter(ctx, i, stream)
+            if fused:
+                H.hpz_reduce_scatter_adam(ctx, i, adam, stream)   # RS + this layer's Adam
+            else:
+                H.hpz_reduce_scatter(ctx, i, stream)
             rec("rs1")
-        for i in range(L):
-            rec("adam0")
-            H.hpz_step(ctx, i, adam, stream)
-            rec("adam1")
+        if not fused:
+            for i in range(L):
+                rec("adam0")
+                H.hpz_step(ctx, i, adam, stream)
+                rec("adam1")
 
     for _ in range(args.warmup):
         one_step()
@@ -272,16 +283,22 @@ def main():
     # ------------------------------------------------ roofline of the dominant kernel
     pk = peaks()
     hbm_peak = pk.get("hbm_gbs", 6650.0)
-    share = {"fwd_gather": fwd_ms, "bwd_gather": bwd_ms, "reduce_scatter": rs_ms, "adam": adam_ms}
+    rs_name = "reduce_scatter+adam" if fused else "reduce_scatter"
+    share = {"fwd_gather": fwd_ms, "bwd_gather": bwd_ms, rs_name: rs_ms}
+    if not fused:
+        share["adam"] = adam_ms
     dom = max(share, key=share.get)
     if world == 1:
         hbm_alg = {"fwd_gather": 3 * ag_bytes,     # read primary, write full out + secondary (P'=1)
-                   "bwd_gather": 2 * ag_bytes, "reduce_scatter": 2 * rs_bytes, "adam": adam_bytes}
+                   "bwd_gather": 2 * ag_bytes, "reduce_scatter": 2 * rs_bytes, "adam": adam_bytes,
+                   # fused at P=1: read grad slot 4 + w,m,v 12; write w,m,v 12 + primary e
+                   "reduce_scatter+adam": sum(x.shard for x in infos) * (28 + e)}
         alg = hbm_alg[dom]
         bound, peak, unit = "hbm", hbm_peak, "GB/s"
     else:
         nv_alg = {"fwd_gather": ag_bytes * (P - 1) / P, "bwd_gather": ag_bytes * (Pp - 1) / Pp,
-                  "reduce_scatter": rs_bytes * (P - 1) / P, "adam": adam_bytes}
+                  "reduce_scatter": rs_bytes * (P - 1) / P, "adam": adam_bytes,
+                  "reduce_scatter+adam": rs_bytes * (P - 1) / P}
         alg = nv_alg[dom]
         if dom == "adam":
             bound, peak, unit = "hbm", hbm_peak, "GB/s"
@@ -356,13 +373,16 @@ def main():
                        "l2": "no flush: per-step working set >> 126 MB L2 (every layer buffer is "
                              "touched once per phase)",
                        "value_def": "sum over ranks of AllGather output bytes (fwd+bwd) + ReduceScatter "
-                                    "input bytes, / max-over-ranks collective device time per step (algbw)"},
+                                    "input bytes, / max-over-ranks collective device time per step (algbw); "
+                                    "with the fused RS+Adam kernel the optimizer time is inside the "
+                                    "collective time"},
             "stale_param_mismatches": {"fingerprint_layers": int(stats[0]), "exact_elements": int(stats[1]),
                                        "nan_reads": int(stats[2]), "timeouts": int(stats[3]),
                                        "layers_checked": int(stats[4])},
             "breakdown_ms_per_step": {"fwd_gather": round(fwd_ms, 3), "bwd_gather": round(bwd_ms, 3),
-                                      "reduce_scatter": round(rs_ms, 3), "adam": round(adam_ms, 3),
+                                      rs_name: round(rs_ms, 3), "adam": round(adam_ms, 3),
                                       "collectives": round(coll_ms, 3)},
+            "fused_rs_adam": fused,
             "nvlink_ingress_GBps_per_gpu": round(ingress / (coll_ms * 1e-3) / 1e9, 2) if world > 1 else None,
             "nvlink_frac_of_900": round(ingress / (coll_ms * 1e-3) / 1e9 / 900, 4) if world > 1 else None,
             "step_GBps_incl_adam": round(world * coll_bytes / (step_ms * 1e-3) / 1e9, 2),

@@ -259,6 +259,21 @@ HPZ_API int hpz_reduce_scatter(hpz_ctx* ctx, int layer, void* stream);
  * layer's reduce-scatter of step t was not issued. */
 HPZ_API int hpz_step(hpz_ctx* ctx, int layer, const hpz_adam* adam, void* stream);
 
+/* Fused reduce-scatter + partitioned Adam of one layer (a5 + a6 in one kernel): the
+ * fixed-order reduced gradient feeds the Adam update of the same shard elements in
+ * registers (the per-layer optimizer step of ZeRO-3 overlapped with the backward pass;
+ * mathematically identical to hpz_reduce_scatter + hpz_step, bit for bit).  Waits E5,
+ * E2 (+E7); releases E6 and E1(t+1).  The grad shard is stored only if
+ * HPZ_OPT_STORE_GRAD_SHARD is on (default on).  Counts as both calls for the layer. */
+HPZ_API int hpz_reduce_scatter_adam(hpz_ctx* ctx, int layer, const hpz_adam* adam, void* stream);
+
+/* Tuning / behaviour options (identical on all ranks). */
+typedef enum {
+  HPZ_OPT_STORE_GRAD_SHARD = 0,  /* 0/1: fused RS+Adam writes the reduced gradient shard */
+  HPZ_OPT_CTAS_PER_SM = 1        /* 1..32: persistent-grid CTAs per SM of the streaming kernels */
+} hpz_option;
+HPZ_API int hpz_set_option(hpz_ctx* ctx, int option, int64_t value);
+
 #ifdef __cplusplus
 }
 #endif

@@ -303,9 +303,6 @@ __global__ void __launch_bounds__(kThreads) rs_kernel(const __grid_constant__ RS
 }
 
 // ------------------------------------------------------------------ Adam (a6)
-struct AdamScalarsDev {
-  float beta1, beta2, omb1, omb2, step_size, bc2_sqrt, eps, lr_wd;
-};
 
 // One element, exactly the oracle's operation sequence (no contraction: every
 // operation is an explicit round-to-nearest intrinsic).
@@ -359,6 +356,78 @@ __global__ void __launch_bounds__(kThreads) adam_kernel(const __grid_constant__ 
     }
   }
   if (last_cta(p.done_ctr)) release_all(p.rel);   // E1: primary of step t+1 is ready
+}
+
+__device__ __forceinline__ void store_prim(void* prim, int bf16, int64_t i, const float4& w) {
+  if (bf16) {
+    __nv_bfloat162 lo = __floats2bfloat162_rn(w.x, w.y);
+    __nv_bfloat162 hi = __floats2bfloat162_rn(w.z, w.w);
+    uint2 pk;
+    pk.x = *reinterpret_cast<uint32_t*>(&lo);
+    pk.y = *reinterpret_cast<uint32_t*>(&hi);
+    reinterpret_cast<uint2*>(prim)[i] = pk;
+  } else {
+    reinterpret_cast<float4*>(prim)[i] = w;
+  }
+}
+
+// ------------------------------------------------------------------ fused RS + Adam (a5 + a6)
+// The owner's reduced gradient never round-trips through HBM: the fixed-order sum of the
+// P peers' slices feeds the Adam update of the same shard elements in registers.  Saves
+// the grad-shard write + read (8 B per shard element) and, on NVLink-bound worlds, hides
+// the optimizer's HBM traffic under the reduce-scatter's NVLink time.
+template <int P, int U>
+__global__ void __launch_bounds__(kThreads) rs_adam_kernel(const __grid_constant__ RSParams r,
+                                                           const __grid_constant__ AdamParams a) {
+  if (threadIdx.x == 0) {
+    if (r.ready.n) {
+      __threadfence_system();
+      release_all(r.ready);                  // E5
+    }
+    wait_all(r.ready_wait, r.sync);          // E5: every rank's slot is written
+    wait_all(a.wait, a.sync);                // E2 (+E7): nobody still reads my primary
+  }
+  __syncthreads();
+  const int64_t stride = (int64_t)gridDim.x * kThreads * U;
+  for (int64_t base = (int64_t)blockIdx.x * kThreads * U + threadIdx.x; base < r.n_vec; base += stride) {
+    float4 x[U][P];
+    float4 w[U], m[U], v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = base + (int64_t)u * kThreads;
+      if (i < r.n_vec) {
+#pragma unroll
+        for (int j = 0; j < P; ++j) x[u][j] = ld_f4(r.src[j] + 4 * i);
+        w[u] = ld_f4(a.w + 4 * i);
+        m[u] = ld_f4(a.m + 4 * i);
+        v[u] = ld_f4(a.v + 4 * i);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = base + (int64_t)u * kThreads;
+      if (i < r.n_vec) {
+        float4 g = pairwise_sum<P>(x[u]);
+        g.x = __fmul_rn(g.x, r.inv_p);
+        g.y = __fmul_rn(g.y, r.inv_p);
+        g.z = __fmul_rn(g.z, r.inv_p);
+        g.w = __fmul_rn(g.w, r.inv_p);
+        if (r.out) reinterpret_cast<float4*>(r.out)[i] = g;    // optional (inspection/tests)
+        adam1(w[u].x, m[u].x, v[u].x, g.x, a);
+        adam1(w[u].y, m[u].y, v[u].y, g.y, a);
+        adam1(w[u].z, m[u].z, v[u].z, g.z, a);
+        adam1(w[u].w, m[u].w, v[u].w, g.w, a);
+        reinterpret_cast<float4*>(a.w)[i] = w[u];
+        reinterpret_cast<float4*>(a.m)[i] = m[u];
+        reinterpret_cast<float4*>(a.v)[i] = v[u];
+        store_prim(a.prim, a.prim_bf16, i, w[u]);
+      }
+    }
+  }
+  if (last_cta(r.done_ctr)) {
+    release_all(r.rel);   // E6: my reads of every slot are done
+    release_all(a.rel);   // E1: my primary of step t+1 is ready
+  }
 }
 
 // ------------------------------------------------------------------ small kernels
@@ -461,6 +530,20 @@ cudaError_t launch_reduce_scatter(const RSParams& p, int world, int grid, cudaSt
     HPZ_RS_CASE(7) HPZ_RS_CASE(8) HPZ_RS_CASE(9) HPZ_RS_CASE(10) HPZ_RS_CASE(11) HPZ_RS_CASE(12)
     HPZ_RS_CASE(13) HPZ_RS_CASE(14) HPZ_RS_CASE(15) HPZ_RS_CASE(16)
 #undef HPZ_RS_CASE
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rs_adam(const RSParams& r, const AdamParams& a, int world, int grid, cudaStream_t s) {
+  switch (world) {
+#define HPZ_RSA_CASE(P, U) \
+  case P: rs_adam_kernel<P, U><<<grid, kThreads, 0, s>>>(r, a); break;
+    HPZ_RSA_CASE(1, 2) HPZ_RSA_CASE(2, 2) HPZ_RSA_CASE(3, 2) HPZ_RSA_CASE(4, 2) HPZ_RSA_CASE(5, 1)
+    HPZ_RSA_CASE(6, 1) HPZ_RSA_CASE(7, 1) HPZ_RSA_CASE(8, 1) HPZ_RSA_CASE(9, 1) HPZ_RSA_CASE(10, 1)
+    HPZ_RSA_CASE(11, 1) HPZ_RSA_CASE(12, 1) HPZ_RSA_CASE(13, 1) HPZ_RSA_CASE(14, 1) HPZ_RSA_CASE(15, 1)
+    HPZ_RSA_CASE(16, 1)
+#undef HPZ_RSA_CASE
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();

@@ -58,6 +58,8 @@ struct hpz_ctx {
   cudaStream_t side = nullptr;            // stock-mode copy stream
   cudaEvent_t side_ev = nullptr;
   uint64_t launches = 0;
+  bool store_grad_shard = true;           // fused RS+Adam also stores the reduced gradient
+  int ctas_per_sm = 4;
   std::string err;
 
   // ---- arena addressing (identical on every rank) ----
@@ -521,7 +523,7 @@ int hpz_fwd_gather(hpz_ctx* c, int layer, void* full_out, void* stream) {
   p.rel.value = t1;
   p.sync = c->sync();
   const int64_t tiles = (p.src_bytes / 16 + 2047) / 2048 * c->world;
-  cudaError_t e = launch_gather(p, grid_for(c, tiles, 4), s);
+  cudaError_t e = launch_gather(p, grid_for(c, tiles, c->ctas_per_sm), s);
   if (e != cudaSuccess) return fail(c, HPZ_ECUDA, "fwd gather launch: %s", cudaGetErrorString(e));
   c->launches += 1;
   if (c->order == HPZ_ORDER_STOCK) {
@@ -620,7 +622,7 @@ int hpz_bwd_gather(hpz_ctx* c, int layer, void* full_out, void* stream) {
     }
   }
   const int64_t tiles = (p.src_bytes / 16 + 2047) / 2048 * p.n_src;
-  cudaError_t e = launch_gather(p, grid_for(c, tiles, 4), s);
+  cudaError_t e = launch_gather(p, grid_for(c, tiles, c->ctas_per_sm), s);
   if (e != cudaSuccess) return fail(c, HPZ_ECUDA, "bwd gather launch: %s", cudaGetErrorString(e));
   c->launches += 1;
   L.bwd_t = c->t;
@@ -670,14 +672,11 @@ int hpz_grads_ready(hpz_ctx* c, int layer, void* stream) {
   return HPZ_OK;
 }
 
-int hpz_reduce_scatter(hpz_ctx* c, int layer, void* stream) {
-  if (int rc = check_ready(c)) return rc;
-  if (int rc = check_layer(c, layer)) return rc;
+static void build_rs(hpz_ctx* c, int layer, RSParams& p) {
   Layer& L = c->layers[layer];
-  if (L.rs_t == c->t) return fail(c, HPZ_ESTATE, "layer %d already reduce-scattered at step %lld", layer, (long long)c->t);
   const int slot = L.slot;
   const uint32_t u1 = epoch(c->slot_use[slot] + 1);
-  RSParams p{};
+  p = RSParams{};
   for (int j = 0; j < c->world; ++j)
     p.src[j] = reinterpret_cast<const float*>(c->arena[j] + c->off_slot[slot]) + (int64_t)c->rank * L.shard;
   p.out = reinterpret_cast<float*>(c->arena[c->rank] + L.off_gshard);
@@ -690,24 +689,44 @@ int hpz_reduce_scatter(hpz_ctx* c, int layer, void* stream) {
   for (int j = 0; j < c->world; ++j) p.rel.ptr[p.rel.n++] = c->slot_flag(j, S_RS_DONE, slot, c->rank);   // E6
   p.rel.value = u1;
   p.sync = c->sync();
-  cudaError_t e = launch_reduce_scatter(p, c->world, grid_for(c, (p.n_vec + 511) / 512, 4), static_cast<cudaStream_t>(stream));
+}
+
+static void rs_issued(hpz_ctx* c, int layer) {
+  Layer& L = c->layers[layer];
+  c->slot_use[L.slot] += 1;
+  c->slot_ready_sent[L.slot] = 0;
+  L.rs_t = c->t;
+}
+
+int hpz_reduce_scatter(hpz_ctx* c, int layer, void* stream) {
+  if (int rc = check_ready(c)) return rc;
+  if (int rc = check_layer(c, layer)) return rc;
+  Layer& L = c->layers[layer];
+  if (L.rs_t == c->t) return fail(c, HPZ_ESTATE, "layer %d already reduce-scattered at step %lld", layer, (long long)c->t);
+  RSParams p;
+  build_rs(c, layer, p);
+  cudaError_t e = launch_reduce_scatter(p, c->world, grid_for(c, (p.n_vec + 511) / 512, c->ctas_per_sm), static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return fail(c, HPZ_ECUDA, "reduce-scatter launch: %s", cudaGetErrorString(e));
   c->launches += 1;
-  c->slot_use[slot] += 1;
-  c->slot_ready_sent[slot] = 0;
-  L.rs_t = c->t;
+  rs_issued(c, layer);
   return HPZ_OK;
 }
 
-static int step_one(hpz_ctx* c, int layer, const hpz_adam* a, cudaStream_t s) {
+static int check_adam(hpz_ctx* c, const hpz_adam* a) {
+  if (!a) return fail(c, HPZ_EINVAL, "null adam");
+  if (!(a->lr >= 0) || !(a->beta1 >= 0 && a->beta1 < 1) || !(a->beta2 >= 0 && a->beta2 < 1) || !(a->eps > 0) ||
+      !(a->weight_decay >= 0))
+    return fail(c, HPZ_EINVAL, "bad Adam hyper-parameters");
+  return HPZ_OK;
+}
+
+static void build_adam(hpz_ctx* c, int layer, const hpz_adam* a, AdamParams& p) {
   Layer& L = c->layers[layer];
-  if (L.rs_t != c->t) return fail(c, HPZ_ESTATE, "layer %d: step without its reduce-scatter at step %lld", layer, (long long)c->t);
-  if (L.step_t == c->t) return fail(c, HPZ_ESTATE, "layer %d already stepped at step %lld", layer, (long long)c->t);
   const int64_t tad = a->step > 0 ? a->step : c->t + 1;    // 1-based Adam count (R24)
   const double bc1 = 1.0 - std::pow(a->beta1, (double)tad);
   const double bc2 = 1.0 - std::pow(a->beta2, (double)tad);
   char* ar = c->arena[c->rank];
-  AdamParams p{};
+  p = AdamParams{};
   p.w = reinterpret_cast<float*>(ar + L.off_master);
   p.m = reinterpret_cast<float*>(ar + L.off_m);
   p.v = reinterpret_cast<float*>(ar + L.off_v);
@@ -726,38 +745,85 @@ static int step_one(hpz_ctx* c, int layer, const hpz_adam* a, cudaStream_t s) {
   const uint32_t t1 = epoch(c->t + 1);
   for (int j = 0; j < c->world; ++j) p.wait.ptr[p.wait.n++] = c->flag(c->rank, F_FWD_DONE, layer, j);   // E2
   if (c->order == HPZ_ORDER_OFF || c->verify == HPZ_VERIFY_EXACT)
-    for (int j = 0; j < c->world; ++j) p.wait.ptr[p.wait.n++] = c->flag(c->rank, F_BWDP_DONE, layer, j);
+    for (int j = 0; j < c->world; ++j) p.wait.ptr[p.wait.n++] = c->flag(c->rank, F_BWDP_DONE, layer, j);   // E7
   p.wait.target = t1;
   p.done_ctr = c->ctr(C_ADAM, layer);
   for (int j = 0; j < c->world; ++j) p.rel.ptr[p.rel.n++] = c->flag(j, F_PRIM_READY, layer, c->rank);   // E1
   p.rel.value = epoch(c->t + 2);
   p.sync = c->sync();
-  cudaError_t e = launch_adam(p, grid_for(c, (p.n_vec + 511) / 512, 4), s);
+}
+
+static void stepped(hpz_ctx* c, int layer) {
+  c->layers[layer].step_t = c->t;
+  bool all = true;
+  for (int i = 0; i < c->n_layers; ++i) all = all && c->layers[i].step_t == c->t;
+  if (all) c->t += 1;
+}
+
+static int step_one(hpz_ctx* c, int layer, const hpz_adam* a, cudaStream_t s) {
+  Layer& L = c->layers[layer];
+  if (L.rs_t != c->t) return fail(c, HPZ_ESTATE, "layer %d: step without its reduce-scatter at step %lld", layer, (long long)c->t);
+  if (L.step_t == c->t) return fail(c, HPZ_ESTATE, "layer %d already stepped at step %lld", layer, (long long)c->t);
+  AdamParams p;
+  build_adam(c, layer, a, p);
+  cudaError_t e = launch_adam(p, grid_for(c, (p.n_vec + 511) / 512, c->ctas_per_sm), s);
   if (e != cudaSuccess) return fail(c, HPZ_ECUDA, "adam launch: %s", cudaGetErrorString(e));
   c->launches += 1;
-  L.step_t = c->t;
   return HPZ_OK;
 }
 
 int hpz_step(hpz_ctx* c, int layer, const hpz_adam* a, void* stream) {
   if (int rc = check_ready(c)) return rc;
-  if (!a) return fail(c, HPZ_EINVAL, "null adam");
-  if (!(a->lr >= 0) || !(a->beta1 >= 0 && a->beta1 < 1) || !(a->beta2 >= 0 && a->beta2 < 1) || !(a->eps > 0))
-    return fail(c, HPZ_EINVAL, "bad Adam hyper-parameters");
+  if (int rc = check_adam(c, a)) return rc;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (layer == -1) {
     for (int i = 0; i < c->n_layers; ++i)
-      if (c->layers[i].rs_t != c->t) return fail(c, HPZ_ESTATE, "layer %d not reduce-scattered at step %lld", i, (long long)c->t);
-    for (int i = 0; i < c->n_layers; ++i)
+      if (c->layers[i].rs_t != c->t || c->layers[i].step_t == c->t)
+        return fail(c, HPZ_ESTATE, "layer %d not reduce-scattered (or already stepped) at step %lld", i, (long long)c->t);
+    const int64_t t = c->t;
+    for (int i = 0; i < c->n_layers; ++i) {
       if (int rc = step_one(c, i, a, s)) return rc;
-  } else {
-    if (int rc = check_layer(c, layer)) return rc;
-    if (int rc = step_one(c, layer, a, s)) return rc;
+      c->layers[i].step_t = t;
+    }
+    c->t += 1;
+    return HPZ_OK;
   }
-  bool all = true;
-  for (int i = 0; i < c->n_layers; ++i) all = all && c->layers[i].step_t == c->t;
-  if (all) c->t += 1;
+  if (int rc = check_layer(c, layer)) return rc;
+  if (int rc = step_one(c, layer, a, s)) return rc;
+  stepped(c, layer);
   return HPZ_OK;
+}
+
+int hpz_reduce_scatter_adam(hpz_ctx* c, int layer, const hpz_adam* a, void* stream) {
+  if (int rc = check_ready(c)) return rc;
+  if (int rc = check_layer(c, layer)) return rc;
+  if (int rc = check_adam(c, a)) return rc;
+  Layer& L = c->layers[layer];
+  if (L.rs_t == c->t) return fail(c, HPZ_ESTATE, "layer %d already reduce-scattered at step %lld", layer, (long long)c->t);
+  if (L.step_t == c->t) return fail(c, HPZ_ESTATE, "layer %d already stepped at step %lld", layer, (long long)c->t);
+  RSParams r;
+  AdamParams p;
+  build_rs(c, layer, r);
+  build_adam(c, layer, a, p);
+  if (!c->store_grad_shard) r.out = nullptr;
+  cudaError_t e = launch_rs_adam(r, p, c->world, grid_for(c, (r.n_vec + 511) / 512, c->ctas_per_sm), static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return fail(c, HPZ_ECUDA, "rs+adam launch: %s", cudaGetErrorString(e));
+  c->launches += 1;
+  rs_issued(c, layer);
+  stepped(c, layer);
+  return HPZ_OK;
+}
+
+int hpz_set_option(hpz_ctx* c, int option, int64_t value) {
+  if (!c) return HPZ_EINVAL;
+  switch (option) {
+    case HPZ_OPT_STORE_GRAD_SHARD: c->store_grad_shard = value != 0; return HPZ_OK;
+    case HPZ_OPT_CTAS_PER_SM:
+      if (value < 1 || value > 32) return fail(c, HPZ_EINVAL, "ctas_per_sm must be in [1, 32]");
+      c->ctas_per_sm = (int)value;
+      return HPZ_OK;
+    default: return fail(c, HPZ_EINVAL, "unknown option %d", option);
+  }
 }
 
 }  // extern "C"

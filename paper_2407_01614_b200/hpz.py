@@ -27,8 +27,9 @@ EXPORTED = [
     "hpz_counters", "hpz_last_error", "hpz_version", "hpz_set_order", "hpz_set_verify",
     "hpz_set_timeout", "hpz_load_master", "hpz_synth_master", "hpz_fwd_gather", "hpz_bwd_gather",
     "hpz_grad_buffer", "hpz_grad_upload", "hpz_synth_grads", "hpz_grads_ready",
-    "hpz_reduce_scatter", "hpz_step",
+    "hpz_reduce_scatter", "hpz_step", "hpz_reduce_scatter_adam", "hpz_set_option",
 ]
+OPT = {"store_grad_shard": 0, "ctas_per_sm": 1}
 
 
 class hpz_adam(ctypes.Structure):
@@ -87,6 +88,8 @@ def _load() -> ctypes.CDLL:
         "hpz_grads_ready": (c_int, [P, c_int, c_void_p]),
         "hpz_reduce_scatter": (c_int, [P, c_int, c_void_p]),
         "hpz_step": (c_int, [P, c_int, POINTER(hpz_adam), c_void_p]),
+        "hpz_reduce_scatter_adam": (c_int, [P, c_int, POINTER(hpz_adam), c_void_p]),
+        "hpz_set_option": (c_int, [P, c_int, c_int64]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -249,3 +252,12 @@ def make_adam(lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.0, step=
 
 def hpz_step(ctx, layer: int, adam: hpz_adam, stream=None):
     _check(ctx, "hpz_step", LIB.hpz_step(ctx, layer, byref(adam), _stream(stream)))
+
+
+def hpz_reduce_scatter_adam(ctx, layer: int, adam: hpz_adam, stream=None):
+    _check(ctx, "hpz_reduce_scatter_adam", LIB.hpz_reduce_scatter_adam(ctx, layer, byref(adam), _stream(stream)))
+
+
+def hpz_set_option(ctx, option: str | int, value: int):
+    o = OPT[option] if isinstance(option, str) else option
+    _check(ctx, "hpz_set_option", LIB.hpz_set_option(ctx, o, c_int64(int(value))))

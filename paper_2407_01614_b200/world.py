@@ -148,9 +148,11 @@ def full_buffers(world_obj, n_bufs: int = 1, device=None):
 
 
 def run_step(ranks: list[RankCtx], fwd_out, bwd_out, adam, stream=None, grad_fn=None,
-             emulated: bool = False, layer_hook=None):
+             emulated: bool = False, layer_hook=None, fused: bool = False):
     """One step of Algorithm 1 for the given ranks (all P in emulation, or this process's one).
 
+    fused=True replaces each layer's reduce-scatter and the final optimizer step by the
+    fused per-layer RS+Adam kernel (same bits).
     fwd_out[r](i) / bwd_out[r](i) return the device pointer of the caller-owned full buffer
     for rank r, layer i.  grad_fn(rank_ctx, i) fills the rank's gradient slot (or None:
     gradients already resident).  In emulation every phase is issued for all ranks before
@@ -173,11 +175,15 @@ def run_step(ranks: list[RankCtx], fwd_out, bwd_out, adam, stream=None, grad_fn=
             for rc in ranks:
                 H.hpz_grads_ready(rc.ctx, i, stream)
         for rc in ranks:
-            H.hpz_reduce_scatter(rc.ctx, i, stream)
+            if fused:                                       # RS + this layer's Adam, one kernel
+                H.hpz_reduce_scatter_adam(rc.ctx, i, adam, stream)
+            else:
+                H.hpz_reduce_scatter(rc.ctx, i, stream)
         if layer_hook:
             layer_hook("rs", i)
-    for rc in ranks:                                        # optimizer.step()
-        H.hpz_step(rc.ctx, -1, adam, stream)
+    if not fused:
+        for rc in ranks:                                    # optimizer.step()
+            H.hpz_step(rc.ctx, -1, adam, stream)
 
 
 class _CAI:

@@ -27,12 +27,14 @@ class ParityRun:
     """Drive an EmulatedWorld and an HpzOracle side by side on the same seeded inputs."""
 
     def __init__(self, numels, world, node_size, dtype="bf16", align=256, order="fixed",
-                 verify="exact", grad_kind="uniform", n_grad_slots=None, stock_schedule="program"):
+                 verify="exact", grad_kind="uniform", n_grad_slots=None, stock_schedule="program",
+                 fused=False, store_grad_shard=True):
         from paper_2407_01614_b200 import hpz as H
         from paper_2407_01614_b200.world import EmulatedWorld
         self.H = H
         self.numels, self.P, self.Pp, self.dtype = list(numels), world, node_size, dtype
         self.grad_kind = grad_kind
+        self.fused, self.store_grad_shard = fused, store_grad_shard
         self.w = EmulatedWorld(numels, world, node_size, dtype=dtype, align=align, n_grad_slots=n_grad_slots,
                                timeout_s=10.0)
         self.o = O.HpzOracle(self.numels, world, node_size, align=align, param_dtype=dtype, order=order,
@@ -41,6 +43,7 @@ class ParityRun:
         for rc in self.w.ranks:
             H.hpz_set_order(rc.ctx, order)
             H.hpz_set_verify(rc.ctx, verify)
+            H.hpz_set_option(rc.ctx, "store_grad_shard", int(store_grad_shard))
         tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
         L = len(self.numels)
         self.fwd = [[torch.zeros(rc.infos[i].numel_pad, dtype=tdt, device="cuda") for i in range(L)] for rc in self.w.ranks]
@@ -63,7 +66,7 @@ class ParityRun:
         self._keep = []
         run_step(self.w.ranks, [lambda i, r=r: self.fwd[r][i].data_ptr() for r in range(self.P)],
                  [lambda i, r=r: self.bwd[r][i].data_ptr() for r in range(self.P)], self.adam,
-                 stream=self.stream, grad_fn=self.grad_fn, emulated=True)
+                 stream=self.stream, grad_fn=self.grad_fn, emulated=True, fused=self.fused)
         torch.cuda.synchronize()
         rec = self.o.step()
         self.t += 1

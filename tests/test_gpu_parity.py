@@ -43,9 +43,10 @@ def _check_step(run: ParityRun, rec, check_all=True):
                 sec = bits_np(buffer_view(rc, i, "secondary", dtype), dtype)
                 assert np.array_equal(sec, O.param_bits(st.sec, dtype)), f"secondary layer {i} rank {r}"
             # a5 reduce-scatter bit-exact in the fixed order
-            g_gpu = buffer_view(rc, i, "grad_shard", "f32").cpu().numpy()
-            g_ref = O.reduce_scatter(grads, lay, r)
-            assert np.array_equal(g_gpu.view(np.uint32), g_ref.view(np.uint32)), f"RS layer {i} rank {r}"
+            if run.store_grad_shard:
+                g_gpu = buffer_view(rc, i, "grad_shard", "f32").cpu().numpy()
+                g_ref = O.reduce_scatter(grads, lay, r)
+                assert np.array_equal(g_gpu.view(np.uint32), g_ref.view(np.uint32)), f"RS layer {i} rank {r}"
             # a6 Adam + bf16 refresh
             for kind, ref in (("master", st.master), ("m", st.m), ("v", st.v)):
                 got = buffer_view(rc, i, kind, "f32").cpu().numpy()
@@ -66,6 +67,31 @@ def test_parity_fixed(P, Pp):
         c = run.counters()
         assert c["mismatches"] == 0 and c["nan_reads"] == 0 and c["timeouts"] == 0
         assert c["fp_mismatches"] == 0 and c["fp_checked"] == 3 * len(NUMELS) * P
+    finally:
+        run.close()
+
+
+@pytest.mark.parametrize("P,Pp", TOPOS)
+@pytest.mark.parametrize("store", [True, False])
+def test_parity_fused_rs_adam(P, Pp, store):
+    """hpz_reduce_scatter_adam == hpz_reduce_scatter + hpz_step, bit for bit."""
+    if not store and P not in (1, 8):
+        pytest.skip("store=False covered at P=1, 8")
+    run = ParityRun(NUMELS, P, Pp, fused=True, store_grad_shard=store)
+    try:
+        for _ in range(3):
+            _check_step(run, run.step())
+        c = run.counters()
+        assert c["mismatches"] == 0 and c["timeouts"] == 0 and c["fp_mismatches"] == 0
+    finally:
+        run.close()
+
+
+def test_parity_fused_off_order():
+    run = ParityRun(NUMELS, 4, 2, order="off", fused=True)
+    try:
+        for _ in range(2):
+            _check_step(run, run.step())
     finally:
         run.close()
 
