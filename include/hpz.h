@@ -270,8 +270,13 @@ HPZ_API int hpz_reduce_scatter_adam(hpz_ctx* ctx, int layer, const hpz_adam* ada
 /* Tuning / behaviour options (identical on all ranks). */
 typedef enum {
   HPZ_OPT_STORE_GRAD_SHARD = 0,  /* 0/1: fused RS+Adam writes the reduced gradient shard */
-  HPZ_OPT_CTAS_PER_SM = 1        /* 1..32: persistent-grid CTAs per SM of the streaming kernels */
+  HPZ_OPT_CTAS_PER_SM = 1,       /* 1..32: persistent-grid CTAs per SM of the LDG/STG kernels */
+  HPZ_OPT_COPY_ENGINE = 2        /* HPZ_COPY_TMA (default) or HPZ_COPY_LDG */
 } hpz_option;
+/* Copy engine of the gathers and the reduce-scatter: TMA 1-D bulk copies through a
+ * shared-memory stage ring (cp.async.bulk, one persistent CTA per SM), or 16-byte
+ * LDG/STG streams (several CTAs per SM).  EXACT verification always uses LDG/STG. */
+typedef enum { HPZ_COPY_LDG = 0, HPZ_COPY_TMA = 1 } hpz_copy_engine;
 HPZ_API int hpz_set_option(hpz_ctx* ctx, int option, int64_t value);
 
 #ifdef __cplusplus

@@ -12,7 +12,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libhpz.so")
-SOURCES = ["hpz_kernels.cu", "hpz_runtime.cpp"]
+SOURCES = ["hpz_kernels.cu", "hpz_tma.cu", "hpz_runtime.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 

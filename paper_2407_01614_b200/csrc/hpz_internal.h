@@ -99,6 +99,10 @@ cudaError_t launch_reduce_scatter(const RSParams& p, int world, int grid, cudaSt
 cudaError_t launch_adam(const AdamParams& p, int grid, cudaStream_t s);
 // Fused reduce-scatter + Adam (r.out may be nullptr: the reduced gradient is not stored).
 cudaError_t launch_rs_adam(const RSParams& r, const AdamParams& a, int world, int grid, cudaStream_t s);
+// TMA (cp.async.bulk) variants, one persistent CTA per SM (hpz_tma.cu).  The gather
+// variant does not implement EXACT verification (p.mism must be nullptr).
+cudaError_t launch_gather_tma(const GatherParams& p, int grid, cudaStream_t s);
+cudaError_t launch_rs_tma(const RSParams& r, const AdamParams* a, int world, int grid, cudaStream_t s);
 cudaError_t launch_wait(const WaitList& w, const SyncCommon& sync, cudaStream_t s);
 cudaError_t launch_release(const ReleaseList& r, cudaStream_t s);
 cudaError_t launch_copy(void* dst, const void* src, int64_t bytes, int grid, cudaStream_t s);

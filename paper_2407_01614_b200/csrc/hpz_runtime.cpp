@@ -59,7 +59,8 @@ struct hpz_ctx {
   cudaEvent_t side_ev = nullptr;
   uint64_t launches = 0;
   bool store_grad_shard = true;           // fused RS+Adam also stores the reduced gradient
-  int ctas_per_sm = 4;
+  int ctas_per_sm = 4;                    // LDG/STG kernels
+  int copy_engine = HPZ_COPY_TMA;
   std::string err;
 
   // ---- arena addressing (identical on every rank) ----
@@ -134,6 +135,24 @@ int grid_for(const hpz_ctx* c, int64_t work_items, int per_sm) {
 }
 
 uint32_t epoch(int64_t x) { return (uint32_t)x; }
+
+// Pick the gather kernel: TMA bulk pipeline (one CTA/SM) or the LDG/STG kernel (EXACT
+// verification, or when selected with HPZ_OPT_COPY_ENGINE).
+cudaError_t gather_launch(const hpz_ctx* c, const GatherParams& p, cudaStream_t s) {
+  if (c->copy_engine == HPZ_COPY_TMA && p.mism == nullptr) {
+    const int64_t chunks = (p.src_bytes + 32767) / 32768 * p.n_src;
+    return launch_gather_tma(p, grid_for(c, chunks, 1), s);
+  }
+  const int64_t tiles = (p.src_bytes / 16 + 2047) / 2048 * p.n_src;
+  return launch_gather(p, grid_for(c, tiles, c->ctas_per_sm), s);
+}
+
+cudaError_t rs_launch(const hpz_ctx* c, const RSParams& r, const AdamParams* a, cudaStream_t s) {
+  if (c->copy_engine == HPZ_COPY_TMA)
+    return launch_rs_tma(r, a, c->world, grid_for(c, (r.n_vec * 4 + 1023) / 1024, 1), s);
+  const int grid = grid_for(c, (r.n_vec + 511) / 512, c->ctas_per_sm);
+  return a ? launch_rs_adam(r, *a, c->world, grid, s) : launch_reduce_scatter(r, c->world, grid, s);
+}
 
 int do_init_shard(hpz_ctx* c, int layer, const float* src, uint64_t key, float scale, cudaStream_t s) {
   Layer& L = c->layers[layer];
@@ -522,8 +541,7 @@ int hpz_fwd_gather(hpz_ctx* c, int layer, void* full_out, void* stream) {
   for (int j = 0; j < c->world; ++j) p.rel.ptr[p.rel.n++] = c->flag(j, F_FWD_DONE, layer, c->rank);            // E2
   p.rel.value = t1;
   p.sync = c->sync();
-  const int64_t tiles = (p.src_bytes / 16 + 2047) / 2048 * c->world;
-  cudaError_t e = launch_gather(p, grid_for(c, tiles, c->ctas_per_sm), s);
+  cudaError_t e = gather_launch(c, p, s);
   if (e != cudaSuccess) return fail(c, HPZ_ECUDA, "fwd gather launch: %s", cudaGetErrorString(e));
   c->launches += 1;
   if (c->order == HPZ_ORDER_STOCK) {
@@ -621,8 +639,7 @@ int hpz_bwd_gather(hpz_ctx* c, int layer, void* full_out, void* stream) {
       c->launches += 1;
     }
   }
-  const int64_t tiles = (p.src_bytes / 16 + 2047) / 2048 * p.n_src;
-  cudaError_t e = launch_gather(p, grid_for(c, tiles, c->ctas_per_sm), s);
+  cudaError_t e = gather_launch(c, p, s);
   if (e != cudaSuccess) return fail(c, HPZ_ECUDA, "bwd gather launch: %s", cudaGetErrorString(e));
   c->launches += 1;
   L.bwd_t = c->t;
@@ -705,7 +722,7 @@ int hpz_reduce_scatter(hpz_ctx* c, int layer, void* stream) {
   if (L.rs_t == c->t) return fail(c, HPZ_ESTATE, "layer %d already reduce-scattered at step %lld", layer, (long long)c->t);
   RSParams p;
   build_rs(c, layer, p);
-  cudaError_t e = launch_reduce_scatter(p, c->world, grid_for(c, (p.n_vec + 511) / 512, c->ctas_per_sm), static_cast<cudaStream_t>(stream));
+  cudaError_t e = rs_launch(c, p, nullptr, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return fail(c, HPZ_ECUDA, "reduce-scatter launch: %s", cudaGetErrorString(e));
   c->launches += 1;
   rs_issued(c, layer);
@@ -806,7 +823,7 @@ int hpz_reduce_scatter_adam(hpz_ctx* c, int layer, const hpz_adam* a, void* stre
   build_rs(c, layer, r);
   build_adam(c, layer, a, p);
   if (!c->store_grad_shard) r.out = nullptr;
-  cudaError_t e = launch_rs_adam(r, p, c->world, grid_for(c, (r.n_vec + 511) / 512, c->ctas_per_sm), static_cast<cudaStream_t>(stream));
+  cudaError_t e = rs_launch(c, r, &p, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return fail(c, HPZ_ECUDA, "rs+adam launch: %s", cudaGetErrorString(e));
   c->launches += 1;
   rs_issued(c, layer);
@@ -821,6 +838,10 @@ int hpz_set_option(hpz_ctx* c, int option, int64_t value) {
     case HPZ_OPT_CTAS_PER_SM:
       if (value < 1 || value > 32) return fail(c, HPZ_EINVAL, "ctas_per_sm must be in [1, 32]");
       c->ctas_per_sm = (int)value;
+      return HPZ_OK;
+    case HPZ_OPT_COPY_ENGINE:
+      if (value != HPZ_COPY_LDG && value != HPZ_COPY_TMA) return fail(c, HPZ_EINVAL, "copy engine must be 0 (LDG) or 1 (TMA)");
+      c->copy_engine = (int)value;
       return HPZ_OK;
     default: return fail(c, HPZ_EINVAL, "unknown option %d", option);
   }

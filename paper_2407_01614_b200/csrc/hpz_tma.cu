@@ -1,0 +1,444 @@
+// TMA (cp.async.bulk) pipelines of the hpZ hot path for sm_100a.
+//
+// One persistent CTA per SM.  A single elected producer thread streams chunks of the
+// sources (peer arenas over NVLink, or local HBM) into a ring of shared-memory stages
+// with 1-D bulk copies completing on mbarriers; the data never passes through
+// registers unless it must be computed on:
+//   * gather_tma_kernel: producer bulk-loads a 32 KiB chunk of source j, then bulk-stores
+//     the same smem stage to the full buffer and (fused secondary store, a2) to the
+//     secondary; optional fingerprint consumer warps read the stage (a7).
+//   * rs_tma_kernel<P, ADAM>: producer bulk-loads the P peers' gradient slices of a
+//     chunk (+ the master/m/v chunk when ADAM); 256 consumer threads sum in the fixed
+//     pairwise-by-rank order (R7) and apply Adam (R8) from smem, storing with STG.128.
+// Flags are acquired by the producer before the first bulk read of a source; a
+// fence.proxy.async orders the generic-proxy acquire before the async-proxy reads, and
+// the bulk stores are drained (wait_group 0) and proxy-fenced before the grid-wide
+// release.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "hpz_internal.h"
+
+namespace hpz {
+
+namespace {
+
+constexpr int kGatherChunk = 32768;     // bytes per gather stage
+constexpr int kGatherStages = 4;
+constexpr int kFpWarps = 4;             // fingerprint consumer warps
+constexpr int kRsChunk = 1024;          // shard elements per RS stage
+constexpr int kRsConsumers = 256;       // one float4 per consumer thread per stage
+
+// ------------------------------------------------------------------ PTX wrappers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{ .reg .pred q; mbarrier.try_wait.parity.shared::cta.b64 q, [%1], %2; selp.u32 %0, 1, 0, q; }"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void tma_load(void* sdst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(sdst)),
+      "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_store(void* gdst, const void* ssrc, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_u32(ssrc)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ bool wait_geq(const uint32_t* flag, uint32_t target, const SyncCommon& s) {
+  if (ld_acquire_sys(flag) >= target) return true;
+  if (*(volatile uint32_t*)s.abort_flag) return false;
+  const uint64_t t0 = globaltimer();
+  uint32_t spins = 0;
+  while (ld_acquire_sys(flag) < target) {
+    if ((++spins & 63u) == 0) {
+      if (*(volatile uint32_t*)s.abort_flag) return false;
+      if (globaltimer() - t0 > s.timeout_ns) {
+        atomicAdd(s.timeouts, 1ull);
+        atomicExch(s.abort_flag, 1u);
+        *s.host_err = 1u;
+        __threadfence_system();
+        return false;
+      }
+    }
+    __nanosleep(32);
+  }
+  return true;
+}
+__device__ void wait_all(const WaitList& w, const SyncCommon& s) {
+  for (int k = 0; k < w.n; ++k) wait_geq(w.ptr[k], w.target, s);
+}
+__device__ void release_all(const ReleaseList& r) {
+  for (int k = 0; k < r.n; ++k) st_release_sys(r.ptr[k], r.value);
+}
+__device__ __forceinline__ bool last_cta(uint32_t* ctr) {
+  __syncthreads();
+  bool last = false;
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    const uint32_t prev = atomicAdd(ctr, 1u);
+    if (prev == gridDim.x - 1) {
+      *ctr = 0u;
+      __threadfence_system();
+      last = true;
+    }
+  }
+  return last;
+}
+__device__ __forceinline__ uint64_t fp_word(uint32_t gi, const int4& w) {
+  uint32_t h = (uint32_t)w.x * 0x85EBCA6Bu ^ (uint32_t)w.y * 0xC2B2AE35u ^ (uint32_t)w.z * 0x27D4EB2Fu ^
+               (uint32_t)w.w * 0x165667B1u ^ gi * 0x9E3779B1u;
+  h ^= h >> 15;
+  h *= 0x2C1B3C6Du;
+  h ^= h >> 12;
+  uint32_t h2 = h * 0x297A2D39u;
+  h2 ^= h2 >> 16;
+  return ((uint64_t)h2 << 32) | h;
+}
+
+// ------------------------------------------------------------------ gather (a2, a4)
+// Block = 1 producer warp (+ kFpWarps fingerprint warps when FP).  Dynamic smem =
+// kGatherStages * kGatherChunk.
+template <bool FP>
+__global__ void __launch_bounds__(32 * (1 + kFpWarps), 1)
+    gather_tma_kernel(const __grid_constant__ GatherParams p) {
+  extern __shared__ __align__(1024) char smem[];
+  __shared__ __align__(8) uint64_t full_bar[kGatherStages];
+  __shared__ __align__(8) uint64_t empty_bar[kGatherStages];
+  __shared__ unsigned long long fp_red[kFpWarps];
+
+  const int n_src = p.n_src;
+  const int64_t chunks_per_src = (p.src_bytes + kGatherChunk - 1) / kGatherChunk;
+  const int64_t total = chunks_per_src * n_src;
+  const int64_t nk = blockIdx.x < total ? (total - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kGatherStages; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], kFpWarps);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  auto chunk_of = [&](int64_t k, int& j, int64_t& off, uint32_t& bytes) {
+    const int64_t w = blockIdx.x + k * gridDim.x;
+    j = (int)(w % n_src);
+    off = (w / n_src) * kGatherChunk;
+    const int64_t rem = p.src_bytes - off;
+    bytes = (uint32_t)(rem < kGatherChunk ? rem : kGatherChunk);
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {
+      uint32_t waited = 0;
+      bool war_done = false;
+      auto issue_load = [&](int64_t k) {
+        int j;
+        int64_t off;
+        uint32_t bytes;
+        chunk_of(k, j, off, bytes);
+        if (!((waited >> j) & 1u)) {
+          if (p.src_flag[j] != nullptr) wait_geq(p.src_flag[j], p.src_target, p.sync);   // E1 / E3
+          fence_proxy_async();
+          waited |= 1u << j;
+        }
+        const int s = (int)(k % kGatherStages);
+        mbar_expect_tx(&full_bar[s], bytes);
+        tma_load(smem + (size_t)s * kGatherChunk, p.src[j] + off, bytes, &full_bar[s]);
+      };
+      const int64_t pre = nk < kGatherStages - 1 ? nk : kGatherStages - 1;
+      for (int64_t k = 0; k < pre; ++k) issue_load(k);
+      for (int64_t k = 0; k < nk; ++k) {
+        const int s = (int)(k % kGatherStages);
+        mbar_wait(&full_bar[s], (uint32_t)((k / kGatherStages) & 1));
+        int j;
+        int64_t off;
+        uint32_t bytes;
+        chunk_of(k, j, off, bytes);
+        const char* stage = smem + (size_t)s * kGatherChunk;
+        tma_store(p.out + (int64_t)j * p.src_bytes + off, stage, bytes);
+        if (p.sec != nullptr && j >= p.sec_lo && j < p.sec_hi) {
+          if (!war_done) {
+            wait_all(p.war, p.sync);   // E4: node peers' backward reads of step t-1 are done
+            fence_proxy_async();
+            war_done = true;
+          }
+          tma_store(p.sec + (int64_t)(j - p.sec_lo) * p.src_bytes + off, stage, bytes);
+        }
+        bulk_commit();
+        if (k + kGatherStages - 1 < nk) {
+          // the stage of chunk k-1 is refilled: its stores must have read it ...
+          bulk_wait_read<1>();
+          // ... and the fingerprint warps must be done with it
+          if (FP && k >= 1) mbar_wait(&empty_bar[(k - 1) % kGatherStages], (uint32_t)(((k - 1) / kGatherStages) & 1));
+          issue_load(k + kGatherStages - 1);
+        }
+      }
+      bulk_wait_all();       // all bulk stores performed
+      fence_proxy_async();   // ... and ordered before the generic-proxy release below
+    }
+  } else if (FP) {
+    // fingerprint consumers: order-independent checksum of every 16-byte word
+    uint64_t fp = 0;
+    const int ct = threadIdx.x - 32;
+    for (int64_t k = 0; k < nk; ++k) {
+      const int s = (int)(k % kGatherStages);
+      mbar_wait(&full_bar[s], (uint32_t)((k / kGatherStages) & 1));
+      int j;
+      int64_t off;
+      uint32_t bytes;
+      chunk_of(k, j, off, bytes);
+      const int4* st = reinterpret_cast<const int4*>(smem + (size_t)s * kGatherChunk);
+      const int64_t gv0 = ((int64_t)j * p.src_bytes + off) >> 4;
+      for (uint32_t v = ct; v < bytes / 16; v += 32 * kFpWarps) fp += fp_word((uint32_t)(gv0 + v), st[v]);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty_bar[s]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) fp += __shfl_xor_sync(0xffffffffu, fp, o);
+    if (lane == 0) fp_red[warp - 1] = fp;
+  }
+  __syncthreads();
+  if (FP && threadIdx.x == 0) {
+    unsigned long long s = 0;
+    for (int w = 0; w < kFpWarps; ++w) s += fp_red[w];
+    if (s) atomicAdd(p.fp_acc, s);
+  }
+  if (last_cta(p.done_ctr)) {
+    if (p.fp_a != nullptr) {
+      wait_all(p.cmp_wait, p.sync);
+      const unsigned long long a = atomicExch(p.fp_a, 0ull);
+      const unsigned long long b = atomicExch(p.fp_b, 0ull);
+      atomicAdd(p.fp_checked, 1ull);
+      if (a != b) atomicAdd(p.fp_mism, 1ull);
+    }
+    release_all(p.rel);
+  }
+}
+
+// ------------------------------------------------------------------ RS (+ Adam) (a5, a6)
+__device__ __forceinline__ float4 add4(const float4& a, const float4& b) {
+  return make_float4(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y), __fadd_rn(a.z, b.z), __fadd_rn(a.w, b.w));
+}
+template <int P>
+__device__ __forceinline__ float4 pairwise_sum(float4 (&x)[P]) {
+#pragma unroll
+  for (int n = P; n > 1; n = (n + 1) / 2) {
+#pragma unroll
+    for (int k = 0; k < n / 2; ++k) x[k] = add4(x[2 * k], x[2 * k + 1]);
+    if (n & 1) x[n / 2] = x[n - 1];
+  }
+  return x[0];
+}
+__device__ __forceinline__ void adam1(float& w, float& m, float& v, float g, const AdamParams& p) {
+  m = __fadd_rn(__fmul_rn(p.beta1, m), __fmul_rn(p.omb1, g));
+  v = __fadd_rn(__fmul_rn(p.beta2, v), __fmul_rn(__fmul_rn(p.omb2, g), g));
+  const float d = __fadd_rn(__fdiv_rn(__fsqrt_rn(v), p.bc2_sqrt), p.eps);
+  if (p.lr_wd != 0.0f) w = __fsub_rn(w, __fmul_rn(p.lr_wd, w));
+  w = __fsub_rn(w, __fmul_rn(p.step_size, __fdiv_rn(m, d)));
+}
+
+template <int P, bool ADAM>
+struct RsCfg {
+  static constexpr int kBufs = P + (ADAM ? 3 : 0);          // P gradient slices (+ w, m, v)
+  static constexpr int kStageBytes = kBufs * kRsChunk * 4;
+  static constexpr int kStages = (200 * 1024) / kStageBytes >= 6 ? 6 : (200 * 1024) / kStageBytes;
+};
+
+// Block = 1 producer warp + 8 consumer warps.  Dynamic smem = kStages * kStageBytes.
+template <int P, bool ADAM>
+__global__ void __launch_bounds__(32 + kRsConsumers, 1)
+    rs_tma_kernel(const __grid_constant__ RSParams r, const __grid_constant__ AdamParams a) {
+  using C = RsCfg<P, ADAM>;
+  static_assert(C::kStages >= 2, "stage ring too small");
+  extern __shared__ __align__(1024) char smem[];
+  __shared__ __align__(8) uint64_t full_bar[C::kStages];
+  __shared__ __align__(8) uint64_t empty_bar[C::kStages];
+  const int64_t n = r.n_vec * 4;   // shard elements (multiple of 256)
+  const int64_t total = (n + kRsChunk - 1) / kRsChunk;
+  const int64_t nk = blockIdx.x < total ? (total - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    if (r.ready.n) {
+      __threadfence_system();
+      release_all(r.ready);              // E5
+    }
+    wait_all(r.ready_wait, r.sync);      // E5: every rank's gradient slot is written
+    if (ADAM) wait_all(a.wait, a.sync);  // E2 (+E7): nobody still reads my primary
+    fence_proxy_async();
+    for (int s = 0; s < C::kStages; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], kRsConsumers / 32);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int64_t k = 0; k < nk; ++k) {
+        const int s = (int)(k % C::kStages);
+        if (k >= C::kStages) mbar_wait(&empty_bar[s], (uint32_t)(((k / C::kStages) - 1) & 1));
+        const int64_t e0 = (blockIdx.x + k * gridDim.x) * (int64_t)kRsChunk;
+        const int64_t rem = n - e0;
+        const uint32_t cnt = (uint32_t)(rem < kRsChunk ? rem : kRsChunk);
+        const uint32_t bytes = cnt * 4;
+        float* st = reinterpret_cast<float*>(smem + (size_t)s * C::kStageBytes);
+        mbar_expect_tx(&full_bar[s], bytes * C::kBufs);
+#pragma unroll
+        for (int j = 0; j < P; ++j) tma_load(st + j * kRsChunk, r.src[j] + e0, bytes, &full_bar[s]);
+        if (ADAM) {
+          tma_load(st + (P + 0) * kRsChunk, a.w + e0, bytes, &full_bar[s]);
+          tma_load(st + (P + 1) * kRsChunk, a.m + e0, bytes, &full_bar[s]);
+          tma_load(st + (P + 2) * kRsChunk, a.v + e0, bytes, &full_bar[s]);
+        }
+      }
+    }
+  } else {
+    const int ct = threadIdx.x - 32;     // 0..255: one float4 of the 1024-element chunk
+    for (int64_t k = 0; k < nk; ++k) {
+      const int s = (int)(k % C::kStages);
+      mbar_wait(&full_bar[s], (uint32_t)((k / C::kStages) & 1));
+      const int64_t e0 = (blockIdx.x + k * gridDim.x) * (int64_t)kRsChunk;
+      const int64_t rem = n - e0;
+      const int cnt = (int)(rem < kRsChunk ? rem : kRsChunk);
+      const float4* st = reinterpret_cast<const float4*>(smem + (size_t)s * C::kStageBytes);
+      if (ct * 4 < cnt) {
+        float4 x[P];
+#pragma unroll
+        for (int j = 0; j < P; ++j) x[j] = st[j * (kRsChunk / 4) + ct];
+        float4 g = pairwise_sum<P>(x);
+        g.x = __fmul_rn(g.x, r.inv_p);
+        g.y = __fmul_rn(g.y, r.inv_p);
+        g.z = __fmul_rn(g.z, r.inv_p);
+        g.w = __fmul_rn(g.w, r.inv_p);
+        const int64_t i = e0 / 4 + ct;   // float4 index in the shard
+        if (r.out) reinterpret_cast<float4*>(r.out)[i] = g;
+        if (ADAM) {
+          float4 w = st[(P + 0) * (kRsChunk / 4) + ct];
+          float4 m = st[(P + 1) * (kRsChunk / 4) + ct];
+          float4 v = st[(P + 2) * (kRsChunk / 4) + ct];
+          adam1(w.x, m.x, v.x, g.x, a);
+          adam1(w.y, m.y, v.y, g.y, a);
+          adam1(w.z, m.z, v.z, g.z, a);
+          adam1(w.w, m.w, v.w, g.w, a);
+          reinterpret_cast<float4*>(a.w)[i] = w;
+          reinterpret_cast<float4*>(a.m)[i] = m;
+          reinterpret_cast<float4*>(a.v)[i] = v;
+          if (a.prim_bf16) {
+            __nv_bfloat162 lo = __floats2bfloat162_rn(w.x, w.y);
+            __nv_bfloat162 hi = __floats2bfloat162_rn(w.z, w.w);
+            uint2 pk;
+            pk.x = *reinterpret_cast<uint32_t*>(&lo);
+            pk.y = *reinterpret_cast<uint32_t*>(&hi);
+            reinterpret_cast<uint2*>(a.prim)[i] = pk;
+          } else {
+            reinterpret_cast<float4*>(a.prim)[i] = w;
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty_bar[s]);
+    }
+  }
+  if (last_cta(r.done_ctr)) {
+    release_all(r.rel);              // E6
+    if (ADAM) release_all(a.rel);    // E1 (t+1)
+  }
+}
+
+template <int P, bool ADAM>
+cudaError_t launch_rs_tma_t(const RSParams& r, const AdamParams& a, int grid, cudaStream_t s) {
+  using C = RsCfg<P, ADAM>;
+  const int smem = C::kStages * C::kStageBytes;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(rs_tma_kernel<P, ADAM>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  rs_tma_kernel<P, ADAM><<<grid, 32 + kRsConsumers, smem, s>>>(r, a);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_gather_tma(const GatherParams& p, int grid, cudaStream_t s) {
+  const int smem = kGatherStages * kGatherChunk;
+  static bool attr_set[2] = {false, false};
+  const bool fp = p.fp_acc != nullptr;
+  if (!attr_set[fp]) {
+    cudaError_t e = fp ? cudaFuncSetAttribute(gather_tma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)
+                       : cudaFuncSetAttribute(gather_tma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    attr_set[fp] = true;
+  }
+  if (fp)
+    gather_tma_kernel<true><<<grid, 32 * (1 + kFpWarps), smem, s>>>(p);
+  else
+    gather_tma_kernel<false><<<grid, 32, smem, s>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rs_tma(const RSParams& r, const AdamParams* a, int world, int grid, cudaStream_t s) {
+  AdamParams none{};
+  switch (world) {
+#define HPZ_RST_CASE(P) \
+  case P: return a ? launch_rs_tma_t<P, true>(r, *a, grid, s) : launch_rs_tma_t<P, false>(r, none, grid, s);
+    HPZ_RST_CASE(1) HPZ_RST_CASE(2) HPZ_RST_CASE(3) HPZ_RST_CASE(4) HPZ_RST_CASE(5) HPZ_RST_CASE(6)
+    HPZ_RST_CASE(7) HPZ_RST_CASE(8) HPZ_RST_CASE(9) HPZ_RST_CASE(10) HPZ_RST_CASE(11) HPZ_RST_CASE(12)
+    HPZ_RST_CASE(13) HPZ_RST_CASE(14) HPZ_RST_CASE(15) HPZ_RST_CASE(16)
+#undef HPZ_RST_CASE
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace hpz

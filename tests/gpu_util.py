@@ -28,7 +28,7 @@ class ParityRun:
 
     def __init__(self, numels, world, node_size, dtype="bf16", align=256, order="fixed",
                  verify="exact", grad_kind="uniform", n_grad_slots=None, stock_schedule="program",
-                 fused=False, store_grad_shard=True):
+                 fused=False, store_grad_shard=True, copy_engine="tma"):
         from paper_2407_01614_b200 import hpz as H
         from paper_2407_01614_b200.world import EmulatedWorld
         self.H = H
@@ -44,6 +44,7 @@ class ParityRun:
             H.hpz_set_order(rc.ctx, order)
             H.hpz_set_verify(rc.ctx, verify)
             H.hpz_set_option(rc.ctx, "store_grad_shard", int(store_grad_shard))
+            H.hpz_set_option(rc.ctx, "copy_engine", H.COPY[copy_engine])
         tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
         L = len(self.numels)
         self.fwd = [[torch.zeros(rc.infos[i].numel_pad, dtype=tdt, device="cuda") for i in range(L)] for rc in self.w.ranks]

@@ -29,6 +29,9 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--numels", default="300007,65536,4099,77")
     ap.add_argument("--stock-delay-us", type=int, default=0)
+    ap.add_argument("--engine", default="tma")
+    ap.add_argument("--verify", default="fingerprint")
+    ap.add_argument("--fused", type=int, default=1)
     args = ap.parse_args()
     local = int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
@@ -42,7 +45,8 @@ def main():
     rc = W.ranks[0]
     s = torch.cuda.current_stream()
     H.hpz_set_order(rc.ctx, args.order, stock_delay_us=args.stock_delay_us, stock_poison=args.order == "stock")
-    H.hpz_set_verify(rc.ctx, "exact")
+    H.hpz_set_verify(rc.ctx, "exact" if args.order == "stock" else args.verify)
+    H.hpz_set_option(rc.ctx, "copy_engine", H.COPY[args.engine])
     for i, n in enumerate(numels):
         w0 = torch.from_numpy(S.layer_params(i, n)).cuda()
         H.hpz_load_master(rc.ctx, i, w0.data_ptr(), s)
@@ -62,7 +66,7 @@ def main():
     for t in range(args.steps):
         t_box[0] = t
         run_step([rc], {r: (lambda i: fwd[i].data_ptr())}, {r: (lambda i: bwd[i].data_ptr())}, adam,
-                 stream=s, grad_fn=grad_fn)
+                 stream=s, grad_fn=grad_fn, fused=bool(args.fused))
         torch.cuda.synchronize()
         rec = o.step()
         if args.order == "stock":

@@ -28,7 +28,14 @@ def _run(n, node_size, order="fixed", extra=(), port=29611):
 def test_multiproc_parity_fixed(n, node):
     if n > NGPU:
         pytest.skip(f"needs {n} GPUs")
-    _run(n, node, port=29611 + n * 10 + node)
+    _run(n, node, port=29611 + n * 10 + node)                       # TMA engine, fused RS+Adam
+
+
+@pytest.mark.parametrize("n,node", [(2, 1), (4, 2), (8, 4)])
+def test_multiproc_parity_ldg_exact_unfused(n, node):
+    if n > NGPU:
+        pytest.skip(f"needs {n} GPUs")
+    _run(n, node, extra=("--engine", "ldg", "--verify", "exact", "--fused", "0"), port=29711 + n * 10 + node)
 
 
 def test_multiproc_parity_off():

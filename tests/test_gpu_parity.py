@@ -57,9 +57,13 @@ def _check_step(run: ParityRun, rec, check_all=True):
             assert np.array_equal(prim, O.param_bits(st.prim, dtype)), f"primary layer {i} rank {r}"
 
 
+ENGINES = [("ldg", "exact"), ("tma", "fingerprint")]   # EXACT verification runs on the LDG kernel
+
+
+@pytest.mark.parametrize("engine,verify", ENGINES)
 @pytest.mark.parametrize("P,Pp", TOPOS)
-def test_parity_fixed(P, Pp):
-    run = ParityRun(NUMELS, P, Pp)
+def test_parity_fixed(P, Pp, engine, verify):
+    run = ParityRun(NUMELS, P, Pp, copy_engine=engine, verify=verify)
     try:
         for _ in range(3):
             rec = run.step()
@@ -71,13 +75,14 @@ def test_parity_fixed(P, Pp):
         run.close()
 
 
+@pytest.mark.parametrize("engine,verify", ENGINES)
 @pytest.mark.parametrize("P,Pp", TOPOS)
 @pytest.mark.parametrize("store", [True, False])
-def test_parity_fused_rs_adam(P, Pp, store):
+def test_parity_fused_rs_adam(P, Pp, store, engine, verify):
     """hpz_reduce_scatter_adam == hpz_reduce_scatter + hpz_step, bit for bit."""
     if not store and P not in (1, 8):
         pytest.skip("store=False covered at P=1, 8")
-    run = ParityRun(NUMELS, P, Pp, fused=True, store_grad_shard=store)
+    run = ParityRun(NUMELS, P, Pp, fused=True, store_grad_shard=store, copy_engine=engine, verify=verify)
     try:
         for _ in range(3):
             _check_step(run, run.step())
@@ -108,9 +113,10 @@ def test_parity_off_equals_fixed(P, Pp):
         run.close()
 
 
-def test_parity_fp32_params_toy_shapes():
+@pytest.mark.parametrize("engine", ["ldg", "tma"])
+def test_parity_fp32_params_toy_shapes(engine):
     """Config C1 shapes with fp32 parameters (primary == master copy)."""
-    run = ParityRun(O.toy_layer_numels(), 8, 4, dtype="f32")
+    run = ParityRun(O.toy_layer_numels(), 8, 4, dtype="f32", copy_engine=engine, fused=engine == "tma")
     try:
         for _ in range(2):
             _check_step(run, run.step())
@@ -120,7 +126,7 @@ def test_parity_fp32_params_toy_shapes():
 
 def test_parity_dyadic_rs_closed_form():
     """Dyadic gradients: the GPU reduce-scatter equals the exact rational mean."""
-    run = ParityRun([40_000], 8, 2, grad_kind="dyadic")
+    run = ParityRun([40_000], 8, 2, grad_kind="dyadic", verify="fingerprint")
     try:
         rec = run.step()
         _check_step(run, rec)
@@ -130,7 +136,7 @@ def test_parity_dyadic_rs_closed_form():
 
 def test_parity_shared_grad_slots():
     """Fewer gradient slots than layers: the E6 wait orders slot reuse."""
-    run = ParityRun(NUMELS, 4, 2, n_grad_slots=2)
+    run = ParityRun(NUMELS, 4, 2, n_grad_slots=2, verify="fingerprint")
     try:
         for _ in range(2):
             _check_step(run, run.step())
