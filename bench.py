@@ -48,6 +48,7 @@ def parse():
                     help="separate reduce-scatter and Adam kernels (default: fused per-layer RS+Adam)")
     ap.add_argument("--ctas-per-sm", type=int, default=None)
     ap.add_argument("--copy-engine", default="tma", choices=["tma", "ldg"])
+    ap.add_argument("--qgz", action="store_true", help="ZeRO++ qgZ: INT4 gradient all-to-all (SURVEY f1)")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -182,9 +183,11 @@ def main():
     L = len(numels)
 
     if world > 1:
-        W = DistWorld(numels, node_size, dtype=dtype, n_grad_slots=L, device=local_rank, timeout_s=60.0)
+        W = DistWorld(numels, node_size, dtype=dtype, n_grad_slots=L, device=local_rank, timeout_s=60.0,
+                      qgz=args.qgz)
     else:
-        W = EmulatedWorld(numels, 1, 1, dtype=dtype, n_grad_slots=L, device=local_rank, timeout_s=60.0)
+        W = EmulatedWorld(numels, 1, 1, dtype=dtype, n_grad_slots=L, device=local_rank, timeout_s=60.0,
+                          qgz=args.qgz)
     rc = W.ranks[0]
     ctx = rc.ctx
     H.hpz_set_order(ctx, args.order)
@@ -272,7 +275,8 @@ def main():
     coll_bytes = 2 * ag_bytes + rs_bytes
     # NVLink ingress per rank per step (busbw convention)
     P, Pp = world, node_size
-    ingress = ag_bytes * (P - 1) / P + ag_bytes * (Pp - 1) / Pp + rs_bytes * (P - 1) / P
+    rs_wire = rs_bytes * (0.625 / 4 if args.qgz else 1.0)
+    ingress = ag_bytes * (P - 1) / P + ag_bytes * (Pp - 1) / Pp + rs_wire * (P - 1) / P
     adam_bytes = sum(x.shard for x in infos) * (30 if dtype == "bf16" else 32)
 
     vals = max_over_ranks([step_ms, tot["fwd"], tot["bwd"], tot["rs"], tot["adam"],
@@ -301,8 +305,8 @@ def main():
         bound, peak, unit = "hbm", hbm_peak, "GB/s"
     else:
         nv_alg = {"fwd_gather": ag_bytes * (P - 1) / P, "bwd_gather": ag_bytes * (Pp - 1) / Pp,
-                  "reduce_scatter": rs_bytes * (P - 1) / P, "adam": adam_bytes,
-                  "reduce_scatter+adam": rs_bytes * (P - 1) / P}
+                  "reduce_scatter": rs_wire * (P - 1) / P, "adam": adam_bytes,
+                  "reduce_scatter+adam": rs_wire * (P - 1) / P}
         alg = nv_alg[dom]
         if dom == "adam":
             bound, peak, unit = "hbm", hbm_peak, "GB/s"
@@ -374,6 +378,8 @@ def main():
                        "world": world, "node_size": node_size, "virtual_nodes": world // node_size,
                        "parallelism": f"hpZ dp{world} (P={world}, P'={node_size})", "order": args.order,
                        "verify": args.verify, "copy_engine": args.copy_engine,
+                       "qgz": "int4 blockwise (64) gradient all-to-all; RS bytes counted as the fp32 "
+                              "gradient bytes reduced, wire bytes 0.625 B/elem" if args.qgz else None,
                        "l2": "no flush: per-step working set >> 126 MB L2 (every layer buffer is "
                              "touched once per phase)",
                        "value_def": "sum over ranks of AllGather output bytes (fwd+bwd) + ReduceScatter "

@@ -242,8 +242,8 @@ HPZ_API int hpz_grad_upload(hpz_ctx* ctx, int layer, const float* src, int64_t n
  * uniform*scale, 1: dyadic grid), zero in padding. */
 HPZ_API int hpz_synth_grads(hpz_ctx* ctx, int layer, uint64_t key, float scale, int kind, void* stream);
 
-/* Optional: publish "my gradient slot of `layer` is written" (E5) early.  Called
- * implicitly by hpz_reduce_scatter if not called for this use of the slot. */
+/* Optional: publish "my gradient slot of `layer` is written" (E5) early (with qgZ: after
+ * quantizing it).  Done implicitly by hpz_reduce_scatter if not called for this use. */
 HPZ_API int hpz_grads_ready(hpz_ctx* ctx, int layer, void* stream);
 
 /* Reduce-scatter of layer `layer` (Alg. 1, ReduceScatter(∇L_i, P)): the
@@ -271,7 +271,16 @@ HPZ_API int hpz_reduce_scatter_adam(hpz_ctx* ctx, int layer, const hpz_adam* ada
 typedef enum {
   HPZ_OPT_STORE_GRAD_SHARD = 0,  /* 0/1: fused RS+Adam writes the reduced gradient shard */
   HPZ_OPT_CTAS_PER_SM = 1,       /* 1..32: persistent-grid CTAs per SM of the LDG/STG kernels */
-  HPZ_OPT_COPY_ENGINE = 2        /* HPZ_COPY_TMA (default) or HPZ_COPY_LDG */
+  HPZ_OPT_COPY_ENGINE = 2,       /* HPZ_COPY_TMA (default) or HPZ_COPY_LDG */
+  HPZ_OPT_QGZ = 3                /* 0 (default) or 4: ZeRO++ qgZ (Alg. 1 comment
+                                    PAPER.md:114 "Replaced with INT4 AllToAll if with qgZ").
+                                    The reduce-scatter quantizes this rank's gradient slot
+                                    blockwise to INT4 (64-element blocks, fp32 min + scale,
+                                    round-half-even codes; reading R26) and the owner pulls
+                                    every rank's codes of its shard (0.625 B/elem instead of
+                                    4), dequantizes (min + code*scale) and reduces in the R7
+                                    order.  Set BEFORE hpz_register_flat_params (it sizes the
+                                    arena).  With qgZ, hpz_grads_ready also quantizes. */
 } hpz_option;
 /* Copy engine of the gathers and the reduce-scatter: TMA 1-D bulk copies through a
  * shared-memory stage ring (cp.async.bulk, one persistent CTA per SM), or 16-byte

@@ -422,6 +422,7 @@ class HpzOracle:
     grad_kind: str = "uniform"
     toy_identical_batches: bool = False
     half_seed: int = 1234
+    qgz: bool = False                    # f1: INT4 quantized gradient all-to-all (qgz_reduce_scatter)
 
     def __post_init__(self):
         check_topology(self.world, self.node_size)
@@ -533,7 +534,8 @@ class HpzOracle:
         # ReduceScatter(∇L_i, P), then optimizer.step()
         for i, lay in enumerate(self.layouts):
             for r in range(P):
-                g = reduce_scatter([G[j][i] for j in range(P)], lay, r)
+                rs = qgz_reduce_scatter if self.qgz else reduce_scatter
+                g = rs([G[j][i] for j in range(P)], lay, r)
                 st = self.state[i][r]
                 if self.optimizer == "adam":
                     st.master, st.m, st.v = adam_update(st.master, st.m, st.v, g,

@@ -64,8 +64,21 @@ struct GatherParams {
   SyncCommon sync;
 };
 
+// qgZ (f1): blockwise INT4 quantization of one rank's gradient slot.
+constexpr int kQgzBlock = 64;          // elements per (min, scale) block
+struct QuantParams {
+  const float* g;                      // local gradient slot (n elements, n % 64 == 0)
+  uint8_t* codes;                      // n/2 bytes: element 2i in the low nibble, 2i+1 high
+  float2* params;                      // n/64 (min, scale) pairs
+  int64_t n;
+  WaitList war;                        // E6 of the previous use: peers done reading codes
+  SyncCommon sync;
+};
+
 // Reduce-scatter (a5).
 struct RSParams {
+  const uint8_t* qcodes[kMaxWorld];    // qgZ: rank j's codes of my shard (peer-mapped), or unused
+  const float2* qparams[kMaxWorld];    // qgZ: rank j's (min, scale) of my shard's blocks
   const float* src[kMaxWorld];         // src[j] = rank j's gradient slot + r*shard (peer-mapped)
   float* out;                          // local gradient shard
   int64_t n_vec;                       // shard / 4
@@ -102,7 +115,9 @@ cudaError_t launch_rs_adam(const RSParams& r, const AdamParams& a, int world, in
 // TMA (cp.async.bulk) variants, one persistent CTA per SM (hpz_tma.cu).  The gather
 // variant does not implement EXACT verification (p.mism must be nullptr).
 cudaError_t launch_gather_tma(const GatherParams& p, int grid, cudaStream_t s);
-cudaError_t launch_rs_tma(const RSParams& r, const AdamParams* a, int world, int grid, cudaStream_t s);
+cudaError_t launch_rs_tma(const RSParams& r, const AdamParams* a, int world, int grid, cudaStream_t s,
+                          bool qgz = false);
+cudaError_t launch_qgz_quantize(const QuantParams& q, int grid, cudaStream_t s);
 cudaError_t launch_wait(const WaitList& w, const SyncCommon& sync, cudaStream_t s);
 cudaError_t launch_release(const ReleaseList& r, cudaStream_t s);
 cudaError_t launch_copy(void* dst, const void* src, int64_t bytes, int grid, cudaStream_t s);

@@ -61,6 +61,8 @@ struct hpz_ctx {
   bool store_grad_shard = true;           // fused RS+Adam also stores the reduced gradient
   int ctas_per_sm = 4;                    // LDG/STG kernels
   int copy_engine = HPZ_COPY_TMA;
+  int qgz_bits = 0;                       // f1: 4 = INT4 quantized gradient all-to-all
+  std::vector<uint64_t> off_qcodes, off_qparams;   // per grad slot (qgZ)
   std::string err;
 
   // ---- arena addressing (identical on every rank) ----
@@ -148,6 +150,7 @@ cudaError_t gather_launch(const hpz_ctx* c, const GatherParams& p, cudaStream_t 
 }
 
 cudaError_t rs_launch(const hpz_ctx* c, const RSParams& r, const AdamParams* a, cudaStream_t s) {
+  if (c->qgz_bits) return launch_rs_tma(r, a, c->world, grid_for(c, (r.n_vec * 4 + 1023) / 1024, 1), s, true);
   if (c->copy_engine == HPZ_COPY_TMA)
     return launch_rs_tma(r, a, c->world, grid_for(c, (r.n_vec * 4 + 1023) / 1024, 1), s);
   const int grid = grid_for(c, (r.n_vec + 511) / 512, c->ctas_per_sm);
@@ -291,9 +294,17 @@ int hpz_register_flat_params(hpz_ctx* c, int n_layers, const int64_t* numel, int
     if (true) { L.off_secondary = off; off = align_up(off + (uint64_t)L.sec_shard * elem, kBufAlign); }
   }
   c->off_slot.assign(n_grad_slots, 0);
+  c->off_qcodes.assign(n_grad_slots, 0);
+  c->off_qparams.assign(n_grad_slots, 0);
   for (int s = 0; s < n_grad_slots; ++s) {
     c->off_slot[s] = off;
     off = align_up(off + (uint64_t)c->slot_numel[s] * 4, kBufAlign);
+    if (c->qgz_bits) {   // int4 codes + (min, scale) per 64-element block
+      c->off_qcodes[s] = off;
+      off = align_up(off + (uint64_t)c->slot_numel[s] / 2, kBufAlign);
+      c->off_qparams[s] = off;
+      off = align_up(off + (uint64_t)c->slot_numel[s] / kQgzBlock * 8, kBufAlign);
+    }
   }
   c->arena_bytes = off;
   c->registered = true;
@@ -677,11 +688,34 @@ int hpz_synth_grads(hpz_ctx* c, int layer, uint64_t key, float scale, int kind, 
   return HPZ_OK;
 }
 
+// qgZ: quantize this rank's gradient slot of `layer` (whole numel_pad) before the RS kernel
+// publishes E5; waits E6 of the slot's previous use (peers done reading the old codes).
+static int qgz_quantize(hpz_ctx* c, int layer, cudaStream_t s) {
+  const Layer& L = c->layers[layer];
+  const int slot = L.slot;
+  QuantParams q{};
+  q.g = reinterpret_cast<const float*>(c->arena[c->rank] + c->off_slot[slot]);
+  q.codes = reinterpret_cast<uint8_t*>(c->arena[c->rank] + c->off_qcodes[slot]);
+  q.params = reinterpret_cast<float2*>(c->arena[c->rank] + c->off_qparams[slot]);
+  q.n = L.numel_pad;
+  if (c->slot_use[slot] > 0) {
+    for (int j = 0; j < c->world; ++j) q.war.ptr[q.war.n++] = c->slot_flag(c->rank, S_RS_DONE, slot, j);
+    q.war.target = epoch(c->slot_use[slot]);
+  }
+  q.sync = c->sync();
+  cudaError_t e = launch_qgz_quantize(q, grid_for(c, (L.numel_pad / kQgzBlock + 15) / 16, 8), s);
+  if (e != cudaSuccess) return fail(c, HPZ_ECUDA, "qgZ quantize launch: %s", cudaGetErrorString(e));
+  c->launches += 1;
+  return HPZ_OK;
+}
+
 int hpz_grads_ready(hpz_ctx* c, int layer, void* stream) {
   if (int rc = check_ready(c)) return rc;
   if (int rc = check_layer(c, layer)) return rc;
   const int slot = c->layers[layer].slot;
   if (c->slot_ready_sent[slot]) return fail(c, HPZ_ESTATE, "grads_ready already published for this use of the slot");
+  if (c->qgz_bits)
+    if (int rc = qgz_quantize(c, layer, static_cast<cudaStream_t>(stream))) return rc;
   cudaError_t e = launch_release(grad_ready_list(c, slot), static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return fail(c, HPZ_ECUDA, "release launch: %s", cudaGetErrorString(e));
   c->launches += 1;
@@ -706,6 +740,12 @@ static void build_rs(hpz_ctx* c, int layer, RSParams& p) {
   for (int j = 0; j < c->world; ++j) p.rel.ptr[p.rel.n++] = c->slot_flag(j, S_RS_DONE, slot, c->rank);   // E6
   p.rel.value = u1;
   p.sync = c->sync();
+  if (c->qgz_bits) {
+    for (int j = 0; j < c->world; ++j) {
+      p.qcodes[j] = reinterpret_cast<const uint8_t*>(c->arena[j] + c->off_qcodes[slot]) + (int64_t)c->rank * L.shard / 2;
+      p.qparams[j] = reinterpret_cast<const float2*>(c->arena[j] + c->off_qparams[slot]) + (int64_t)c->rank * L.shard / kQgzBlock;
+    }
+  }
 }
 
 static void rs_issued(hpz_ctx* c, int layer) {
@@ -722,6 +762,8 @@ int hpz_reduce_scatter(hpz_ctx* c, int layer, void* stream) {
   if (L.rs_t == c->t) return fail(c, HPZ_ESTATE, "layer %d already reduce-scattered at step %lld", layer, (long long)c->t);
   RSParams p;
   build_rs(c, layer, p);
+  if (c->qgz_bits && !c->slot_ready_sent[L.slot])
+    if (int rc = qgz_quantize(c, layer, static_cast<cudaStream_t>(stream))) return rc;
   cudaError_t e = rs_launch(c, p, nullptr, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return fail(c, HPZ_ECUDA, "reduce-scatter launch: %s", cudaGetErrorString(e));
   c->launches += 1;
@@ -823,6 +865,8 @@ int hpz_reduce_scatter_adam(hpz_ctx* c, int layer, const hpz_adam* a, void* stre
   build_rs(c, layer, r);
   build_adam(c, layer, a, p);
   if (!c->store_grad_shard) r.out = nullptr;
+  if (c->qgz_bits && !c->slot_ready_sent[L.slot])
+    if (int rc = qgz_quantize(c, layer, static_cast<cudaStream_t>(stream))) return rc;
   cudaError_t e = rs_launch(c, r, &p, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return fail(c, HPZ_ECUDA, "rs+adam launch: %s", cudaGetErrorString(e));
   c->launches += 1;
@@ -838,6 +882,11 @@ int hpz_set_option(hpz_ctx* c, int option, int64_t value) {
     case HPZ_OPT_CTAS_PER_SM:
       if (value < 1 || value > 32) return fail(c, HPZ_EINVAL, "ctas_per_sm must be in [1, 32]");
       c->ctas_per_sm = (int)value;
+      return HPZ_OK;
+    case HPZ_OPT_QGZ:
+      if (c->registered) return fail(c, HPZ_ESTATE, "qgZ must be chosen before hpz_register_flat_params");
+      if (value != 0 && value != 4) return fail(c, HPZ_EINVAL, "qgZ bits must be 0 (off) or 4");
+      c->qgz_bits = (int)value;
       return HPZ_OK;
     case HPZ_OPT_COPY_ENGINE:
       if (value != HPZ_COPY_LDG && value != HPZ_COPY_TMA) return fail(c, HPZ_EINVAL, "copy engine must be 0 (LDG) or 1 (TMA)");

@@ -285,18 +285,22 @@ __device__ __forceinline__ void adam1(float& w, float& m, float& v, float g, con
   w = __fsub_rn(w, __fmul_rn(p.step_size, __fdiv_rn(m, d)));
 }
 
-template <int P, bool ADAM>
+template <int P, bool ADAM, bool QGZ>
 struct RsCfg {
-  static constexpr int kBufs = P + (ADAM ? 3 : 0);          // P gradient slices (+ w, m, v)
-  static constexpr int kStageBytes = kBufs * kRsChunk * 4;
+  // per stage: P gradient slices (fp32, or qgZ int4 codes + (min, scale) per 64) (+ w, m, v)
+  static constexpr int kCodeBytes = kRsChunk / 2;
+  static constexpr int kParamBytes = kRsChunk / kQgzBlock * 8;
+  static constexpr int kSrcBytes = QGZ ? kCodeBytes + kParamBytes : kRsChunk * 4;
+  static constexpr int kWmvOff = P * kSrcBytes;
+  static constexpr int kStageBytes = kWmvOff + (ADAM ? 3 * kRsChunk * 4 : 0);
   static constexpr int kStages = (200 * 1024) / kStageBytes >= 6 ? 6 : (200 * 1024) / kStageBytes;
 };
 
 // Block = 1 producer warp + 8 consumer warps.  Dynamic smem = kStages * kStageBytes.
-template <int P, bool ADAM>
+template <int P, bool ADAM, bool QGZ>
 __global__ void __launch_bounds__(32 + kRsConsumers, 1)
     rs_tma_kernel(const __grid_constant__ RSParams r, const __grid_constant__ AdamParams a) {
-  using C = RsCfg<P, ADAM>;
+  using C = RsCfg<P, ADAM, QGZ>;
   static_assert(C::kStages >= 2, "stage ring too small");
   extern __shared__ __align__(1024) char smem[];
   __shared__ __align__(8) uint64_t full_bar[C::kStages];
@@ -331,14 +335,24 @@ __global__ void __launch_bounds__(32 + kRsConsumers, 1)
         const int64_t rem = n - e0;
         const uint32_t cnt = (uint32_t)(rem < kRsChunk ? rem : kRsChunk);
         const uint32_t bytes = cnt * 4;
-        float* st = reinterpret_cast<float*>(smem + (size_t)s * C::kStageBytes);
-        mbar_expect_tx(&full_bar[s], bytes * C::kBufs);
+        char* st = smem + (size_t)s * C::kStageBytes;
+        const uint32_t src_bytes = QGZ ? cnt / 2 + cnt / kQgzBlock * 8 : bytes;
+        mbar_expect_tx(&full_bar[s], src_bytes * P + (ADAM ? 3 * bytes : 0));
 #pragma unroll
-        for (int j = 0; j < P; ++j) tma_load(st + j * kRsChunk, r.src[j] + e0, bytes, &full_bar[s]);
+        for (int j = 0; j < P; ++j) {
+          char* dst = st + j * C::kSrcBytes;
+          if (QGZ) {
+            tma_load(dst, r.qcodes[j] + e0 / 2, cnt / 2, &full_bar[s]);
+            tma_load(dst + C::kCodeBytes, r.qparams[j] + e0 / kQgzBlock, cnt / kQgzBlock * 8, &full_bar[s]);
+          } else {
+            tma_load(dst, r.src[j] + e0, bytes, &full_bar[s]);
+          }
+        }
         if (ADAM) {
-          tma_load(st + (P + 0) * kRsChunk, a.w + e0, bytes, &full_bar[s]);
-          tma_load(st + (P + 1) * kRsChunk, a.m + e0, bytes, &full_bar[s]);
-          tma_load(st + (P + 2) * kRsChunk, a.v + e0, bytes, &full_bar[s]);
+          float* wmv = reinterpret_cast<float*>(st + C::kWmvOff);
+          tma_load(wmv + 0 * kRsChunk, a.w + e0, bytes, &full_bar[s]);
+          tma_load(wmv + 1 * kRsChunk, a.m + e0, bytes, &full_bar[s]);
+          tma_load(wmv + 2 * kRsChunk, a.v + e0, bytes, &full_bar[s]);
         }
       }
     }
@@ -350,11 +364,25 @@ __global__ void __launch_bounds__(32 + kRsConsumers, 1)
       const int64_t e0 = (blockIdx.x + k * gridDim.x) * (int64_t)kRsChunk;
       const int64_t rem = n - e0;
       const int cnt = (int)(rem < kRsChunk ? rem : kRsChunk);
-      const float4* st = reinterpret_cast<const float4*>(smem + (size_t)s * C::kStageBytes);
+      const char* stc = smem + (size_t)s * C::kStageBytes;
+      const float4* wmv = reinterpret_cast<const float4*>(stc + C::kWmvOff);
       if (ct * 4 < cnt) {
         float4 x[P];
 #pragma unroll
-        for (int j = 0; j < P; ++j) x[j] = st[j * (kRsChunk / 4) + ct];
+        for (int j = 0; j < P; ++j) {
+          const char* sj = stc + j * C::kSrcBytes;
+          if (QGZ) {
+            // dequantize 4 elements: v = min_b + code * scale_b (multiply, then add)
+            const uint32_t c2 = reinterpret_cast<const uint16_t*>(sj)[ct];
+            const float2 ms = reinterpret_cast<const float2*>(sj + C::kCodeBytes)[ct * 4 / kQgzBlock];
+            x[j].x = __fadd_rn(ms.x, __fmul_rn((float)(c2 & 15u), ms.y));
+            x[j].y = __fadd_rn(ms.x, __fmul_rn((float)((c2 >> 4) & 15u), ms.y));
+            x[j].z = __fadd_rn(ms.x, __fmul_rn((float)((c2 >> 8) & 15u), ms.y));
+            x[j].w = __fadd_rn(ms.x, __fmul_rn((float)((c2 >> 12) & 15u), ms.y));
+          } else {
+            x[j] = reinterpret_cast<const float4*>(sj)[ct];
+          }
+        }
         float4 g = pairwise_sum<P>(x);
         g.x = __fmul_rn(g.x, r.inv_p);
         g.y = __fmul_rn(g.y, r.inv_p);
@@ -363,9 +391,9 @@ __global__ void __launch_bounds__(32 + kRsConsumers, 1)
         const int64_t i = e0 / 4 + ct;   // float4 index in the shard
         if (r.out) reinterpret_cast<float4*>(r.out)[i] = g;
         if (ADAM) {
-          float4 w = st[(P + 0) * (kRsChunk / 4) + ct];
-          float4 m = st[(P + 1) * (kRsChunk / 4) + ct];
-          float4 v = st[(P + 2) * (kRsChunk / 4) + ct];
+          float4 w = wmv[0 * (kRsChunk / 4) + ct];
+          float4 m = wmv[1 * (kRsChunk / 4) + ct];
+          float4 v = wmv[2 * (kRsChunk / 4) + ct];
           adam1(w.x, m.x, v.x, g.x, a);
           adam1(w.y, m.y, v.y, g.y, a);
           adam1(w.z, m.z, v.z, g.z, a);
@@ -395,18 +423,61 @@ __global__ void __launch_bounds__(32 + kRsConsumers, 1)
   }
 }
 
-template <int P, bool ADAM>
+template <int P, bool ADAM, bool QGZ>
 cudaError_t launch_rs_tma_t(const RSParams& r, const AdamParams& a, int grid, cudaStream_t s) {
-  using C = RsCfg<P, ADAM>;
+  using C = RsCfg<P, ADAM, QGZ>;
   const int smem = C::kStages * C::kStageBytes;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(rs_tma_kernel<P, ADAM>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaError_t e =
+        cudaFuncSetAttribute(rs_tma_kernel<P, ADAM, QGZ>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  rs_tma_kernel<P, ADAM><<<grid, 32 + kRsConsumers, smem, s>>>(r, a);
+  rs_tma_kernel<P, ADAM, QGZ><<<grid, 32 + kRsConsumers, smem, s>>>(r, a);
   return cudaGetLastError();
+}
+
+// qgZ quantizer: 16 threads per 64-element block (one float4 each); block min/max by
+// shuffles; NaN anywhere in a block makes its (min, scale) NaN so it surfaces after
+// dequantization.  fp32, one IEEE op per operator, round-half-to-even codes — the
+// oracle's quantize_blockwise decisions, bit for bit.
+__global__ void __launch_bounds__(256) qgz_quantize_kernel(const __grid_constant__ QuantParams q) {
+  if (threadIdx.x == 0 && q.war.n) wait_all(q.war, q.sync);   // E6: peers done with the old codes
+  __syncthreads();
+  const int64_t n_blocks = q.n / kQgzBlock;
+  const int sub = threadIdx.x & 15;
+  const int64_t b_stride = (int64_t)gridDim.x * (blockDim.x / 16);
+  for (int64_t b = (int64_t)blockIdx.x * (blockDim.x / 16) + (threadIdx.x >> 4); b < n_blocks; b += b_stride) {
+    const float4 v = reinterpret_cast<const float4*>(q.g)[b * 16 + sub];
+    bool nan = isnan(v.x) || isnan(v.y) || isnan(v.z) || isnan(v.w);
+    float mn = fminf(fminf(v.x, v.y), fminf(v.z, v.w));
+    float mx = fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w));
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) {
+      mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      nan = nan || __shfl_xor_sync(0xffffffffu, (int)nan, o);
+    }
+    float scale = __fdiv_rn(__fsub_rn(mx, mn), 15.0f);
+    if (nan) {
+      mn = __int_as_float(0x7fc00000);
+      scale = mn;
+    }
+    uint32_t packed = 0;
+    const float e[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      int c = 0;
+      if (scale > 0.0f) {
+        c = __float2int_rn(__fdiv_rn(__fsub_rn(e[k], mn), scale));
+        c = c < 0 ? 0 : (c > 15 ? 15 : c);
+      }
+      packed |= (uint32_t)c << (4 * k);
+    }
+    reinterpret_cast<uint16_t*>(q.codes)[b * 16 + sub] = (uint16_t)packed;
+    if (sub == 0) q.params[b] = make_float2(mn, scale);
+  }
 }
 
 }  // namespace
@@ -428,11 +499,18 @@ cudaError_t launch_gather_tma(const GatherParams& p, int grid, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_rs_tma(const RSParams& r, const AdamParams* a, int world, int grid, cudaStream_t s) {
+cudaError_t launch_qgz_quantize(const QuantParams& q, int grid, cudaStream_t s) {
+  qgz_quantize_kernel<<<grid, 256, 0, s>>>(q);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rs_tma(const RSParams& r, const AdamParams* a, int world, int grid, cudaStream_t s, bool qgz) {
   AdamParams none{};
   switch (world) {
-#define HPZ_RST_CASE(P) \
-  case P: return a ? launch_rs_tma_t<P, true>(r, *a, grid, s) : launch_rs_tma_t<P, false>(r, none, grid, s);
+#define HPZ_RST_CASE(P)                                                                          \
+  case P:                                                                                        \
+    if (qgz) return a ? launch_rs_tma_t<P, true, true>(r, *a, grid, s) : launch_rs_tma_t<P, false, true>(r, none, grid, s); \
+    return a ? launch_rs_tma_t<P, true, false>(r, *a, grid, s) : launch_rs_tma_t<P, false, false>(r, none, grid, s);
     HPZ_RST_CASE(1) HPZ_RST_CASE(2) HPZ_RST_CASE(3) HPZ_RST_CASE(4) HPZ_RST_CASE(5) HPZ_RST_CASE(6)
     HPZ_RST_CASE(7) HPZ_RST_CASE(8) HPZ_RST_CASE(9) HPZ_RST_CASE(10) HPZ_RST_CASE(11) HPZ_RST_CASE(12)
     HPZ_RST_CASE(13) HPZ_RST_CASE(14) HPZ_RST_CASE(15) HPZ_RST_CASE(16)

@@ -28,17 +28,18 @@ class ParityRun:
 
     def __init__(self, numels, world, node_size, dtype="bf16", align=256, order="fixed",
                  verify="exact", grad_kind="uniform", n_grad_slots=None, stock_schedule="program",
-                 fused=False, store_grad_shard=True, copy_engine="tma"):
+                 fused=False, store_grad_shard=True, copy_engine="tma", qgz=False):
         from paper_2407_01614_b200 import hpz as H
         from paper_2407_01614_b200.world import EmulatedWorld
         self.H = H
         self.numels, self.P, self.Pp, self.dtype = list(numels), world, node_size, dtype
         self.grad_kind = grad_kind
         self.fused, self.store_grad_shard = fused, store_grad_shard
+        self.qgz = qgz
         self.w = EmulatedWorld(numels, world, node_size, dtype=dtype, align=align, n_grad_slots=n_grad_slots,
-                               timeout_s=10.0)
+                               timeout_s=10.0, qgz=qgz)
         self.o = O.HpzOracle(self.numels, world, node_size, align=align, param_dtype=dtype, order=order,
-                             stock_schedule=stock_schedule, grad_kind=grad_kind)
+                             stock_schedule=stock_schedule, grad_kind=grad_kind, qgz=qgz)
         self.stream = torch.cuda.current_stream()
         for rc in self.w.ranks:
             H.hpz_set_order(rc.ctx, order)

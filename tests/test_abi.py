@@ -121,3 +121,28 @@ def test_baseline_layout_numbers(H):
         assert (info.numel_pad, info.shard, info.sec_shard) == (207071232, 25883904, 51767808)
     finally:
         H.hpz_finalize(ctx)
+
+
+def test_options_host_only(H):
+    ctx = H.hpz_init(8, 4, 0, -1)
+    try:
+        with pytest.raises(H.HpzError):
+            H.hpz_set_option(ctx, "qgz", 8)                # only INT4
+        with pytest.raises(H.HpzError):
+            H.hpz_set_option(ctx, 99, 1)
+        with pytest.raises(H.HpzError):
+            H.hpz_set_option(ctx, "copy_engine", 7)
+        H.hpz_set_option(ctx, "qgz", 4)
+        a_q = H.hpz_register_flat_params(ctx, [1_000_000, 2048])
+        with pytest.raises(H.HpzError) as e:                # sizes the arena: before register only
+            H.hpz_set_option(ctx, "qgz", 0)
+        assert e.value.code == H.HPZ_ESTATE
+    finally:
+        H.hpz_finalize(ctx)
+    ctx = H.hpz_init(8, 4, 0, -1)
+    try:
+        a = H.hpz_register_flat_params(ctx, [1_000_000, 2048])
+    finally:
+        H.hpz_finalize(ctx)
+    # qgZ adds int4 codes (N̂/2 B) + (min, scale) per 64 elements (N̂/8 B) per gradient slot
+    assert a_q - a >= (1_001_472 + 2048) * 0.625 - 4 * 4096

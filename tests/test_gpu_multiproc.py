@@ -44,3 +44,10 @@ def test_multiproc_parity_off():
 
 def test_multiproc_stock_shows_mismatches():
     _run(2, 2, order="stock", extra=("--stock-delay-us", "3000"), port=29691)
+
+
+@pytest.mark.parametrize("n,node", [(2, 1), (4, 2), (8, 4)])
+def test_multiproc_parity_qgz(n, node):
+    if n > NGPU:
+        pytest.skip(f"needs {n} GPUs")
+    _run(n, node, extra=("--qgz", "1"), port=29811 + n * 10 + node)

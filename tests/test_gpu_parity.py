@@ -45,7 +45,7 @@ def _check_step(run: ParityRun, rec, check_all=True):
             # a5 reduce-scatter bit-exact in the fixed order
             if run.store_grad_shard:
                 g_gpu = buffer_view(rc, i, "grad_shard", "f32").cpu().numpy()
-                g_ref = O.reduce_scatter(grads, lay, r)
+                g_ref = (O.qgz_reduce_scatter if run.qgz else O.reduce_scatter)(grads, lay, r)
                 assert np.array_equal(g_gpu.view(np.uint32), g_ref.view(np.uint32)), f"RS layer {i} rank {r}"
             # a6 Adam + bf16 refresh
             for kind, ref in (("master", st.master), ("m", st.m), ("v", st.v)):
@@ -88,6 +88,20 @@ def test_parity_fused_rs_adam(P, Pp, store, engine, verify):
             _check_step(run, run.step())
         c = run.counters()
         assert c["mismatches"] == 0 and c["timeouts"] == 0 and c["fp_mismatches"] == 0
+    finally:
+        run.close()
+
+
+@pytest.mark.parametrize("P,Pp", [(1, 1), (2, 1), (4, 2), (8, 4), (8, 1), (3, 3)])
+@pytest.mark.parametrize("fused", [True, False])
+def test_parity_qgz(P, Pp, fused):
+    """f1 qgZ: INT4 blockwise-quantized gradient all-to-all + fixed-order reduction, bit-exact
+    vs the oracle's qgz_reduce_scatter (same fp32 rounding decisions for every code)."""
+    run = ParityRun(NUMELS, P, Pp, qgz=True, fused=fused, verify="fingerprint")
+    try:
+        for _ in range(3):
+            _check_step(run, run.step())
+        assert run.counters()["timeouts"] == 0
     finally:
         run.close()
 
