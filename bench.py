@@ -313,12 +313,14 @@ def main():
         else:
             bound, peak, unit = "nvlink", 770.0, "GB/s"
     achieved = alg / (share[dom] * 1e-3) / 1e9          # per-launch bytes / per-launch time, summed over L launches
-    traffic = None
+    traffic = traffic_alg = traffic_src = None
     tr = ncu_traffic().get(f"{args.model}_P{world}_{dom}")
-    if tr:
-        traffic = tr.get("dram_bytes_per_launch")
+    if tr and not args.qgz:
+        # DRAM bytes of ONE captured launch (ncu --set full) next to that launch's algorithmic bytes
+        traffic, traffic_alg, traffic_src = tr["dram_bytes_per_launch"], tr["launch_alg_bytes"], tr["source"]
     roofline = {"bound": bound, "kernel": dom, "achieved": round(achieved, 1), "peak": peak, "unit": unit,
                 "frac": round(achieved / peak, 4), "traffic": traffic,
+                "traffic_launch_alg_bytes": traffic_alg, "traffic_source": traffic_src,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if bound == "hbm" else
                 "B200_PROFILING.md measured peer copy 770 GB/s per direction (900 nominal)",
                 "alg_bytes_per_step": alg, "launches_per_step": L, "ms_per_step": round(share[dom], 4),
