@@ -233,6 +233,10 @@ def main():
             rec("bwd1")
             if grads_from is not None:
                 H.hpz_grad_upload(ctx, i, grads_from.data_ptr(), infos[i].numel, stream)
+            if args.qgz:
+                rec("q0")
+                H.hpz_grads_ready(ctx, i, stream)      # qgZ: INT4-quantize my slot, publish E5
+                rec("q1")
             rec("rs0")
             if fused:
                 H.hpz_reduce_scatter_adam(ctx, i, adam, stream)   # RS + this layer's Adam
@@ -253,7 +257,7 @@ def main():
     barrier()
     if rank == 0:
         clocks.start()
-    evs = {k: [] for k in ("fwd0", "fwd1", "bwd0", "bwd1", "rs0", "rs1", "adam0", "adam1")}
+    evs = {k: [] for k in ("fwd0", "fwd1", "bwd0", "bwd1", "rs0", "rs1", "adam0", "adam1", "q0", "q1")}
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
     t_start.record(stream)
@@ -268,7 +272,7 @@ def main():
     K = args.steps
     step_ms = t_start.elapsed_time(t_end) / K
     tot = {k: sum(a.elapsed_time(b) for a, b in zip(evs[k + "0"], evs[k + "1"])) / K
-           for k in ("fwd", "bwd", "rs", "adam")}
+           for k in ("fwd", "bwd", "rs", "adam", "q")}
     # bytes per rank per step (algbw: AG output bytes, RS input bytes)
     ag_bytes = sum(x.numel_pad for x in infos) * e
     rs_bytes = sum(x.numel_pad for x in infos) * 4
@@ -280,10 +284,10 @@ def main():
     adam_bytes = sum(x.shard for x in infos) * (30 if dtype == "bf16" else 32)
 
     vals = max_over_ranks([step_ms, tot["fwd"], tot["bwd"], tot["rs"], tot["adam"],
-                           tot["fwd"] + tot["bwd"] + tot["rs"]], device=dev)
+                           tot["fwd"] + tot["bwd"] + tot["rs"] + tot["q"], tot["q"]], device=dev)
     stats = sum_over_ranks([cnt["fp_mismatches"], cnt["mismatches"], cnt["nan_reads"], cnt["timeouts"],
                             cnt["fp_checked"], launches], device=dev)
-    step_ms, fwd_ms, bwd_ms, rs_ms, adam_ms, coll_ms = vals
+    step_ms, fwd_ms, bwd_ms, rs_ms, adam_ms, coll_ms, q_ms = vals
     # whole-job throughput of the step: the collectives' algorithmic bytes of all ranks per
     # step / the max-over-ranks time of the whole step (incl. the optimizer)
     value = world * coll_bytes / (step_ms * 1e-3) / 1e9
@@ -392,6 +396,7 @@ def main():
                                        "layers_checked": int(stats[4])},
             "breakdown_ms_per_step": {"fwd_gather": round(fwd_ms, 3), "bwd_gather": round(bwd_ms, 3),
                                       rs_name: round(rs_ms, 3), "adam": round(adam_ms, 3),
+                                      "qgz_quantize": round(q_ms, 3),
                                       "collectives": round(coll_ms, 3)},
             "fused_rs_adam": fused,
             "nvlink_ingress_GBps_per_gpu": round(ingress / (step_ms * 1e-3) / 1e9, 2) if world > 1 else None,

@@ -44,14 +44,30 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  uint32_t done = 0;
-  while (!done) {
-    asm volatile(
-        "{ .reg .pred q; mbarrier.try_wait.parity.shared::cta.b64 q, [%1], %2; selp.u32 %0, 1, 0, q; }"
-        : "=r"(done)
-        : "r"(smem_u32(bar)), "r"(parity)
-        : "memory");
+__device__ __forceinline__ uint32_t mbar_try(uint64_t* bar, uint32_t parity) {
+  uint32_t done;
+  asm volatile(
+      "{ .reg .pred q; mbarrier.try_wait.parity.shared::cta.b64 q, [%1], %2; selp.u32 %0, 1, 0, q; }"
+      : "=r"(done)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return done;
+}
+__device__ __forceinline__ uint64_t globaltimer_();
+// Bounded mbarrier wait: a pipeline that never completes (lost bulk copy, aborted peer)
+// records a timeout and returns instead of hanging the GPU.
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity, const SyncCommon& sc) {
+  if (mbar_try(bar, parity)) return;
+  const uint64_t t0 = globaltimer_();
+  uint32_t spins = 0;
+  while (!mbar_try(bar, parity)) {
+    if ((++spins & 1023u) == 0 && globaltimer_() - t0 > sc.timeout_ns) {
+      atomicAdd(sc.timeouts, 1ull);
+      atomicExch(sc.abort_flag, 1u);
+      *sc.host_err = 1u;
+      __threadfence_system();
+      return;
+    }
   }
 }
 __device__ __forceinline__ void tma_load(void* sdst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
@@ -90,6 +106,7 @@ __device__ __forceinline__ uint64_t globaltimer() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
+__device__ __forceinline__ uint64_t globaltimer_() { return globaltimer(); }
 __device__ bool wait_geq(const uint32_t* flag, uint32_t target, const SyncCommon& s) {
   if (ld_acquire_sys(flag) >= target) return true;
   if (*(volatile uint32_t*)s.abort_flag) return false;
@@ -197,7 +214,7 @@ __global__ void __launch_bounds__(32 * (1 + kFpWarps), 1)
       for (int64_t k = 0; k < pre; ++k) issue_load(k);
       for (int64_t k = 0; k < nk; ++k) {
         const int s = (int)(k % kGatherStages);
-        mbar_wait(&full_bar[s], (uint32_t)((k / kGatherStages) & 1));
+        mbar_wait(&full_bar[s], (uint32_t)((k / kGatherStages) & 1), p.sync);
         int j;
         int64_t off;
         uint32_t bytes;
@@ -217,7 +234,7 @@ __global__ void __launch_bounds__(32 * (1 + kFpWarps), 1)
           // the stage of chunk k-1 is refilled: its stores must have read it ...
           bulk_wait_read<1>();
           // ... and the fingerprint warps must be done with it
-          if (FP && k >= 1) mbar_wait(&empty_bar[(k - 1) % kGatherStages], (uint32_t)(((k - 1) / kGatherStages) & 1));
+          if (FP && k >= 1) mbar_wait(&empty_bar[(k - 1) % kGatherStages], (uint32_t)(((k - 1) / kGatherStages) & 1), p.sync);
           issue_load(k + kGatherStages - 1);
         }
       }
@@ -230,7 +247,7 @@ __global__ void __launch_bounds__(32 * (1 + kFpWarps), 1)
     const int ct = threadIdx.x - 32;
     for (int64_t k = 0; k < nk; ++k) {
       const int s = (int)(k % kGatherStages);
-      mbar_wait(&full_bar[s], (uint32_t)((k / kGatherStages) & 1));
+      mbar_wait(&full_bar[s], (uint32_t)((k / kGatherStages) & 1), p.sync);
       int j;
       int64_t off;
       uint32_t bytes;
@@ -330,7 +347,7 @@ __global__ void __launch_bounds__(32 + kRsConsumers, 1)
     if (lane == 0) {
       for (int64_t k = 0; k < nk; ++k) {
         const int s = (int)(k % C::kStages);
-        if (k >= C::kStages) mbar_wait(&empty_bar[s], (uint32_t)(((k / C::kStages) - 1) & 1));
+        if (k >= C::kStages) mbar_wait(&empty_bar[s], (uint32_t)(((k / C::kStages) - 1) & 1), r.sync);
         const int64_t e0 = (blockIdx.x + k * gridDim.x) * (int64_t)kRsChunk;
         const int64_t rem = n - e0;
         const uint32_t cnt = (uint32_t)(rem < kRsChunk ? rem : kRsChunk);
@@ -360,7 +377,7 @@ __global__ void __launch_bounds__(32 + kRsConsumers, 1)
     const int ct = threadIdx.x - 32;     // 0..255: one float4 of the 1024-element chunk
     for (int64_t k = 0; k < nk; ++k) {
       const int s = (int)(k % C::kStages);
-      mbar_wait(&full_bar[s], (uint32_t)((k / C::kStages) & 1));
+      mbar_wait(&full_bar[s], (uint32_t)((k / C::kStages) & 1), r.sync);
       const int64_t e0 = (blockIdx.x + k * gridDim.x) * (int64_t)kRsChunk;
       const int64_t rem = n - e0;
       const int cnt = (int)(rem < kRsChunk ? rem : kRsChunk);
