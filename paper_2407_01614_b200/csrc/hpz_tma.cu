@@ -304,12 +304,14 @@ __device__ __forceinline__ void adam1(float& w, float& m, float& v, float g, con
 
 template <int P, bool ADAM, bool QGZ>
 struct RsCfg {
-  // per stage: P gradient slices (fp32, or qgZ int4 codes + (min, scale) per 64) (+ w, m, v)
-  static constexpr int kCodeBytes = kRsChunk / 2;
-  static constexpr int kParamBytes = kRsChunk / kQgzBlock * 8;
-  static constexpr int kSrcBytes = QGZ ? kCodeBytes + kParamBytes : kRsChunk * 4;
+  // per stage: P gradient slices (fp32, or qgZ int4 codes + (min, scale) per 64) (+ w, m, v);
+  // qgZ chunks are longer so its small code/param copies stay >= 1 KiB / 256 B
+  static constexpr int kChunk = QGZ ? 2 * kRsChunk : kRsChunk;
+  static constexpr int kCodeBytes = kChunk / 2;
+  static constexpr int kParamBytes = kChunk / kQgzBlock * 8;
+  static constexpr int kSrcBytes = QGZ ? kCodeBytes + kParamBytes : kChunk * 4;
   static constexpr int kWmvOff = P * kSrcBytes;
-  static constexpr int kStageBytes = kWmvOff + (ADAM ? 3 * kRsChunk * 4 : 0);
+  static constexpr int kStageBytes = kWmvOff + (ADAM ? 3 * kChunk * 4 : 0);
   static constexpr int kStages = (200 * 1024) / kStageBytes >= 6 ? 6 : (200 * 1024) / kStageBytes;
 };
 
@@ -323,7 +325,7 @@ __global__ void __launch_bounds__(32 + kRsConsumers, 1)
   __shared__ __align__(8) uint64_t full_bar[C::kStages];
   __shared__ __align__(8) uint64_t empty_bar[C::kStages];
   const int64_t n = r.n_vec * 4;   // shard elements (multiple of 256)
-  const int64_t total = (n + kRsChunk - 1) / kRsChunk;
+  const int64_t total = (n + C::kChunk - 1) / C::kChunk;
   const int64_t nk = blockIdx.x < total ? (total - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -348,9 +350,9 @@ __global__ void __launch_bounds__(32 + kRsConsumers, 1)
       for (int64_t k = 0; k < nk; ++k) {
         const int s = (int)(k % C::kStages);
         if (k >= C::kStages) mbar_wait(&empty_bar[s], (uint32_t)(((k / C::kStages) - 1) & 1), r.sync);
-        const int64_t e0 = (blockIdx.x + k * gridDim.x) * (int64_t)kRsChunk;
+        const int64_t e0 = (blockIdx.x + k * gridDim.x) * (int64_t)C::kChunk;
         const int64_t rem = n - e0;
-        const uint32_t cnt = (uint32_t)(rem < kRsChunk ? rem : kRsChunk);
+        const uint32_t cnt = (uint32_t)(rem < C::kChunk ? rem : C::kChunk);
         const uint32_t bytes = cnt * 4;
         char* st = smem + (size_t)s * C::kStageBytes;
         const uint32_t src_bytes = QGZ ? cnt / 2 + cnt / kQgzBlock * 8 : bytes;
@@ -367,23 +369,23 @@ __global__ void __launch_bounds__(32 + kRsConsumers, 1)
         }
         if (ADAM) {
           float* wmv = reinterpret_cast<float*>(st + C::kWmvOff);
-          tma_load(wmv + 0 * kRsChunk, a.w + e0, bytes, &full_bar[s]);
-          tma_load(wmv + 1 * kRsChunk, a.m + e0, bytes, &full_bar[s]);
-          tma_load(wmv + 2 * kRsChunk, a.v + e0, bytes, &full_bar[s]);
+          tma_load(wmv + 0 * C::kChunk, a.w + e0, bytes, &full_bar[s]);
+          tma_load(wmv + 1 * C::kChunk, a.m + e0, bytes, &full_bar[s]);
+          tma_load(wmv + 2 * C::kChunk, a.v + e0, bytes, &full_bar[s]);
         }
       }
     }
   } else {
-    const int ct = threadIdx.x - 32;     // 0..255: one float4 of the 1024-element chunk
     for (int64_t k = 0; k < nk; ++k) {
       const int s = (int)(k % C::kStages);
       mbar_wait(&full_bar[s], (uint32_t)((k / C::kStages) & 1), r.sync);
-      const int64_t e0 = (blockIdx.x + k * gridDim.x) * (int64_t)kRsChunk;
+      const int64_t e0 = (blockIdx.x + k * gridDim.x) * (int64_t)C::kChunk;
       const int64_t rem = n - e0;
-      const int cnt = (int)(rem < kRsChunk ? rem : kRsChunk);
+      const int cnt = (int)(rem < C::kChunk ? rem : C::kChunk);
       const char* stc = smem + (size_t)s * C::kStageBytes;
       const float4* wmv = reinterpret_cast<const float4*>(stc + C::kWmvOff);
-      if (ct * 4 < cnt) {
+      // consumer thread ct handles float4s ct, ct+256, ... of the chunk
+      for (int ct = threadIdx.x - 32; ct * 4 < cnt; ct += kRsConsumers) {
         float4 x[P];
 #pragma unroll
         for (int j = 0; j < P; ++j) {
@@ -408,9 +410,9 @@ __global__ void __launch_bounds__(32 + kRsConsumers, 1)
         const int64_t i = e0 / 4 + ct;   // float4 index in the shard
         if (r.out) reinterpret_cast<float4*>(r.out)[i] = g;
         if (ADAM) {
-          float4 w = wmv[0 * (kRsChunk / 4) + ct];
-          float4 m = wmv[1 * (kRsChunk / 4) + ct];
-          float4 v = wmv[2 * (kRsChunk / 4) + ct];
+          float4 w = wmv[0 * (C::kChunk / 4) + ct];
+          float4 m = wmv[1 * (C::kChunk / 4) + ct];
+          float4 v = wmv[2 * (C::kChunk / 4) + ct];
           adam1(w.x, m.x, v.x, g.x, a);
           adam1(w.y, m.y, v.y, g.y, a);
           adam1(w.z, m.z, v.z, g.z, a);
@@ -455,45 +457,64 @@ cudaError_t launch_rs_tma_t(const RSParams& r, const AdamParams& a, int grid, cu
   return cudaGetLastError();
 }
 
-// qgZ quantizer: 16 threads per 64-element block (one float4 each); block min/max by
-// shuffles; NaN anywhere in a block makes its (min, scale) NaN so it surfaces after
-// dequantization.  fp32, one IEEE op per operator, round-half-to-even codes — the
-// oracle's quantize_blockwise decisions, bit for bit.
+// qgZ quantizer: 16 threads per 64-element block (one float4 each), kQU blocks per
+// half-warp in flight (ILP); block min/max by shuffles; NaN anywhere in a block makes its
+// (min, scale) NaN so it surfaces after dequantization.  fp32, one IEEE op per operator,
+// round-half-to-even codes — the oracle's quantize_blockwise decisions, bit for bit.
+constexpr int kQU = 4;
 __global__ void __launch_bounds__(256) qgz_quantize_kernel(const __grid_constant__ QuantParams q) {
   if (threadIdx.x == 0 && q.war.n) wait_all(q.war, q.sync);   // E6: peers done with the old codes
   __syncthreads();
   const int64_t n_blocks = q.n / kQgzBlock;
   const int sub = threadIdx.x & 15;
-  const int64_t b_stride = (int64_t)gridDim.x * (blockDim.x / 16);
-  for (int64_t b = (int64_t)blockIdx.x * (blockDim.x / 16) + (threadIdx.x >> 4); b < n_blocks; b += b_stride) {
-    const float4 v = reinterpret_cast<const float4*>(q.g)[b * 16 + sub];
-    bool nan = isnan(v.x) || isnan(v.y) || isnan(v.z) || isnan(v.w);
-    float mn = fminf(fminf(v.x, v.y), fminf(v.z, v.w));
-    float mx = fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w));
+  const int64_t hw = (int64_t)blockIdx.x * (blockDim.x / 16) + (threadIdx.x >> 4);   // half-warp id
+  const int64_t n_hw = (int64_t)gridDim.x * (blockDim.x / 16);
+  for (int64_t b0 = hw * kQU; b0 < n_blocks; b0 += n_hw * kQU) {
+    float4 v[kQU];
+#pragma unroll
+    for (int u = 0; u < kQU; ++u)
+      if (b0 + u < n_blocks) v[u] = reinterpret_cast<const float4*>(q.g)[(b0 + u) * 16 + sub];
+    float mn[kQU], mx[kQU];
+    int nan[kQU];
+#pragma unroll
+    for (int u = 0; u < kQU; ++u) {
+      if (b0 + u >= n_blocks) v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      nan[u] = isnan(v[u].x) || isnan(v[u].y) || isnan(v[u].z) || isnan(v[u].w);
+      mn[u] = fminf(fminf(v[u].x, v[u].y), fminf(v[u].z, v[u].w));
+      mx[u] = fmaxf(fmaxf(v[u].x, v[u].y), fmaxf(v[u].z, v[u].w));
+    }
 #pragma unroll
     for (int o = 8; o > 0; o >>= 1) {
-      mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-      nan = nan || __shfl_xor_sync(0xffffffffu, (int)nan, o);
-    }
-    float scale = __fdiv_rn(__fsub_rn(mx, mn), 15.0f);
-    if (nan) {
-      mn = __int_as_float(0x7fc00000);
-      scale = mn;
-    }
-    uint32_t packed = 0;
-    const float e[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      int c = 0;
-      if (scale > 0.0f) {
-        c = __float2int_rn(__fdiv_rn(__fsub_rn(e[k], mn), scale));
-        c = c < 0 ? 0 : (c > 15 ? 15 : c);
+      for (int u = 0; u < kQU; ++u) {
+        mn[u] = fminf(mn[u], __shfl_xor_sync(0xffffffffu, mn[u], o));
+        mx[u] = fmaxf(mx[u], __shfl_xor_sync(0xffffffffu, mx[u], o));
+        nan[u] |= __shfl_xor_sync(0xffffffffu, nan[u], o);
       }
-      packed |= (uint32_t)c << (4 * k);
     }
-    reinterpret_cast<uint16_t*>(q.codes)[b * 16 + sub] = (uint16_t)packed;
-    if (sub == 0) q.params[b] = make_float2(mn, scale);
+#pragma unroll
+    for (int u = 0; u < kQU; ++u) {
+      if (b0 + u >= n_blocks) continue;
+      float m0 = mn[u];
+      float scale = __fdiv_rn(__fsub_rn(mx[u], m0), 15.0f);
+      if (nan[u]) {
+        m0 = __int_as_float(0x7fc00000);
+        scale = m0;
+      }
+      uint32_t packed = 0;
+      const float e[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        int c = 0;
+        if (scale > 0.0f) {
+          c = __float2int_rn(__fdiv_rn(__fsub_rn(e[k], m0), scale));
+          c = c < 0 ? 0 : (c > 15 ? 15 : c);
+        }
+        packed |= (uint32_t)c << (4 * k);
+      }
+      reinterpret_cast<uint16_t*>(q.codes)[(b0 + u) * 16 + sub] = (uint16_t)packed;
+      if (sub == 0) q.params[b0 + u] = make_float2(m0, scale);
+    }
   }
 }
 
