@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--ctas-per-sm", type=int, default=None)
     ap.add_argument("--copy-engine", default="tma", choices=["tma", "ldg"])
     ap.add_argument("--qgz", action="store_true", help="ZeRO++ qgZ: INT4 gradient all-to-all (SURVEY f1)")
+    ap.add_argument("--grad-dtype", default="f32", choices=["f32", "bf16"],
+                    help="gradient slot dtype (bf16: SURVEY f4, fp32 accumulation)")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -184,10 +186,10 @@ def main():
 
     if world > 1:
         W = DistWorld(numels, node_size, dtype=dtype, n_grad_slots=L, device=local_rank, timeout_s=60.0,
-                      qgz=args.qgz)
+                      qgz=args.qgz, grad_dtype=args.grad_dtype)
     else:
         W = EmulatedWorld(numels, 1, 1, dtype=dtype, n_grad_slots=L, device=local_rank, timeout_s=60.0,
-                          qgz=args.qgz)
+                          qgz=args.qgz, grad_dtype=args.grad_dtype)
     rc = W.ranks[0]
     ctx = rc.ctx
     H.hpz_set_order(ctx, args.order)
@@ -279,6 +281,8 @@ def main():
     coll_bytes = 2 * ag_bytes + rs_bytes
     # NVLink ingress per rank per step (busbw convention)
     P, Pp = world, node_size
+    gsz = 2 if args.grad_dtype == "bf16" else 4
+    rs_bytes = sum(x.numel_pad for x in infos) * gsz      # RS input bytes in the slot dtype
     rs_wire = rs_bytes * (0.625 / 4 if args.qgz else 1.0)
     ingress = ag_bytes * (P - 1) / P + ag_bytes * (Pp - 1) / Pp + rs_wire * (P - 1) / P
     adam_bytes = sum(x.shard for x in infos) * (30 if dtype == "bf16" else 32)
@@ -333,11 +337,15 @@ def main():
     # ------------------------------------------------ end-to-end arm (host buffers)
     e2e = None
     if not args.no_e2e and args.e2e_steps > 0:
-        host = torch.empty(max(x.numel for x in infos), dtype=torch.float32, pin_memory=True)
+        host = torch.empty(max(x.numel for x in infos), pin_memory=True,
+                           dtype=torch.bfloat16 if args.grad_dtype == "bf16" else torch.float32)
         H.hpz_synth_grads(ctx, 0, S.stream_key(S.SEED_GRADS, 0, 0, rank), S.GRAD_SCALE, 0, stream)
         # fill the pinned buffer with this rank's synthetic gradient values (device generator)
         from paper_2407_01614_b200.world import buffer_view
         src = buffer_view(rc, 0, "grad_slot", "f32")
+        if args.grad_dtype == "bf16":
+            from paper_2407_01614_b200.world import device_view
+            src = device_view(H.hpz_buffer(ctx, 0, "grad_slot")[0], infos[0].numel_pad, "bf16")
         host[: infos[0].numel].copy_(src[: infos[0].numel])
         one_step(grads_from=host)          # warm-up of the e2e path
         barrier()
@@ -354,7 +362,7 @@ def main():
         barrier()
         e2e_ms = max_over_ranks([a.elapsed_time(b) / args.e2e_steps], device=dev)[0]
         e2e = {"value": round(world * coll_bytes / (e2e_ms * 1e-3) / 1e9, 2), "unit": "GB/s",
-               "h2d_bytes_per_step": sum(x.numel for x in infos) * 4, "d2h_bytes_per_step": 5 * 8,
+               "h2d_bytes_per_step": sum(x.numel for x in infos) * gsz, "d2h_bytes_per_step": 5 * 8,
                "ms_per_step": round(e2e_ms, 3),
                "note": "through the C ABI: every layer's fp32 gradient uploaded from pinned host memory "
                        "(hpz_grad_upload) inside the timed step; counters read back (hpz_counters)"}
@@ -386,6 +394,7 @@ def main():
                        "verify": args.verify, "copy_engine": args.copy_engine,
                        "qgz": "int4 blockwise (64) gradient all-to-all; RS bytes counted as the fp32 "
                               "gradient bytes reduced, wire bytes 0.625 B/elem" if args.qgz else None,
+                       "grad_dtype": args.grad_dtype,
                        "l2": "no flush: per-step working set >> 126 MB L2 (every layer buffer is "
                              "touched once per phase)",
                        "value_def": "sum over ranks of AllGather output bytes (fwd+bwd) + ReduceScatter "

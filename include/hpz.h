@@ -229,14 +229,15 @@ HPZ_API int hpz_fwd_gather(hpz_ctx* ctx, int layer, void* full_out, void* stream
  * primaries.  ESTATE if the layer's forward gather of step t was not issued. */
 HPZ_API int hpz_bwd_gather(hpz_ctx* ctx, int layer, void* full_out, void* stream);
 
-/* The gradient slot (fp32, numel_pad elements, device) the caller fills with this rank's
+/* The gradient slot (fp32 — or bf16 with HPZ_OPT_GRAD_DTYPE — numel_pad elements, device)
+ * the caller fills with this rank's
  * local gradient of `layer` (zero in padding).  Enqueues on `stream` the wait for every
  * rank's reduce-scatter of the slot's previous use (E6) before returning the pointer. */
-HPZ_API int hpz_grad_buffer(hpz_ctx* ctx, int layer, float** grad_slot, void* stream);
+HPZ_API int hpz_grad_buffer(hpz_ctx* ctx, int layer, void** grad_slot, void* stream);
 
-/* hpz_grad_buffer + copy of n <= numel fp32 values from `src` (host or device) into the
+/* hpz_grad_buffer + copy of n <= numel gradient values (fp32 or bf16) from `src` (host or device) into the
  * slot, zero-filling [n, numel_pad).  The end-to-end entry point for host gradients. */
-HPZ_API int hpz_grad_upload(hpz_ctx* ctx, int layer, const float* src, int64_t n, void* stream);
+HPZ_API int hpz_grad_upload(hpz_ctx* ctx, int layer, const void* src, int64_t n, void* stream);
 
 /* hpz_grad_buffer + fill the slot on the device with the seeded generator (kind 0:
  * uniform*scale, 1: dyadic grid), zero in padding. */
@@ -272,7 +273,7 @@ typedef enum {
   HPZ_OPT_STORE_GRAD_SHARD = 0,  /* 0/1: fused RS+Adam writes the reduced gradient shard */
   HPZ_OPT_CTAS_PER_SM = 1,       /* 1..32: persistent-grid CTAs per SM of the LDG/STG kernels */
   HPZ_OPT_COPY_ENGINE = 2,       /* HPZ_COPY_TMA (default) or HPZ_COPY_LDG */
-  HPZ_OPT_QGZ = 3                /* 0 (default) or 4: ZeRO++ qgZ (Alg. 1 comment
+  HPZ_OPT_QGZ = 3,               /* 0 (default) or 4: ZeRO++ qgZ (Alg. 1 comment
                                     PAPER.md:114 "Replaced with INT4 AllToAll if with qgZ").
                                     The reduce-scatter quantizes this rank's gradient slot
                                     blockwise to INT4 (64-element blocks, fp32 min + scale,
@@ -281,6 +282,10 @@ typedef enum {
                                     4), dequantizes (min + code*scale) and reduces in the R7
                                     order.  Set BEFORE hpz_register_flat_params (it sizes the
                                     arena).  With qgZ, hpz_grads_ready also quantizes. */
+  HPZ_OPT_GRAD_DTYPE = 4         /* HPZ_F32 (default) or HPZ_BF16: gradient slots hold
+                                    bf16; the reduce-scatter converts (exactly) to fp32 and
+                                    reduces in fp32 in the R7 order — half the NVLink bytes.
+                                    Set before hpz_register_flat_params; not with qgZ. */
 } hpz_option;
 /* Copy engine of the gathers and the reduce-scatter: TMA 1-D bulk copies through a
  * shared-memory stage ring (cp.async.bulk, one persistent CTA per SM), or 16-byte

@@ -423,6 +423,7 @@ class HpzOracle:
     toy_identical_batches: bool = False
     half_seed: int = 1234
     qgz: bool = False                    # f1: INT4 quantized gradient all-to-all (qgz_reduce_scatter)
+    grad_dtype: str = "f32"              # f4: "bf16" = gradients stored/communicated as bf16 (RNE)
 
     def __post_init__(self):
         check_topology(self.world, self.node_size)
@@ -468,6 +469,8 @@ class HpzOracle:
             else:
                 G.append([S.layer_grads(i, t, r, lay.numel, lay.numel_pad, kind=self.grad_kind)
                           for i, lay in enumerate(self.layouts)])
+            if self.grad_dtype == "bf16":     # f4: the slot holds bf16; widening to fp32 is exact
+                G[-1] = [bf16_to_f32(bf16_rne(g)) for g in G[-1]]
         return G, (float(np.mean(losses)) if losses else None)
 
     # --- one training step (Alg. 1 While body) ---------------

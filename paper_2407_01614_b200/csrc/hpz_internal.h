@@ -79,7 +79,8 @@ struct QuantParams {
 struct RSParams {
   const uint8_t* qcodes[kMaxWorld];    // qgZ: rank j's codes of my shard (peer-mapped), or unused
   const float2* qparams[kMaxWorld];    // qgZ: rank j's (min, scale) of my shard's blocks
-  const float* src[kMaxWorld];         // src[j] = rank j's gradient slot + r*shard (peer-mapped)
+  const float* src[kMaxWorld];         // src[j] = rank j's gradient slot + r*shard (peer-mapped);
+                                       // with bf16 gradients the pointer addresses __nv_bfloat16 data
   float* out;                          // local gradient shard
   int64_t n_vec;                       // shard / 4
   float inv_p;
@@ -115,8 +116,9 @@ cudaError_t launch_rs_adam(const RSParams& r, const AdamParams& a, int world, in
 // TMA (cp.async.bulk) variants, one persistent CTA per SM (hpz_tma.cu).  The gather
 // variant does not implement EXACT verification (p.mism must be nullptr).
 cudaError_t launch_gather_tma(const GatherParams& p, int grid, cudaStream_t s);
+// mode: 0 fp32 gradients, 1 bf16 gradients (fp32 accumulation), 2 qgZ INT4 codes
 cudaError_t launch_rs_tma(const RSParams& r, const AdamParams* a, int world, int grid, cudaStream_t s,
-                          bool qgz = false);
+                          int mode = 0);
 cudaError_t launch_qgz_quantize(const QuantParams& q, int grid, cudaStream_t s);
 cudaError_t launch_wait(const WaitList& w, const SyncCommon& sync, cudaStream_t s);
 cudaError_t launch_release(const ReleaseList& r, cudaStream_t s);
@@ -127,6 +129,9 @@ cudaError_t launch_delay(int us, cudaStream_t s);
 // e >= numel are 0.  kind 0: uniform*scale, 1: dyadic.
 cudaError_t launch_synth_f32(float* dst, int64_t n, int64_t e0, int64_t numel, uint64_t key,
                              float scale, int kind, int grid, cudaStream_t s);
+// Same generator, each value rounded to bf16 (RNE).
+cudaError_t launch_synth_bf16(void* dst, int64_t n, int64_t e0, int64_t numel, uint64_t key,
+                              float scale, int kind, int grid, cudaStream_t s);
 // Master init from a generator or an fp32 source (src == nullptr: generator), m = v = 0,
 // primary = rne(master).  n = shard elements, e0 = rank*shard.
 cudaError_t launch_init_shard(float* master, float* m, float* v, void* prim, int prim_bf16,

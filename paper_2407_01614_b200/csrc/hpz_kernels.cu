@@ -488,6 +488,16 @@ __global__ void __launch_bounds__(kThreads) synth_kernel(float* dst, int64_t n, 
   }
 }
 
+__global__ void __launch_bounds__(kThreads) synth_bf16_kernel(__nv_bfloat16* dst, int64_t n, int64_t e0,
+                                                              int64_t numel, uint64_t key, float scale,
+                                                              int kind) {
+  for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * kThreads) {
+    const int64_t e = e0 + i;
+    dst[i] = __float2bfloat16_rn(e < numel ? synth_value(key, e, scale, kind) : 0.0f);
+  }
+}
+
 __global__ void __launch_bounds__(kThreads) init_shard_kernel(float* master, float* m, float* v,
                                                               void* prim, int prim_bf16,
                                                               const float* src_full, int64_t n,
@@ -583,6 +593,13 @@ cudaError_t launch_delay(int us, cudaStream_t s) {
 cudaError_t launch_synth_f32(float* dst, int64_t n, int64_t e0, int64_t numel, uint64_t key,
                              float scale, int kind, int grid, cudaStream_t s) {
   synth_kernel<<<grid, kThreads, 0, s>>>(dst, n, e0, numel, key, scale, kind);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_synth_bf16(void* dst, int64_t n, int64_t e0, int64_t numel, uint64_t key,
+                              float scale, int kind, int grid, cudaStream_t s) {
+  synth_bf16_kernel<<<grid, kThreads, 0, s>>>(reinterpret_cast<__nv_bfloat16*>(dst), n, e0, numel, key, scale,
+                                              kind);
   return cudaGetLastError();
 }
 

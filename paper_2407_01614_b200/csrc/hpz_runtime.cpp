@@ -62,6 +62,7 @@ struct hpz_ctx {
   int ctas_per_sm = 4;                    // LDG/STG kernels
   int copy_engine = HPZ_COPY_TMA;
   int qgz_bits = 0;                       // f1: 4 = INT4 quantized gradient all-to-all
+  int grad_bytes = 4;                     // f4: 2 = bf16 gradients (fp32 accumulation)
   std::vector<uint64_t> off_qcodes, off_qparams;   // per grad slot (qgZ)
   std::string err;
 
@@ -150,7 +151,8 @@ cudaError_t gather_launch(const hpz_ctx* c, const GatherParams& p, cudaStream_t 
 }
 
 cudaError_t rs_launch(const hpz_ctx* c, const RSParams& r, const AdamParams* a, cudaStream_t s) {
-  if (c->qgz_bits) return launch_rs_tma(r, a, c->world, grid_for(c, (r.n_vec * 4 + 1023) / 1024, 1), s, true);
+  if (c->qgz_bits || c->grad_bytes == 2)   // qgZ codes / bf16 gradients: TMA engine only
+    return launch_rs_tma(r, a, c->world, grid_for(c, (r.n_vec * 4 + 1023) / 1024, 1), s, c->qgz_bits ? 2 : 1);
   if (c->copy_engine == HPZ_COPY_TMA)
     return launch_rs_tma(r, a, c->world, grid_for(c, (r.n_vec * 4 + 1023) / 1024, 1), s);
   const int grid = grid_for(c, (r.n_vec + 511) / 512, c->ctas_per_sm);
@@ -298,7 +300,7 @@ int hpz_register_flat_params(hpz_ctx* c, int n_layers, const int64_t* numel, int
   c->off_qparams.assign(n_grad_slots, 0);
   for (int s = 0; s < n_grad_slots; ++s) {
     c->off_slot[s] = off;
-    off = align_up(off + (uint64_t)c->slot_numel[s] * 4, kBufAlign);
+    off = align_up(off + (uint64_t)c->slot_numel[s] * c->grad_bytes, kBufAlign);
     if (c->qgz_bits) {   // int4 codes + (min, scale) per 64-element block
       c->off_qcodes[s] = off;
       off = align_up(off + (uint64_t)c->slot_numel[s] / 2, kBufAlign);
@@ -657,32 +659,37 @@ int hpz_bwd_gather(hpz_ctx* c, int layer, void* full_out, void* stream) {
   return HPZ_OK;
 }
 
-int hpz_grad_buffer(hpz_ctx* c, int layer, float** slot_ptr, void* stream) {
+int hpz_grad_buffer(hpz_ctx* c, int layer, void** slot_ptr, void* stream) {
   if (int rc = check_ready(c)) return rc;
   if (int rc = check_layer(c, layer)) return rc;
   if (int rc = slot_acquire(c, layer, static_cast<cudaStream_t>(stream))) return rc;
-  if (slot_ptr) *slot_ptr = reinterpret_cast<float*>(c->arena[c->rank] + c->off_slot[c->layers[layer].slot]);
+  if (slot_ptr) *slot_ptr = c->arena[c->rank] + c->off_slot[c->layers[layer].slot];
   return HPZ_OK;
 }
 
-int hpz_grad_upload(hpz_ctx* c, int layer, const float* src, int64_t n, void* stream) {
-  float* slot = nullptr;
+int hpz_grad_upload(hpz_ctx* c, int layer, const void* src, int64_t n, void* stream) {
+  void* slot = nullptr;
   if (int rc = hpz_grad_buffer(c, layer, &slot, stream)) return rc;
   const Layer& L = c->layers[layer];
   if (!src || n < 0 || n > L.numel) return fail(c, HPZ_EINVAL, "bad gradient source or length");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  HPZ_CUDA(c, cudaMemcpyAsync(slot, src, (size_t)n * 4, cudaMemcpyDefault, s));
-  if (n < L.numel_pad) HPZ_CUDA(c, cudaMemsetAsync(slot + n, 0, (size_t)(L.numel_pad - n) * 4, s));
+  const size_t gb = (size_t)c->grad_bytes;
+  HPZ_CUDA(c, cudaMemcpyAsync(slot, src, (size_t)n * gb, cudaMemcpyDefault, s));
+  if (n < L.numel_pad)
+    HPZ_CUDA(c, cudaMemsetAsync(static_cast<char*>(slot) + n * gb, 0, (size_t)(L.numel_pad - n) * gb, s));
   return HPZ_OK;
 }
 
 int hpz_synth_grads(hpz_ctx* c, int layer, uint64_t key, float scale, int kind, void* stream) {
-  float* slot = nullptr;
+  void* slot = nullptr;
   if (int rc = hpz_grad_buffer(c, layer, &slot, stream)) return rc;
   if (kind != 0 && kind != 1) return fail(c, HPZ_EINVAL, "bad generator kind");
   const Layer& L = c->layers[layer];
-  cudaError_t e = launch_synth_f32(slot, L.numel_pad, 0, L.numel, key, scale, kind,
-                                   grid_for(c, (L.numel_pad + 255) / 256, 8), static_cast<cudaStream_t>(stream));
+  const int grid = grid_for(c, (L.numel_pad + 255) / 256, 8);
+  cudaError_t e = c->grad_bytes == 2
+                      ? launch_synth_bf16(slot, L.numel_pad, 0, L.numel, key, scale, kind, grid, static_cast<cudaStream_t>(stream))
+                      : launch_synth_f32(static_cast<float*>(slot), L.numel_pad, 0, L.numel, key, scale, kind, grid,
+                                         static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return fail(c, HPZ_ECUDA, "synth launch: %s", cudaGetErrorString(e));
   c->launches += 1;
   return HPZ_OK;
@@ -729,7 +736,7 @@ static void build_rs(hpz_ctx* c, int layer, RSParams& p) {
   const uint32_t u1 = epoch(c->slot_use[slot] + 1);
   p = RSParams{};
   for (int j = 0; j < c->world; ++j)
-    p.src[j] = reinterpret_cast<const float*>(c->arena[j] + c->off_slot[slot]) + (int64_t)c->rank * L.shard;
+    p.src[j] = reinterpret_cast<const float*>(c->arena[j] + c->off_slot[slot] + (uint64_t)c->rank * L.shard * c->grad_bytes);
   p.out = reinterpret_cast<float*>(c->arena[c->rank] + L.off_gshard);
   p.n_vec = L.shard / 4;
   p.inv_p = (float)(1.0 / c->world);
@@ -886,7 +893,14 @@ int hpz_set_option(hpz_ctx* c, int option, int64_t value) {
     case HPZ_OPT_QGZ:
       if (c->registered) return fail(c, HPZ_ESTATE, "qgZ must be chosen before hpz_register_flat_params");
       if (value != 0 && value != 4) return fail(c, HPZ_EINVAL, "qgZ bits must be 0 (off) or 4");
+      if (value && c->grad_bytes != 4) return fail(c, HPZ_EINVAL, "qgZ quantizes fp32 gradients");
       c->qgz_bits = (int)value;
+      return HPZ_OK;
+    case HPZ_OPT_GRAD_DTYPE:
+      if (c->registered) return fail(c, HPZ_ESTATE, "the gradient dtype must be chosen before hpz_register_flat_params");
+      if (value != HPZ_F32 && value != HPZ_BF16) return fail(c, HPZ_EINVAL, "gradient dtype must be HPZ_F32 or HPZ_BF16");
+      if (value == HPZ_BF16 && c->qgz_bits) return fail(c, HPZ_EINVAL, "qgZ quantizes fp32 gradients");
+      c->grad_bytes = value == HPZ_BF16 ? 2 : 4;
       return HPZ_OK;
     case HPZ_OPT_COPY_ENGINE:
       if (value != HPZ_COPY_LDG && value != HPZ_COPY_TMA) return fail(c, HPZ_EINVAL, "copy engine must be 0 (LDG) or 1 (TMA)");

@@ -302,24 +302,29 @@ __device__ __forceinline__ void adam1(float& w, float& m, float& v, float g, con
   w = __fsub_rn(w, __fmul_rn(p.step_size, __fdiv_rn(m, d)));
 }
 
-template <int P, bool ADAM, bool QGZ>
+enum RsMode { RS_F32 = 0, RS_BF16 = 1, RS_QGZ = 2 };
+
+template <int P, bool ADAM, int MODE>
 struct RsCfg {
+  static constexpr bool QGZ = MODE == RS_QGZ;
   // per stage: P gradient slices (fp32, or qgZ int4 codes + (min, scale) per 64) (+ w, m, v);
   // qgZ chunks are longer so its small code/param copies stay >= 1 KiB / 256 B
   static constexpr int kChunk = QGZ ? 2 * kRsChunk : kRsChunk;
   static constexpr int kCodeBytes = kChunk / 2;
   static constexpr int kParamBytes = kChunk / kQgzBlock * 8;
-  static constexpr int kSrcBytes = QGZ ? kCodeBytes + kParamBytes : kChunk * 4;
+  static constexpr int kSrcBytes = QGZ ? kCodeBytes + kParamBytes : kChunk * (MODE == RS_BF16 ? 2 : 4);
   static constexpr int kWmvOff = P * kSrcBytes;
   static constexpr int kStageBytes = kWmvOff + (ADAM ? 3 * kChunk * 4 : 0);
   static constexpr int kStages = (200 * 1024) / kStageBytes >= 6 ? 6 : (200 * 1024) / kStageBytes;
 };
 
 // Block = 1 producer warp + 8 consumer warps.  Dynamic smem = kStages * kStageBytes.
-template <int P, bool ADAM, bool QGZ>
+template <int P, bool ADAM, int MODE>
 __global__ void __launch_bounds__(32 + kRsConsumers, 1)
     rs_tma_kernel(const __grid_constant__ RSParams r, const __grid_constant__ AdamParams a) {
-  using C = RsCfg<P, ADAM, QGZ>;
+  using C = RsCfg<P, ADAM, MODE>;
+  constexpr bool QGZ = C::QGZ;
+  constexpr bool BF16 = MODE == RS_BF16;
   static_assert(C::kStages >= 2, "stage ring too small");
   extern __shared__ __align__(1024) char smem[];
   __shared__ __align__(8) uint64_t full_bar[C::kStages];
@@ -355,7 +360,7 @@ __global__ void __launch_bounds__(32 + kRsConsumers, 1)
         const uint32_t cnt = (uint32_t)(rem < C::kChunk ? rem : C::kChunk);
         const uint32_t bytes = cnt * 4;
         char* st = smem + (size_t)s * C::kStageBytes;
-        const uint32_t src_bytes = QGZ ? cnt / 2 + cnt / kQgzBlock * 8 : bytes;
+        const uint32_t src_bytes = QGZ ? cnt / 2 + cnt / kQgzBlock * 8 : (BF16 ? cnt * 2 : bytes);
         mbar_expect_tx(&full_bar[s], src_bytes * P + (ADAM ? 3 * bytes : 0));
 #pragma unroll
         for (int j = 0; j < P; ++j) {
@@ -363,6 +368,8 @@ __global__ void __launch_bounds__(32 + kRsConsumers, 1)
           if (QGZ) {
             tma_load(dst, r.qcodes[j] + e0 / 2, cnt / 2, &full_bar[s]);
             tma_load(dst + C::kCodeBytes, r.qparams[j] + e0 / kQgzBlock, cnt / kQgzBlock * 8, &full_bar[s]);
+          } else if (BF16) {
+            tma_load(dst, reinterpret_cast<const __nv_bfloat16*>(r.src[j]) + e0, cnt * 2, &full_bar[s]);
           } else {
             tma_load(dst, r.src[j] + e0, bytes, &full_bar[s]);
           }
@@ -398,6 +405,11 @@ __global__ void __launch_bounds__(32 + kRsConsumers, 1)
             x[j].y = __fadd_rn(ms.x, __fmul_rn((float)((c2 >> 4) & 15u), ms.y));
             x[j].z = __fadd_rn(ms.x, __fmul_rn((float)((c2 >> 8) & 15u), ms.y));
             x[j].w = __fadd_rn(ms.x, __fmul_rn((float)((c2 >> 12) & 15u), ms.y));
+          } else if (BF16) {
+            // bf16 -> fp32 is exact; the reduction itself stays fp32
+            const uint2 b = reinterpret_cast<const uint2*>(sj)[ct];
+            x[j] = make_float4(__uint_as_float(b.x << 16), __uint_as_float(b.x & 0xFFFF0000u),
+                               __uint_as_float(b.y << 16), __uint_as_float(b.y & 0xFFFF0000u));
           } else {
             x[j] = reinterpret_cast<const float4*>(sj)[ct];
           }
@@ -442,18 +454,18 @@ __global__ void __launch_bounds__(32 + kRsConsumers, 1)
   }
 }
 
-template <int P, bool ADAM, bool QGZ>
+template <int P, bool ADAM, int MODE>
 cudaError_t launch_rs_tma_t(const RSParams& r, const AdamParams& a, int grid, cudaStream_t s) {
-  using C = RsCfg<P, ADAM, QGZ>;
+  using C = RsCfg<P, ADAM, MODE>;
   const int smem = C::kStages * C::kStageBytes;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e =
-        cudaFuncSetAttribute(rs_tma_kernel<P, ADAM, QGZ>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(rs_tma_kernel<P, ADAM, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  rs_tma_kernel<P, ADAM, QGZ><<<grid, 32 + kRsConsumers, smem, s>>>(r, a);
+  rs_tma_kernel<P, ADAM, MODE><<<grid, 32 + kRsConsumers, smem, s>>>(r, a);
   return cudaGetLastError();
 }
 
@@ -542,13 +554,21 @@ cudaError_t launch_qgz_quantize(const QuantParams& q, int grid, cudaStream_t s) 
   return cudaGetLastError();
 }
 
-cudaError_t launch_rs_tma(const RSParams& r, const AdamParams* a, int world, int grid, cudaStream_t s, bool qgz) {
+template <int P>
+cudaError_t launch_rs_tma_p(const RSParams& r, const AdamParams* a, int grid, cudaStream_t s, int mode) {
   AdamParams none{};
+  switch (mode) {
+    case RS_F32: return a ? launch_rs_tma_t<P, true, RS_F32>(r, *a, grid, s) : launch_rs_tma_t<P, false, RS_F32>(r, none, grid, s);
+    case RS_BF16: return a ? launch_rs_tma_t<P, true, RS_BF16>(r, *a, grid, s) : launch_rs_tma_t<P, false, RS_BF16>(r, none, grid, s);
+    case RS_QGZ: return a ? launch_rs_tma_t<P, true, RS_QGZ>(r, *a, grid, s) : launch_rs_tma_t<P, false, RS_QGZ>(r, none, grid, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t launch_rs_tma(const RSParams& r, const AdamParams* a, int world, int grid, cudaStream_t s, int mode) {
   switch (world) {
-#define HPZ_RST_CASE(P)                                                                          \
-  case P:                                                                                        \
-    if (qgz) return a ? launch_rs_tma_t<P, true, true>(r, *a, grid, s) : launch_rs_tma_t<P, false, true>(r, none, grid, s); \
-    return a ? launch_rs_tma_t<P, true, false>(r, *a, grid, s) : launch_rs_tma_t<P, false, false>(r, none, grid, s);
+#define HPZ_RST_CASE(P) \
+  case P: return launch_rs_tma_p<P>(r, a, grid, s, mode);
     HPZ_RST_CASE(1) HPZ_RST_CASE(2) HPZ_RST_CASE(3) HPZ_RST_CASE(4) HPZ_RST_CASE(5) HPZ_RST_CASE(6)
     HPZ_RST_CASE(7) HPZ_RST_CASE(8) HPZ_RST_CASE(9) HPZ_RST_CASE(10) HPZ_RST_CASE(11) HPZ_RST_CASE(12)
     HPZ_RST_CASE(13) HPZ_RST_CASE(14) HPZ_RST_CASE(15) HPZ_RST_CASE(16)

@@ -33,6 +33,7 @@ def main():
     ap.add_argument("--verify", default="fingerprint")
     ap.add_argument("--fused", type=int, default=1)
     ap.add_argument("--qgz", type=int, default=0)
+    ap.add_argument("--grad-dtype", default="f32")
     args = ap.parse_args()
     local = int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
@@ -42,7 +43,7 @@ def main():
 
     numels = [int(x) for x in args.numels.split(",")]
     P, r = dist.get_world_size(), dist.get_rank()
-    W = DistWorld(numels, args.node_size, timeout_s=20.0, qgz=bool(args.qgz))
+    W = DistWorld(numels, args.node_size, timeout_s=20.0, qgz=bool(args.qgz), grad_dtype=args.grad_dtype)
     rc = W.ranks[0]
     s = torch.cuda.current_stream()
     H.hpz_set_order(rc.ctx, args.order, stock_delay_us=args.stock_delay_us, stock_poison=args.order == "stock")
@@ -55,13 +56,15 @@ def main():
     fwd = [torch.zeros(x.numel_pad, dtype=torch.bfloat16, device="cuda") for x in rc.infos]
     bwd = [torch.zeros(x.numel_pad, dtype=torch.bfloat16, device="cuda") for x in rc.infos]
     o = O.HpzOracle(numels, P, args.node_size, order="off" if args.order == "off" else "fixed",
-                    qgz=bool(args.qgz))
+                    qgz=bool(args.qgz), grad_dtype=args.grad_dtype)
     adam = H.make_adam()
     keep = []
     t_box = [0]
 
     def grad_fn(rcx, i):
         g = torch.from_numpy(S.layer_grads(i, t_box[0], r, numels[i])).cuda()
+        if args.grad_dtype == "bf16":
+            g = g.to(torch.bfloat16)
         keep.append(g)
         H.hpz_grad_upload(rcx.ctx, i, g.data_ptr(), numels[i], s)
 
@@ -85,7 +88,10 @@ def main():
                 assert np.array_equal(sec, O.param_bits(st.sec, "bf16")), f"rank {r} layer {i}: secondary"
             g = buffer_view(rc, i, "grad_shard", "f32").cpu().numpy()
             rs = O.qgz_reduce_scatter if args.qgz else O.reduce_scatter
-            ref = rs([S.layer_grads(i, t, j, lay.numel, lay.numel_pad) for j in range(P)], lay, r)
+            Gs = [S.layer_grads(i, t, j, lay.numel, lay.numel_pad) for j in range(P)]
+            if args.grad_dtype == "bf16":
+                Gs = [O.bf16_to_f32(O.bf16_rne(x)) for x in Gs]
+            ref = rs(Gs, lay, r)
             assert np.array_equal(g.view(np.uint32), ref.view(np.uint32)), f"rank {r} layer {i}: RS"
             for kind, refv in (("master", st.master), ("m", st.m), ("v", st.v)):
                 got = buffer_view(rc, i, kind, "f32").cpu().numpy()

@@ -51,3 +51,10 @@ def test_multiproc_parity_qgz(n, node):
     if n > NGPU:
         pytest.skip(f"needs {n} GPUs")
     _run(n, node, extra=("--qgz", "1"), port=29811 + n * 10 + node)
+
+
+@pytest.mark.parametrize("n,node", [(2, 2), (4, 2)])
+def test_multiproc_parity_bf16_grads(n, node):
+    if n > NGPU:
+        pytest.skip(f"needs {n} GPUs")
+    _run(n, node, extra=("--grad-dtype", "bf16"), port=29911 + n * 10 + node)

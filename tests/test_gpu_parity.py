@@ -36,6 +36,8 @@ def _check_step(run: ParityRun, rec, check_all=True):
             continue
         from paper_2407_01614_b200.world import buffer_view
         grads = [S.layer_grads(i, run.t - 1, j, lay.numel, lay.numel_pad, kind=run.grad_kind) for j in range(P)]
+        if run.grad_dtype == "bf16":
+            grads = [O.bf16_to_f32(O.bf16_rne(g)) for g in grads]
         for r, rc in enumerate(run.w.ranks):
             st = run.o.state[i][r]
             # a2 secondary store == oracle's Eq. (1) slice
@@ -98,6 +100,19 @@ def test_parity_qgz(P, Pp, fused):
     """f1 qgZ: INT4 blockwise-quantized gradient all-to-all + fixed-order reduction, bit-exact
     vs the oracle's qgz_reduce_scatter (same fp32 rounding decisions for every code)."""
     run = ParityRun(NUMELS, P, Pp, qgz=True, fused=fused, verify="fingerprint")
+    try:
+        for _ in range(3):
+            _check_step(run, run.step())
+        assert run.counters()["timeouts"] == 0
+    finally:
+        run.close()
+
+
+@pytest.mark.parametrize("P,Pp", [(1, 1), (2, 1), (4, 2), (8, 4), (8, 8), (3, 1)])
+@pytest.mark.parametrize("fused", [True, False])
+def test_parity_bf16_grads(P, Pp, fused):
+    """f4: bf16 gradient slots, exact widening, fp32 fixed-order reduction: bit-exact."""
+    run = ParityRun(NUMELS, P, Pp, grad_dtype="bf16", fused=fused, verify="fingerprint")
     try:
         for _ in range(3):
             _check_step(run, run.step())

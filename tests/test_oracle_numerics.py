@@ -187,3 +187,22 @@ def test_adam_partitioned_equals_unpartitioned():
 def test_adam_scalars_validation():
     with pytest.raises(ValueError):
         O.adam_scalars(O.AdamHyper(), 0)
+
+
+def test_bf16_grads_widen_exactly_and_rs_matches_float64_bound():
+    """f4: bf16 gradient values widen to fp32 exactly (torch's cast agrees), and the
+    fp32 fixed-order RS of the widened values obeys the pairwise error bound."""
+    P = 8
+    lay = O.LayerLayout(20_000, P, 4, 256)
+    G = [S.layer_grads(0, 0, j, lay.numel, lay.numel_pad) for j in range(P)]
+    Gb = [O.bf16_to_f32(O.bf16_rne(g)) for g in G]
+    for g, gb in zip(G, Gb):
+        tb = torch.from_numpy(g).to(torch.bfloat16).to(torch.float32).numpy()
+        assert np.array_equal(tb.view(np.uint32), gb.view(np.uint32))
+    u = 2.0 ** -24
+    for r in range(P):
+        got = O.reduce_scatter(Gb, lay, r).astype(np.float64) * P
+        s = lay.shard
+        exact = sum(g[r * s:(r + 1) * s].astype(np.float64) for g in Gb)
+        absum = sum(np.abs(g[r * s:(r + 1) * s].astype(np.float64)) for g in Gb)
+        assert np.all(np.abs(got - exact) <= 3 * u / (1 - 3 * u) * absum + 1e-45)
