@@ -27,8 +27,8 @@ namespace {
 constexpr int kGatherChunk = 32768;     // bytes per gather stage
 constexpr int kGatherStages = 4;
 constexpr int kFpWarps = 4;             // fingerprint consumer warps
-constexpr int kRsChunk = 1024;          // shard elements per RS stage
-constexpr int kRsConsumers = 256;       // one float4 per consumer thread per stage
+constexpr int kRsChunk = 1024;          // base shard elements per RS stage
+constexpr int kRsConsumers = 512;       // 16 consumer warps: enough to hide the Adam math latency
 
 // ------------------------------------------------------------------ PTX wrappers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -309,7 +309,7 @@ struct RsCfg {
   static constexpr bool QGZ = MODE == RS_QGZ;
   // per stage: P gradient slices (fp32, or qgZ int4 codes + (min, scale) per 64) (+ w, m, v);
   // qgZ chunks are longer so its small code/param copies stay >= 1 KiB / 256 B
-  static constexpr int kChunk = QGZ ? 2 * kRsChunk : kRsChunk;
+  static constexpr int kChunk = (P <= 8 ? 2 : 1) * (QGZ ? 2 * kRsChunk : kRsChunk);
   static constexpr int kCodeBytes = kChunk / 2;
   static constexpr int kParamBytes = kChunk / kQgzBlock * 8;
   static constexpr int kSrcBytes = QGZ ? kCodeBytes + kParamBytes : kChunk * (MODE == RS_BF16 ? 2 : 4);
