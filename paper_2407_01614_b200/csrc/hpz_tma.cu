@@ -309,7 +309,8 @@ struct RsCfg {
   static constexpr bool QGZ = MODE == RS_QGZ;
   // per stage: P gradient slices (fp32, or qgZ int4 codes + (min, scale) per 64) (+ w, m, v);
   // qgZ chunks are longer so its small code/param copies stay >= 1 KiB / 256 B
-  static constexpr int kChunk = (P <= 8 ? 2 : 1) * (QGZ ? 2 * kRsChunk : kRsChunk);
+  // P=1 (local, HBM-bound): 1024-element chunks keep 6 stages in flight; 2 <= P <= 8: 2048
+  static constexpr int kChunk = (P >= 2 && P <= 8 ? 2 : 1) * (QGZ ? 2 * kRsChunk : kRsChunk);
   static constexpr int kCodeBytes = kChunk / 2;
   static constexpr int kParamBytes = kChunk / kQgzBlock * 8;
   static constexpr int kSrcBytes = QGZ ? kCodeBytes + kParamBytes : kChunk * (MODE == RS_BF16 ? 2 : 4);
