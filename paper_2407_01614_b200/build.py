@@ -41,6 +41,11 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if verbose:
         sys.stderr.write(res.stderr)
     os.replace(LIB + ".tmp", LIB)
+    # design-experiment tool (not linked into the library): NVLink P2P strategy probe
+    probe = os.path.join(ROOT, "tools", "p2p_probe.cu")
+    if os.path.exists(probe):
+        subprocess.run([NVCC, *ARCH, "-O3", "-o", os.path.join(ROOT, "tools", "p2p_probe"), probe],
+                       capture_output=True, text=True)
     return LIB
 
 
