@@ -470,64 +470,61 @@ cudaError_t launch_rs_tma_t(const RSParams& r, const AdamParams& a, int grid, cu
   return cudaGetLastError();
 }
 
-// qgZ quantizer: 16 threads per 64-element block (one float4 each), kQU blocks per
-// half-warp in flight (ILP); block min/max by shuffles; NaN anywhere in a block makes its
-// (min, scale) NaN so it surfaces after dequantization.  fp32, one IEEE op per operator,
-// round-half-to-even codes — the oracle's quantize_blockwise decisions, bit for bit.
-constexpr int kQU = 4;
+// qgZ quantizer: 4 threads per 64-element block, each holding 4 float4s (elements
+// 4*(q + 4u) .. +3 of the block, q = lane % 4, u = 0..3) so a warp-wide 16-byte load
+// touches 64 contiguous bytes of 8 blocks; block min/max take 2 shuffle levels.  NaN
+// anywhere in a block makes its (min, scale) NaN so it surfaces after dequantization.
+// fp32, one IEEE op per operator, round-half-even codes — the oracle's
+// quantize_blockwise decisions, bit for bit.
 __global__ void __launch_bounds__(256) qgz_quantize_kernel(const __grid_constant__ QuantParams q) {
   if (threadIdx.x == 0 && q.war.n) wait_all(q.war, q.sync);   // E6: peers done with the old codes
   __syncthreads();
   const int64_t n_blocks = q.n / kQgzBlock;
-  const int sub = threadIdx.x & 15;
-  const int64_t hw = (int64_t)blockIdx.x * (blockDim.x / 16) + (threadIdx.x >> 4);   // half-warp id
-  const int64_t n_hw = (int64_t)gridDim.x * (blockDim.x / 16);
-  for (int64_t b0 = hw * kQU; b0 < n_blocks; b0 += n_hw * kQU) {
-    float4 v[kQU];
+  const int sub = threadIdx.x & 3;
+  const int64_t grp = (int64_t)blockIdx.x * (blockDim.x / 4) + (threadIdx.x >> 2);   // 4-thread group id
+  const int64_t n_grp = (int64_t)gridDim.x * (blockDim.x / 4);
+  const float4* g4 = reinterpret_cast<const float4*>(q.g);
+  uint16_t* c16 = reinterpret_cast<uint16_t*>(q.codes);
+  for (int64_t b = grp; b < n_blocks; b += n_grp) {
+    float4 v[4];
 #pragma unroll
-    for (int u = 0; u < kQU; ++u)
-      if (b0 + u < n_blocks) v[u] = reinterpret_cast<const float4*>(q.g)[(b0 + u) * 16 + sub];
-    float mn[kQU], mx[kQU];
-    int nan[kQU];
+    for (int u = 0; u < 4; ++u) v[u] = g4[b * 16 + sub + 4 * u];
+    int nan = 0;
+    float mn = v[0].x, mx = v[0].x;
 #pragma unroll
-    for (int u = 0; u < kQU; ++u) {
-      if (b0 + u >= n_blocks) v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-      nan[u] = isnan(v[u].x) || isnan(v[u].y) || isnan(v[u].z) || isnan(v[u].w);
-      mn[u] = fminf(fminf(v[u].x, v[u].y), fminf(v[u].z, v[u].w));
-      mx[u] = fmaxf(fmaxf(v[u].x, v[u].y), fmaxf(v[u].z, v[u].w));
+    for (int u = 0; u < 4; ++u) {
+      nan |= isnan(v[u].x) | isnan(v[u].y) | isnan(v[u].z) | isnan(v[u].w);
+      mn = fminf(mn, fminf(fminf(v[u].x, v[u].y), fminf(v[u].z, v[u].w)));
+      mx = fmaxf(mx, fmaxf(fmaxf(v[u].x, v[u].y), fmaxf(v[u].z, v[u].w)));
     }
 #pragma unroll
-    for (int o = 8; o > 0; o >>= 1) {
-#pragma unroll
-      for (int u = 0; u < kQU; ++u) {
-        mn[u] = fminf(mn[u], __shfl_xor_sync(0xffffffffu, mn[u], o));
-        mx[u] = fmaxf(mx[u], __shfl_xor_sync(0xffffffffu, mx[u], o));
-        nan[u] |= __shfl_xor_sync(0xffffffffu, nan[u], o);
-      }
+    for (int o = 2; o > 0; o >>= 1) {
+      mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      nan |= __shfl_xor_sync(0xffffffffu, nan, o);
     }
+    float scale = __fdiv_rn(__fsub_rn(mx, mn), 15.0f);
+    if (nan) {
+      mn = __int_as_float(0x7fc00000);
+      scale = mn;
+    }
+    const bool pos = scale > 0.0f;
 #pragma unroll
-    for (int u = 0; u < kQU; ++u) {
-      if (b0 + u >= n_blocks) continue;
-      float m0 = mn[u];
-      float scale = __fdiv_rn(__fsub_rn(mx[u], m0), 15.0f);
-      if (nan[u]) {
-        m0 = __int_as_float(0x7fc00000);
-        scale = m0;
-      }
-      uint32_t packed = 0;
+    for (int u = 0; u < 4; ++u) {
       const float e[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+      uint32_t packed = 0;
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         int c = 0;
-        if (scale > 0.0f) {
-          c = __float2int_rn(__fdiv_rn(__fsub_rn(e[k], m0), scale));
+        if (pos) {
+          c = __float2int_rn(__fdiv_rn(__fsub_rn(e[k], mn), scale));
           c = c < 0 ? 0 : (c > 15 ? 15 : c);
         }
         packed |= (uint32_t)c << (4 * k);
       }
-      reinterpret_cast<uint16_t*>(q.codes)[(b0 + u) * 16 + sub] = (uint16_t)packed;
-      if (sub == 0) q.params[b0 + u] = make_float2(m0, scale);
+      c16[b * 16 + sub + 4 * u] = (uint16_t)packed;
     }
+    if (sub == 0) q.params[b] = make_float2(mn, scale);
   }
 }
 

@@ -249,3 +249,32 @@ def test_api_errors():
         assert e.value.code == H.HPZ_ESTATE
     finally:
         w.close()
+
+
+def test_missing_peer_times_out_instead_of_hanging():
+    """Failure detection: a backward gather whose node peer never released its secondary
+    (the peer skipped its forward) waits at most the timeout, records it, and the next
+    call on that context returns HPZ_ETIMEOUT — the GPU is never hung."""
+    import time
+    from paper_2407_01614_b200 import hpz as H
+    from paper_2407_01614_b200.world import EmulatedWorld
+    w = EmulatedWorld([50_000], 2, 2, timeout_s=1.0)
+    try:
+        s = torch.cuda.current_stream()
+        w0 = torch.from_numpy(S.layer_params(0, 50_000)).cuda()
+        for rc in w.ranks:
+            H.hpz_load_master(rc.ctx, 0, w0.data_ptr(), s)
+        buf = torch.empty(w.ranks[0].infos[0].numel_pad, dtype=torch.bfloat16, device="cuda")
+        r0 = w.ranks[0].ctx
+        H.hpz_fwd_gather(r0, 0, buf.data_ptr(), s)       # rank 1 never runs its forward
+        t0 = time.time()
+        H.hpz_bwd_gather(r0, 0, buf.data_ptr(), s)       # waits for rank 1's SEC_READY
+        torch.cuda.synchronize()
+        assert time.time() - t0 < 30
+        c = H.hpz_counters(r0)
+        assert c["timeouts"] >= 1
+        with pytest.raises(H.HpzError) as e:
+            H.hpz_grad_buffer(r0, 0, s)
+        assert e.value.code == H.HPZ_ETIMEOUT
+    finally:
+        w.close()
