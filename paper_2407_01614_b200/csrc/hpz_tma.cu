@@ -28,7 +28,7 @@ constexpr int kGatherChunk = 32768;     // bytes per gather stage
 constexpr int kGatherStages = 4;
 constexpr int kFpWarps = 4;             // fingerprint consumer warps
 constexpr int kRsChunk = 1024;          // base shard elements per RS stage
-constexpr int kRsConsumers = 512;       // 16 consumer warps: enough to hide the Adam math latency
+constexpr int kRsMaxConsumers = 512;    // up to 16 consumer warps (one float4 each per chunk)
 
 // ------------------------------------------------------------------ PTX wrappers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -317,11 +317,14 @@ struct RsCfg {
   static constexpr int kWmvOff = P * kSrcBytes;
   static constexpr int kStageBytes = kWmvOff + (ADAM ? 3 * kChunk * 4 : 0);
   static constexpr int kStages = (200 * 1024) / kStageBytes >= 6 ? 6 : (200 * 1024) / kStageBytes;
+  // consumer threads: one float4 per thread per chunk, at most 16 warps (idle polling
+  // warps would steal issue slots from the working ones)
+  static constexpr int kConsumers = kChunk / 4 < kRsMaxConsumers ? kChunk / 4 : kRsMaxConsumers;
 };
 
 // Block = 1 producer warp + 8 consumer warps.  Dynamic smem = kStages * kStageBytes.
 template <int P, bool ADAM, int MODE>
-__global__ void __launch_bounds__(32 + kRsConsumers, 1)
+__global__ void __launch_bounds__(32 + kRsMaxConsumers, 1)
     rs_tma_kernel(const __grid_constant__ RSParams r, const __grid_constant__ AdamParams a) {
   using C = RsCfg<P, ADAM, MODE>;
   constexpr bool QGZ = C::QGZ;
@@ -345,7 +348,7 @@ __global__ void __launch_bounds__(32 + kRsConsumers, 1)
     fence_proxy_async();
     for (int s = 0; s < C::kStages; ++s) {
       mbar_init(&full_bar[s], 1);
-      mbar_init(&empty_bar[s], kRsConsumers / 32);
+      mbar_init(&empty_bar[s], C::kConsumers / 32);
     }
     fence_mbar_init();
   }
@@ -393,7 +396,7 @@ __global__ void __launch_bounds__(32 + kRsConsumers, 1)
       const char* stc = smem + (size_t)s * C::kStageBytes;
       const float4* wmv = reinterpret_cast<const float4*>(stc + C::kWmvOff);
       // consumer thread ct handles float4s ct, ct+256, ... of the chunk
-      for (int ct = threadIdx.x - 32; ct * 4 < cnt; ct += kRsConsumers) {
+      for (int ct = threadIdx.x - 32; ct * 4 < cnt; ct += C::kConsumers) {
         float4 x[P];
 #pragma unroll
         for (int j = 0; j < P; ++j) {
@@ -466,7 +469,7 @@ cudaError_t launch_rs_tma_t(const RSParams& r, const AdamParams& a, int grid, cu
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  rs_tma_kernel<P, ADAM, MODE><<<grid, 32 + kRsConsumers, smem, s>>>(r, a);
+  rs_tma_kernel<P, ADAM, MODE><<<grid, 32 + C::kConsumers, smem, s>>>(r, a);
   return cudaGetLastError();
 }
 
