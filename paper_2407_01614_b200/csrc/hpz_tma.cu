@@ -57,16 +57,20 @@ __device__ __forceinline__ uint64_t globaltimer_();
 // Bounded mbarrier wait: a pipeline that never completes (lost bulk copy, aborted peer)
 // records a timeout and returns instead of hanging the GPU.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity, const SyncCommon& sc) {
-  if (mbar_try(bar, parity)) return;
-  const uint64_t t0 = globaltimer_();
   uint32_t spins = 0;
+  uint64_t t0 = 0;
   while (!mbar_try(bar, parity)) {
-    if ((++spins & 1023u) == 0 && globaltimer_() - t0 > sc.timeout_ns) {
-      atomicAdd(sc.timeouts, 1ull);
-      atomicExch(sc.abort_flag, 1u);
-      *sc.host_err = 1u;
-      __threadfence_system();
-      return;
+    if ((++spins & 4095u) == 0) {          // rare: only a stalled pipeline reaches the clock
+      const uint64_t now = globaltimer_();
+      if (t0 == 0) {
+        t0 = now;
+      } else if (now - t0 > sc.timeout_ns) {
+        atomicAdd(sc.timeouts, 1ull);
+        atomicExch(sc.abort_flag, 1u);
+        *sc.host_err = 1u;
+        __threadfence_system();
+        return;
+      }
     }
   }
 }
@@ -324,7 +328,7 @@ struct RsCfg {
 
 // Block = 1 producer warp + 8 consumer warps.  Dynamic smem = kStages * kStageBytes.
 template <int P, bool ADAM, int MODE>
-__global__ void __launch_bounds__(32 + kRsMaxConsumers, 1)
+__global__ void __launch_bounds__(32 + RsCfg<P, ADAM, MODE>::kConsumers, 1)
     rs_tma_kernel(const __grid_constant__ RSParams r, const __grid_constant__ AdamParams a) {
   using C = RsCfg<P, ADAM, MODE>;
   constexpr bool QGZ = C::QGZ;
