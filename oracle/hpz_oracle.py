@@ -424,9 +424,12 @@ class HpzOracle:
     half_seed: int = 1234
     qgz: bool = False                    # f1: INT4 quantized gradient all-to-all (qgz_reduce_scatter)
     grad_dtype: str = "f32"              # f4: "bf16" = gradients stored/communicated as bf16 (RNE)
+    qwz: bool = False                    # f2: INT8 blockwise weights in the forward AllGather
 
     def __post_init__(self):
         check_topology(self.world, self.node_size)
+        if self.qwz and self.align % QWZ_BLOCK:
+            raise ValueError("qwZ needs shards made of whole 256-element blocks (align % 256 == 0)")
         if self.order not in ORDERS or self.stock_schedule not in STOCK_SCHEDULES:
             raise ValueError("bad order/schedule")
         self.layouts = [LayerLayout(n, self.world, self.node_size, self.align) for n in self.numels]
@@ -485,6 +488,8 @@ class HpzOracle:
         # Forward pass, i = 1..N
         for i, lay in enumerate(self.layouts):
             prims = [self.state[i][r].prim for r in range(P)]
+            if self.qwz:                                        # f2: quantize before AllGather
+                prims = [qwz_gathered_shard(p_, self.param_dtype) for p_ in prims]
             F = [fwd_gather(prims) for _ in range(P)]          # AllGather(L_i, P), every rank
             for r in range(P):
                 assert np.array_equal(param_bits(F[r], self.param_dtype), param_bits(F[0], self.param_dtype))
@@ -687,3 +692,27 @@ def qgz_reduce_scatter(grads: list[np.ndarray], lay: LayerLayout, rank: int,
         parts.append(dequantize_blockwise(codes[rank * s:(rank + 1) * s], mins[b0:b1], scales[b0:b1], block))
     total = pairwise_rank_sum(parts)
     return (total * F32(1.0 / lay.world)).astype(F32)
+
+
+# ----------------------------------------------------------------------------
+# f2. qwZ: blockwise INT8 weight quantization before the forward AllGather
+#     ("the qwZ scheme quantizes weights before AllGather operations").
+#     Reading R28 (the paper does not state the scheme): SPEC's asymmetric blockwise
+#     quantizer with 8 bits and 256-element blocks (SPEC's qwZ default),
+#     applied by the owner to its primary shard (the values as fp32); the forward gather
+#     dequantizes (min + code*scale, fp32) and rounds to the parameter dtype (bf16 RNE).
+#     The secondary is written from the forward-gathered values, so the backward gather
+#     returns exactly what the forward gather returned.
+# ----------------------------------------------------------------------------
+
+QWZ_BITS = 8
+QWZ_BLOCK = 256
+
+
+def qwz_gathered_shard(prim: np.ndarray, param_dtype: str) -> np.ndarray:
+    """What every rank receives for one owner's primary shard under qwZ (param storage).
+    Pins: exact on constant blocks; within scale/2 (+ one bf16 rounding) of the primary."""
+    vals = param_values(prim, param_dtype)
+    codes, mins, scales = quantize_blockwise(vals, QWZ_BITS, QWZ_BLOCK)
+    deq = dequantize_blockwise(codes, mins, scales, QWZ_BLOCK)
+    return refresh_primary(deq, param_dtype)

@@ -81,3 +81,29 @@ def test_qgz_rs_exact_on_constant_blocks():
 def test_qgz_payload_bytes():
     """int4 codes + fp32 (min, scale) per 64 elements = 0.625 B/elem vs 4 B/elem fp32."""
     assert O.QGZ_BITS / 8 + 8 / O.QGZ_BLOCK == 0.625
+
+
+# ---------------------------------------------------------------- qwZ (f2)
+def test_qwz_constant_blocks_exact():
+    prim = O.bf16_rne(np.repeat(np.arange(8, dtype=np.float32) * 0.125 - 0.5, 256))
+    assert np.array_equal(O.qwz_gathered_shard(prim, "bf16"), prim)
+
+
+def test_qwz_error_bound():
+    """Gathered weights within scale/2 + one bf16 rounding of the primary."""
+    prim = O.bf16_rne(S.layer_params(0, 256 * 400))
+    got = O.bf16_to_f32(O.qwz_gathered_shard(prim, "bf16")).astype(np.float64)
+    ref = O.bf16_to_f32(prim).astype(np.float64)
+    _, _, sc = O.quantize_blockwise(O.bf16_to_f32(prim), 8, 256)
+    bound = np.repeat(sc.astype(np.float64), 256) / 2 + np.abs(ref) * 2 ** -8 + 1e-30
+    assert np.all(np.abs(got - ref) <= bound)
+
+
+def test_qwz_step_bwd_equals_fwd_and_trains():
+    """hpZ + qwZ: the backward gather equals the (dequantized) forward gather, 0 mismatches."""
+    o = O.HpzOracle([3000, 1234], 4, 2, align=256, qwz=True)
+    for rec in o.run(3):
+        assert sum(rec.mismatches) == 0
+    # the forward-gathered weights differ from the exact primaries (lossy) but stay close
+    prim = O.bf16_to_f32(o.full_primary(0)).astype(np.float64)
+    assert np.max(np.abs(prim)) > 0
