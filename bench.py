@@ -49,6 +49,7 @@ def parse():
     ap.add_argument("--ctas-per-sm", type=int, default=None)
     ap.add_argument("--copy-engine", default="tma", choices=["tma", "ldg"])
     ap.add_argument("--qgz", action="store_true", help="ZeRO++ qgZ: INT4 gradient all-to-all (SURVEY f1)")
+    ap.add_argument("--qwz", action="store_true", help="ZeRO++ qwZ: INT8 weights in the forward gather (SURVEY f2)")
     ap.add_argument("--grad-dtype", default="f32", choices=["f32", "bf16"],
                     help="gradient slot dtype (bf16: SURVEY f4, fp32 accumulation)")
     ap.add_argument("--e2e-steps", type=int, default=2)
@@ -186,10 +187,10 @@ def main():
 
     if world > 1:
         W = DistWorld(numels, node_size, dtype=dtype, n_grad_slots=L, device=local_rank, timeout_s=60.0,
-                      qgz=args.qgz, grad_dtype=args.grad_dtype)
+                      qgz=args.qgz, grad_dtype=args.grad_dtype, qwz=args.qwz)
     else:
         W = EmulatedWorld(numels, 1, 1, dtype=dtype, n_grad_slots=L, device=local_rank, timeout_s=60.0,
-                          qgz=args.qgz, grad_dtype=args.grad_dtype)
+                          qgz=args.qgz, grad_dtype=args.grad_dtype, qwz=args.qwz)
     rc = W.ranks[0]
     ctx = rc.ctx
     H.hpz_set_order(ctx, args.order)
@@ -284,7 +285,8 @@ def main():
     gsz = 2 if args.grad_dtype == "bf16" else 4
     rs_bytes = sum(x.numel_pad for x in infos) * gsz      # RS input bytes in the slot dtype
     rs_wire = rs_bytes * (0.625 / 4 if args.qgz else 1.0)
-    ingress = ag_bytes * (P - 1) / P + ag_bytes * (Pp - 1) / Pp + rs_wire * (P - 1) / P
+    fwd_wire = ag_bytes * ((1 + 8 / 256) / e if args.qwz else 1.0)
+    ingress = fwd_wire * (P - 1) / P + ag_bytes * (Pp - 1) / Pp + rs_wire * (P - 1) / P
     adam_bytes = sum(x.shard for x in infos) * (30 if dtype == "bf16" else 32)
 
     vals = max_over_ranks([step_ms, tot["fwd"], tot["bwd"], tot["rs"], tot["adam"],
@@ -312,7 +314,7 @@ def main():
         alg = hbm_alg[dom]
         bound, peak, unit = "hbm", hbm_peak, "GB/s"
     else:
-        nv_alg = {"fwd_gather": ag_bytes * (P - 1) / P, "bwd_gather": ag_bytes * (Pp - 1) / Pp,
+        nv_alg = {"fwd_gather": fwd_wire * (P - 1) / P, "bwd_gather": ag_bytes * (Pp - 1) / Pp,
                   "reduce_scatter": rs_wire * (P - 1) / P, "adam": adam_bytes,
                   "reduce_scatter+adam": rs_wire * (P - 1) / P}
         alg = nv_alg[dom]
@@ -395,6 +397,8 @@ def main():
                        "qgz": "int4 blockwise (64) gradient all-to-all; RS bytes counted as the fp32 "
                               "gradient bytes reduced, wire bytes 0.625 B/elem" if args.qgz else None,
                        "grad_dtype": args.grad_dtype,
+                       "qwz": "int8 blockwise (256) weights in the forward gather; AG bytes counted as the "
+                              "bf16 parameter bytes delivered" if args.qwz else None,
                        "l2": "no flush: per-step working set >> 126 MB L2 (every layer buffer is "
                              "touched once per phase)",
                        "value_def": "sum over ranks of AllGather output bytes (fwd+bwd) + ReduceScatter "

@@ -282,10 +282,21 @@ typedef enum {
                                     4), dequantizes (min + code*scale) and reduces in the R7
                                     order.  Set BEFORE hpz_register_flat_params (it sizes the
                                     arena).  With qgZ, hpz_grads_ready also quantizes. */
-  HPZ_OPT_GRAD_DTYPE = 4         /* HPZ_F32 (default) or HPZ_BF16: gradient slots hold
+  HPZ_OPT_GRAD_DTYPE = 4,        /* HPZ_F32 (default) or HPZ_BF16: gradient slots hold
                                     bf16; the reduce-scatter converts (exactly) to fp32 and
                                     reduces in fp32 in the R7 order — half the NVLink bytes.
                                     Set before hpz_register_flat_params; not with qgZ. */
+  HPZ_OPT_QWZ = 5                /* 0 (default) or 8: ZeRO++ qwZ ("quantizes weights
+                                    before AllGather"; reading R28): after every
+                                    optimizer step (and at load) the owner quantizes its primary
+                                    shard blockwise to INT8 (256-element blocks, fp32 min +
+                                    scale, round-half-even codes) and the forward gather pulls
+                                    codes (1 + 8/256 B/elem instead of 2), dequantizes
+                                    (min + code*scale, then RNE to the param dtype) and writes
+                                    the full buffer and the secondary; the backward gather is
+                                    unchanged and returns the same values.  Needs align_elems
+                                    % 256 == 0; not with EXACT verification or ORDER_OFF.  Set
+                                    before hpz_register_flat_params. */
 } hpz_option;
 /* Copy engine of the gathers and the reduce-scatter: TMA 1-D bulk copies through a
  * shared-memory stage ring (cp.async.bulk, one persistent CTA per SM), or 16-byte

@@ -61,6 +61,9 @@ struct GatherParams {
   WaitList cmp_wait;
   unsigned long long* fp_mism;
   unsigned long long* fp_checked;
+  // qwZ (f2): src[j] are INT8 codes (1 byte per element, src_bytes = shard elements) and
+  // qw_params[j] their (min, scale) per 256 elements; the kernel dequantizes to elem_bytes
+  const float2* qw_params[kMaxWorld];
   SyncCommon sync;
 };
 
@@ -72,6 +75,20 @@ struct QuantParams {
   float2* params;                      // n/64 (min, scale) pairs
   int64_t n;
   WaitList war;                        // E6 of the previous use: peers done reading codes
+  SyncCommon sync;
+};
+
+// qwZ (f2): blockwise INT8 quantization of one owner's primary shard (after Adam / load);
+// its last CTA releases E1 (PRIMARY_READY) because peers gather the codes, not the primary.
+constexpr int kQwzBlock = 256;
+struct QwzQuantParams {
+  const void* prim;                    // primary shard (bf16 or fp32), n elements, n % 256 == 0
+  int prim_bf16;
+  uint8_t* codes;                      // n bytes
+  float2* params;                      // n/256 (min, scale) pairs
+  int64_t n;
+  uint32_t* done_ctr;
+  ReleaseList rel;                     // E1
   SyncCommon sync;
 };
 
@@ -120,6 +137,9 @@ cudaError_t launch_gather_tma(const GatherParams& p, int grid, cudaStream_t s);
 cudaError_t launch_rs_tma(const RSParams& r, const AdamParams* a, int world, int grid, cudaStream_t s,
                           int mode = 0);
 cudaError_t launch_qgz_quantize(const QuantParams& q, int grid, cudaStream_t s);
+cudaError_t launch_qwz_quantize(const QwzQuantParams& q, int grid, cudaStream_t s);
+// qwZ forward gather: TMA-pulls codes + params, dequantizes, STG to out (+ secondary).
+cudaError_t launch_gather_qwz(const GatherParams& p, int grid, cudaStream_t s);
 cudaError_t launch_wait(const WaitList& w, const SyncCommon& sync, cudaStream_t s);
 cudaError_t launch_release(const ReleaseList& r, cudaStream_t s);
 cudaError_t launch_copy(void* dst, const void* src, int64_t bytes, int grid, cudaStream_t s);

@@ -23,11 +23,12 @@ uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
 
 enum FlagKind { F_PRIM_READY = 0, F_FWD_DONE, F_SEC_READY, F_BWD_DONE, F_BWDP_DONE, F_NUM_LAYER_KINDS };
 enum SlotFlagKind { S_GRAD_READY = 0, S_RS_DONE, S_NUM };
-enum CtrKind { C_FWD = 0, C_BWD, C_RS, C_ADAM, C_NUM };
+enum CtrKind { C_FWD = 0, C_BWD, C_RS, C_ADAM, C_QWZ, C_NUM };
 
 struct Layer {
   int64_t numel, numel_pad, shard, sec_shard;
   uint64_t off_primary, off_master, off_m, off_v, off_gshard, off_secondary;
+  uint64_t off_qw_codes = 0, off_qw_params = 0;   // qwZ (f2)
   int slot;
   // host bookkeeping of the step t the layer's ops were issued for (-1: never)
   int64_t fwd_t = -1, bwd_t = -1, rs_t = -1, step_t = -1;
@@ -63,6 +64,7 @@ struct hpz_ctx {
   int copy_engine = HPZ_COPY_TMA;
   int qgz_bits = 0;                       // f1: 4 = INT4 quantized gradient all-to-all
   int grad_bytes = 4;                     // f4: 2 = bf16 gradients (fp32 accumulation)
+  int qwz_bits = 0;                       // f2: 8 = INT8 blockwise weights in the forward gather
   std::vector<uint64_t> off_qcodes, off_qparams;   // per grad slot (qgZ)
   std::string err;
 
@@ -159,6 +161,27 @@ cudaError_t rs_launch(const hpz_ctx* c, const RSParams& r, const AdamParams* a, 
   return a ? launch_rs_adam(r, *a, c->world, grid, s) : launch_reduce_scatter(r, c->world, grid, s);
 }
 
+// qwZ: quantize my primary shard of `layer` (just written by Adam or the init) and release
+// E1 (value) from the quantizer's last CTA: peers gather the codes, not the primary.
+int qwz_quantize(hpz_ctx* c, int layer, uint32_t value, cudaStream_t s) {
+  const Layer& L = c->layers[layer];
+  char* a = c->arena[c->rank];
+  QwzQuantParams q{};
+  q.prim = a + L.off_primary;
+  q.prim_bf16 = c->dtype == HPZ_BF16;
+  q.codes = reinterpret_cast<uint8_t*>(a + L.off_qw_codes);
+  q.params = reinterpret_cast<float2*>(a + L.off_qw_params);
+  q.n = L.shard;
+  q.done_ctr = c->ctr(C_QWZ, layer);
+  for (int j = 0; j < c->world; ++j) q.rel.ptr[q.rel.n++] = c->flag(j, F_PRIM_READY, layer, c->rank);
+  q.rel.value = value;
+  q.sync = c->sync();
+  cudaError_t e = launch_qwz_quantize(q, grid_for(c, (L.shard / kQwzBlock + 7) / 8, 8), s);
+  if (e != cudaSuccess) return fail(c, HPZ_ECUDA, "qwZ quantize launch: %s", cudaGetErrorString(e));
+  c->launches += 1;
+  return HPZ_OK;
+}
+
 int do_init_shard(hpz_ctx* c, int layer, const float* src, uint64_t key, float scale, cudaStream_t s) {
   Layer& L = c->layers[layer];
   char* a = c->arena[c->rank];
@@ -168,13 +191,15 @@ int do_init_shard(hpz_ctx* c, int layer, const float* src, uint64_t key, float s
                                     src, L.shard, (int64_t)c->rank * L.shard, L.numel, key, scale,
                                     grid_for(c, (L.shard + 255) / 256, 8), s);
   if (e != cudaSuccess) return fail(c, HPZ_ECUDA, "init_shard launch: %s", cudaGetErrorString(e));
+  c->launches += 1;
+  if (c->qwz_bits) return qwz_quantize(c, layer, epoch(c->t + 1), s);   // E1 from the quantizer
   // E1 for step 0: PRIMARY_READY_j[layer][me] = 1 in every rank's arena
   ReleaseList r{};
   for (int j = 0; j < c->world; ++j) r.ptr[r.n++] = c->flag(j, F_PRIM_READY, layer, c->rank);
   r.value = epoch(c->t + 1);
   e = launch_release(r, s);
   if (e != cudaSuccess) return fail(c, HPZ_ECUDA, "release launch: %s", cudaGetErrorString(e));
-  c->launches += 2;
+  c->launches += 1;
   return HPZ_OK;
 }
 
@@ -253,6 +278,8 @@ int hpz_register_flat_params(hpz_ctx* c, int n_layers, const int64_t* numel, int
   if (align_elems < 8 || (align_elems & (align_elems - 1)) || (align_elems * elem) % 16)
     return fail(c, HPZ_EINVAL, "align_elems must be a power of two >= 8 covering 16 bytes");
   if (n_grad_slots < 1 || n_grad_slots > n_layers) return fail(c, HPZ_EINVAL, "n_grad_slots must be in [1, n_layers]");
+  if (c->qwz_bits && align_elems % kQwzBlock)
+    return fail(c, HPZ_EINVAL, "qwZ needs align_elems to be a multiple of 256 (whole quantization blocks per shard)");
   c->dtype = param_dtype;
   c->elem = elem;
   c->align = align_elems;
@@ -293,7 +320,14 @@ int hpz_register_flat_params(hpz_ctx* c, int n_layers, const int64_t* numel, int
     L.off_m = off;         off = align_up(off + (uint64_t)L.shard * 4, kBufAlign);
     L.off_v = off;         off = align_up(off + (uint64_t)L.shard * 4, kBufAlign);
     L.off_gshard = off;    off = align_up(off + (uint64_t)L.shard * 4, kBufAlign);
-    if (true) { L.off_secondary = off; off = align_up(off + (uint64_t)L.sec_shard * elem, kBufAlign); }
+    L.off_secondary = off;
+    off = align_up(off + (uint64_t)L.sec_shard * elem, kBufAlign);
+    if (c->qwz_bits) {   // int8 codes + (min, scale) per 256 elements of the primary shard
+      L.off_qw_codes = off;
+      off = align_up(off + (uint64_t)L.shard, kBufAlign);
+      L.off_qw_params = off;
+      off = align_up(off + (uint64_t)L.shard / kQwzBlock * 8, kBufAlign);
+    }
   }
   c->off_slot.assign(n_grad_slots, 0);
   c->off_qcodes.assign(n_grad_slots, 0);
@@ -524,6 +558,8 @@ int hpz_fwd_gather(hpz_ctx* c, int layer, void* full_out, void* stream) {
   if (!full_out || (reinterpret_cast<uintptr_t>(full_out) & 15)) return fail(c, HPZ_EINVAL, "full_out null or not 16-byte aligned");
   Layer& L = c->layers[layer];
   if (L.fwd_t == c->t) return fail(c, HPZ_ESTATE, "layer %d already forward-gathered at step %lld", layer, (long long)c->t);
+  if (c->qwz_bits && (c->verify == HPZ_VERIFY_EXACT || c->order == HPZ_ORDER_OFF))
+    return fail(c, HPZ_ESTATE, "qwZ gathers dequantized weights: EXACT verification and ORDER_OFF compare/read raw primaries");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const uint32_t t1 = epoch(c->t + 1);
   GatherParams p{};
@@ -554,7 +590,18 @@ int hpz_fwd_gather(hpz_ctx* c, int layer, void* full_out, void* stream) {
   for (int j = 0; j < c->world; ++j) p.rel.ptr[p.rel.n++] = c->flag(j, F_FWD_DONE, layer, c->rank);            // E2
   p.rel.value = t1;
   p.sync = c->sync();
-  cudaError_t e = gather_launch(c, p, s);
+  cudaError_t e;
+  if (c->qwz_bits) {
+    // qwZ: pull every owner's INT8 codes + (min, scale) and dequantize (f2, R28)
+    p.src_bytes = L.shard;   // one code byte per element
+    for (int j = 0; j < c->world; ++j) {
+      p.src[j] = c->arena[j] + L.off_qw_codes;
+      p.qw_params[j] = reinterpret_cast<const float2*>(c->arena[j] + L.off_qw_params);
+    }
+    e = launch_gather_qwz(p, grid_for(c, (L.shard + 8191) / 8192 * c->world, 1), s);
+  } else {
+    e = gather_launch(c, p, s);
+  }
   if (e != cudaSuccess) return fail(c, HPZ_ECUDA, "fwd gather launch: %s", cudaGetErrorString(e));
   c->launches += 1;
   if (c->order == HPZ_ORDER_STOCK) {
@@ -814,7 +861,8 @@ static void build_adam(hpz_ctx* c, int layer, const hpz_adam* a, AdamParams& p) 
     for (int j = 0; j < c->world; ++j) p.wait.ptr[p.wait.n++] = c->flag(c->rank, F_BWDP_DONE, layer, j);   // E7
   p.wait.target = t1;
   p.done_ctr = c->ctr(C_ADAM, layer);
-  for (int j = 0; j < c->world; ++j) p.rel.ptr[p.rel.n++] = c->flag(j, F_PRIM_READY, layer, c->rank);   // E1
+  if (!c->qwz_bits)   // with qwZ the quantizer launched after Adam releases E1
+    for (int j = 0; j < c->world; ++j) p.rel.ptr[p.rel.n++] = c->flag(j, F_PRIM_READY, layer, c->rank);   // E1
   p.rel.value = epoch(c->t + 2);
   p.sync = c->sync();
 }
@@ -835,6 +883,7 @@ static int step_one(hpz_ctx* c, int layer, const hpz_adam* a, cudaStream_t s) {
   cudaError_t e = launch_adam(p, grid_for(c, (p.n_vec + 511) / 512, c->ctas_per_sm), s);
   if (e != cudaSuccess) return fail(c, HPZ_ECUDA, "adam launch: %s", cudaGetErrorString(e));
   c->launches += 1;
+  if (c->qwz_bits) return qwz_quantize(c, layer, epoch(c->t + 2), s);
   return HPZ_OK;
 }
 
@@ -877,6 +926,8 @@ int hpz_reduce_scatter_adam(hpz_ctx* c, int layer, const hpz_adam* a, void* stre
   cudaError_t e = rs_launch(c, r, &p, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return fail(c, HPZ_ECUDA, "rs+adam launch: %s", cudaGetErrorString(e));
   c->launches += 1;
+  if (c->qwz_bits)
+    if (int rc = qwz_quantize(c, layer, epoch(c->t + 2), static_cast<cudaStream_t>(stream))) return rc;
   rs_issued(c, layer);
   stepped(c, layer);
   return HPZ_OK;
@@ -895,6 +946,11 @@ int hpz_set_option(hpz_ctx* c, int option, int64_t value) {
       if (value != 0 && value != 4) return fail(c, HPZ_EINVAL, "qgZ bits must be 0 (off) or 4");
       if (value && c->grad_bytes != 4) return fail(c, HPZ_EINVAL, "qgZ quantizes fp32 gradients");
       c->qgz_bits = (int)value;
+      return HPZ_OK;
+    case HPZ_OPT_QWZ:
+      if (c->registered) return fail(c, HPZ_ESTATE, "qwZ must be chosen before hpz_register_flat_params");
+      if (value != 0 && value != 8) return fail(c, HPZ_EINVAL, "qwZ bits must be 0 (off) or 8");
+      c->qwz_bits = (int)value;
       return HPZ_OK;
     case HPZ_OPT_GRAD_DTYPE:
       if (c->registered) return fail(c, HPZ_ESTATE, "the gradient dtype must be chosen before hpz_register_flat_params");

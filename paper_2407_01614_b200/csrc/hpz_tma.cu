@@ -535,6 +535,197 @@ __global__ void __launch_bounds__(256) qgz_quantize_kernel(const __grid_constant
   }
 }
 
+// ------------------------------------------------------------------ qwZ (f2)
+// One warp per 256-element block of the owner's primary shard: each lane converts 8
+// elements to fp32, the warp reduces min/max/NaN, and the block's codes are
+// round-half-even((v - min) / scale) with scale = (max - min) / 255 — the oracle's
+// quantize_blockwise(bits=8, block=256), bit for bit.  The last CTA releases E1.
+__global__ void __launch_bounds__(256) qwz_quantize_kernel(const __grid_constant__ QwzQuantParams q) {
+  const int lane = threadIdx.x & 31;
+  const int64_t n_blocks = q.n / kQwzBlock;
+  const int64_t warp_id = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  const int64_t n_warps = (int64_t)gridDim.x * (blockDim.x / 32);
+  for (int64_t b = warp_id; b < n_blocks; b += n_warps) {
+    float v[8];
+    if (q.prim_bf16) {
+      const uint4 w = reinterpret_cast<const uint4*>(q.prim)[b * 32 + lane];
+      const uint32_t u[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        v[2 * k] = __uint_as_float(u[k] << 16);
+        v[2 * k + 1] = __uint_as_float(u[k] & 0xFFFF0000u);
+      }
+    } else {
+      const float4 a = reinterpret_cast<const float4*>(q.prim)[(b * 32 + lane) * 2];
+      const float4 c = reinterpret_cast<const float4*>(q.prim)[(b * 32 + lane) * 2 + 1];
+      v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = c.x; v[5] = c.y; v[6] = c.z; v[7] = c.w;
+    }
+    int nan = 0;
+    float mn = v[0], mx = v[0];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      nan |= isnan(v[k]);
+      mn = fminf(mn, v[k]);
+      mx = fmaxf(mx, v[k]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      nan |= __shfl_xor_sync(0xffffffffu, nan, o);
+    }
+    float scale = __fdiv_rn(__fsub_rn(mx, mn), 255.0f);
+    if (nan) {
+      mn = __int_as_float(0x7fc00000);
+      scale = mn;
+    }
+    uint32_t lo = 0, hi = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      int c = 0;
+      if (scale > 0.0f) {
+        c = __float2int_rn(__fdiv_rn(__fsub_rn(v[k], mn), scale));
+        c = c < 0 ? 0 : (c > 255 ? 255 : c);
+      }
+      if (k < 4) lo |= (uint32_t)c << (8 * k);
+      else hi |= (uint32_t)c << (8 * (k - 4));
+    }
+    reinterpret_cast<uint2*>(q.codes)[b * 32 + lane] = make_uint2(lo, hi);
+    if (lane == 0) q.params[b] = make_float2(mn, scale);
+  }
+  if (last_cta(q.done_ctr)) release_all(q.rel);   // E1: codes of step t+1 are ready
+}
+
+// qwZ forward gather: producer TMA-pulls 8192-element chunks of source j's codes (8 KiB)
+// and (min, scale) pairs (256 B); 8 consumer warps dequantize 8 elements per thread-step
+// (fp32 min + code*scale, then the parameter dtype), store 16-byte words to the full
+// buffer and — fused secondary store — to the secondary, and fingerprint them.
+constexpr int kQwChunk = 8192;
+constexpr int kQwStages = 4;
+constexpr int kQwConsumers = 256;
+__global__ void __launch_bounds__(32 + kQwConsumers, 1) gather_qwz_kernel(const __grid_constant__ GatherParams p) {
+  extern __shared__ __align__(1024) char smem[];
+  __shared__ __align__(8) uint64_t full_bar[kQwStages];
+  __shared__ __align__(8) uint64_t empty_bar[kQwStages];
+  __shared__ unsigned long long fp_red[kQwConsumers / 32];
+  constexpr int kStage = kQwChunk + kQwChunk / kQwzBlock * 8;
+  const int n_src = p.n_src;
+  const int64_t n_el = p.src_bytes;                     // codes: 1 byte per element
+  const int64_t chunks_per_src = (n_el + kQwChunk - 1) / kQwChunk;
+  const int64_t total = chunks_per_src * n_src;
+  const int64_t nk = blockIdx.x < total ? (total - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int eb = p.elem_bytes;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kQwStages; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], kQwConsumers / 32);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  auto chunk_of = [&](int64_t k, int& j, int64_t& off, uint32_t& cnt) {
+    const int64_t w = blockIdx.x + k * gridDim.x;
+    j = (int)(w % n_src);
+    off = (w / n_src) * kQwChunk;
+    const int64_t rem = n_el - off;
+    cnt = (uint32_t)(rem < kQwChunk ? rem : kQwChunk);
+  };
+  if (warp == 0) {
+    if (lane == 0) {
+      uint32_t waited = 0;
+      for (int64_t k = 0; k < nk; ++k) {
+        const int s = (int)(k % kQwStages);
+        if (k >= kQwStages) mbar_wait(&empty_bar[s], (uint32_t)(((k / kQwStages) - 1) & 1), p.sync);
+        int j;
+        int64_t off;
+        uint32_t cnt;
+        chunk_of(k, j, off, cnt);
+        if (!((waited >> j) & 1u)) {
+          if (p.src_flag[j] != nullptr) wait_geq(p.src_flag[j], p.src_target, p.sync);   // E1
+          fence_proxy_async();
+          waited |= 1u << j;
+        }
+        char* st = smem + (size_t)s * kStage;
+        mbar_expect_tx(&full_bar[s], cnt + cnt / kQwzBlock * 8);
+        tma_load(st, p.src[j] + off, cnt, &full_bar[s]);
+        tma_load(st + kQwChunk, p.qw_params[j] + off / kQwzBlock, cnt / kQwzBlock * 8, &full_bar[s]);
+      }
+    }
+  } else {
+    uint64_t fp = 0;
+    bool war_done = false;
+    for (int64_t k = 0; k < nk; ++k) {
+      const int s = (int)(k % kQwStages);
+      mbar_wait(&full_bar[s], (uint32_t)((k / kQwStages) & 1), p.sync);
+      int j;
+      int64_t off;
+      uint32_t cnt;
+      chunk_of(k, j, off, cnt);
+      const bool to_sec = p.sec != nullptr && j >= p.sec_lo && j < p.sec_hi;
+      if (to_sec && !war_done) {
+        // E4 once per thread before its first secondary store (cheap local flag reads)
+        wait_all(p.war, p.sync);
+        war_done = true;
+      }
+      const char* st = smem + (size_t)s * kStage;
+      const float2* prm = reinterpret_cast<const float2*>(st + kQwChunk);
+      for (uint32_t e = (threadIdx.x - 32) * 8; e < cnt; e += kQwConsumers * 8) {
+        const uint2 c = *reinterpret_cast<const uint2*>(st + e);
+        const float2 ms = prm[e / kQwzBlock];
+        float v[8];
+#pragma unroll
+        for (int k2 = 0; k2 < 8; ++k2) {
+          const uint32_t code = ((k2 < 4 ? c.x : c.y) >> (8 * (k2 & 3))) & 0xFFu;
+          v[k2] = __fadd_rn(ms.x, __fmul_rn((float)code, ms.y));
+        }
+        const int64_t ge = (int64_t)j * n_el + off + e;      // element index in the full buffer
+        if (eb == 2) {
+          uint4 w;
+          uint32_t* wp = &w.x;
+#pragma unroll
+          for (int k2 = 0; k2 < 4; ++k2) {
+            __nv_bfloat162 b2 = __floats2bfloat162_rn(v[2 * k2], v[2 * k2 + 1]);
+            wp[k2] = *reinterpret_cast<uint32_t*>(&b2);
+          }
+          reinterpret_cast<uint4*>(p.out)[ge / 8] = w;
+          if (to_sec) reinterpret_cast<uint4*>(p.sec)[((int64_t)(j - p.sec_lo) * n_el + off + e) / 8] = w;
+          if (p.fp_acc) fp += fp_word((uint32_t)(ge / 8), *reinterpret_cast<int4*>(&w));
+        } else {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const float4 w = make_float4(v[4 * h], v[4 * h + 1], v[4 * h + 2], v[4 * h + 3]);
+            reinterpret_cast<float4*>(p.out)[ge / 4 + h] = w;
+            if (to_sec) reinterpret_cast<float4*>(p.sec)[((int64_t)(j - p.sec_lo) * n_el + off + e) / 4 + h] = w;
+            if (p.fp_acc) fp += fp_word((uint32_t)(ge / 4 + h), *reinterpret_cast<const int4*>(&w));
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty_bar[s]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) fp += __shfl_xor_sync(0xffffffffu, fp, o);
+    if (lane == 0) fp_red[warp - 1] = fp;
+  }
+  __syncthreads();
+  if (p.fp_acc && threadIdx.x == 0) {
+    unsigned long long sum = 0;
+    for (int w = 0; w < kQwConsumers / 32; ++w) sum += fp_red[w];
+    if (sum) atomicAdd(p.fp_acc, sum);
+  }
+  if (last_cta(p.done_ctr)) {
+    if (p.fp_a != nullptr) {
+      wait_all(p.cmp_wait, p.sync);
+      const unsigned long long a = atomicExch(p.fp_a, 0ull);
+      const unsigned long long b = atomicExch(p.fp_b, 0ull);
+      atomicAdd(p.fp_checked, 1ull);
+      if (a != b) atomicAdd(p.fp_mism, 1ull);
+    }
+    release_all(p.rel);
+  }
+}
+
 }  // namespace
 
 cudaError_t launch_gather_tma(const GatherParams& p, int grid, cudaStream_t s) {
@@ -551,6 +742,23 @@ cudaError_t launch_gather_tma(const GatherParams& p, int grid, cudaStream_t s) {
     gather_tma_kernel<true><<<grid, 32 * (1 + kFpWarps), smem, s>>>(p);
   else
     gather_tma_kernel<false><<<grid, 32, smem, s>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_qwz_quantize(const QwzQuantParams& q, int grid, cudaStream_t s) {
+  qwz_quantize_kernel<<<grid, 256, 0, s>>>(q);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gather_qwz(const GatherParams& p, int grid, cudaStream_t s) {
+  constexpr int smem = kQwStages * (kQwChunk + kQwChunk / kQwzBlock * 8);
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(gather_qwz_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  gather_qwz_kernel<<<grid, 32 + kQwConsumers, smem, s>>>(p);
   return cudaGetLastError();
 }
 

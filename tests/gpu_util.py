@@ -28,18 +28,20 @@ class ParityRun:
 
     def __init__(self, numels, world, node_size, dtype="bf16", align=256, order="fixed",
                  verify="exact", grad_kind="uniform", n_grad_slots=None, stock_schedule="program",
-                 fused=False, store_grad_shard=True, copy_engine="tma", qgz=False, grad_dtype="f32"):
+                 fused=False, store_grad_shard=True, copy_engine="tma", qgz=False, grad_dtype="f32",
+                 qwz=False):
         from paper_2407_01614_b200 import hpz as H
         from paper_2407_01614_b200.world import EmulatedWorld
         self.H = H
         self.numels, self.P, self.Pp, self.dtype = list(numels), world, node_size, dtype
         self.grad_kind = grad_kind
         self.fused, self.store_grad_shard = fused, store_grad_shard
-        self.qgz, self.grad_dtype = qgz, grad_dtype
+        self.qgz, self.grad_dtype, self.qwz = qgz, grad_dtype, qwz
         self.w = EmulatedWorld(numels, world, node_size, dtype=dtype, align=align, n_grad_slots=n_grad_slots,
-                               timeout_s=10.0, qgz=qgz, grad_dtype=grad_dtype)
+                               timeout_s=10.0, qgz=qgz, grad_dtype=grad_dtype, qwz=qwz)
         self.o = O.HpzOracle(self.numels, world, node_size, align=align, param_dtype=dtype, order=order,
-                             stock_schedule=stock_schedule, grad_kind=grad_kind, qgz=qgz, grad_dtype=grad_dtype)
+                             stock_schedule=stock_schedule, grad_kind=grad_kind, qgz=qgz, grad_dtype=grad_dtype,
+                             qwz=qwz)
         self.stream = torch.cuda.current_stream()
         for rc in self.w.ranks:
             H.hpz_set_order(rc.ctx, order)

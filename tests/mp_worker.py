@@ -34,6 +34,7 @@ def main():
     ap.add_argument("--fused", type=int, default=1)
     ap.add_argument("--qgz", type=int, default=0)
     ap.add_argument("--grad-dtype", default="f32")
+    ap.add_argument("--qwz", type=int, default=0)
     args = ap.parse_args()
     local = int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
@@ -43,7 +44,8 @@ def main():
 
     numels = [int(x) for x in args.numels.split(",")]
     P, r = dist.get_world_size(), dist.get_rank()
-    W = DistWorld(numels, args.node_size, timeout_s=20.0, qgz=bool(args.qgz), grad_dtype=args.grad_dtype)
+    W = DistWorld(numels, args.node_size, timeout_s=20.0, qgz=bool(args.qgz), grad_dtype=args.grad_dtype,
+                  qwz=bool(args.qwz))
     rc = W.ranks[0]
     s = torch.cuda.current_stream()
     H.hpz_set_order(rc.ctx, args.order, stock_delay_us=args.stock_delay_us, stock_poison=args.order == "stock")
@@ -56,7 +58,7 @@ def main():
     fwd = [torch.zeros(x.numel_pad, dtype=torch.bfloat16, device="cuda") for x in rc.infos]
     bwd = [torch.zeros(x.numel_pad, dtype=torch.bfloat16, device="cuda") for x in rc.infos]
     o = O.HpzOracle(numels, P, args.node_size, order="off" if args.order == "off" else "fixed",
-                    qgz=bool(args.qgz), grad_dtype=args.grad_dtype)
+                    qgz=bool(args.qgz), grad_dtype=args.grad_dtype, qwz=bool(args.qwz))
     adam = H.make_adam()
     keep = []
     t_box = [0]

@@ -58,3 +58,10 @@ def test_multiproc_parity_bf16_grads(n, node):
     if n > NGPU:
         pytest.skip(f"needs {n} GPUs")
     _run(n, node, extra=("--grad-dtype", "bf16"), port=29911 + n * 10 + node)
+
+
+@pytest.mark.parametrize("n,node", [(2, 1), (4, 2)])
+def test_multiproc_parity_qwz_qgz(n, node):
+    if n > NGPU:
+        pytest.skip(f"needs {n} GPUs")
+    _run(n, node, extra=("--qwz", "1", "--qgz", "1"), port=30011 + n * 10 + node)

@@ -121,6 +121,31 @@ def test_parity_bf16_grads(P, Pp, fused):
         run.close()
 
 
+@pytest.mark.parametrize("P,Pp", [(1, 1), (2, 1), (4, 2), (8, 4), (8, 8), (3, 1)])
+@pytest.mark.parametrize("fused", [True, False])
+def test_parity_qwz(P, Pp, fused):
+    """f2 qwZ: INT8 blockwise weights in the forward gather, dequantized into the full
+    buffer and the secondary: bit-exact vs the oracle (same fp32 decisions)."""
+    run = ParityRun(NUMELS, P, Pp, qwz=True, fused=fused, verify="fingerprint")
+    try:
+        for _ in range(3):
+            _check_step(run, run.step())
+        c = run.counters()
+        assert c["timeouts"] == 0 and c["fp_mismatches"] == 0
+    finally:
+        run.close()
+
+
+def test_parity_qwz_fp32_params_and_qgz():
+    """qwZ with fp32 parameters, combined with qgZ gradients (the paper's Table 2 runs qgZ)."""
+    run = ParityRun(O.toy_layer_numels(), 4, 2, dtype="f32", qwz=True, qgz=True, fused=True, verify="fingerprint")
+    try:
+        for _ in range(2):
+            _check_step(run, run.step())
+    finally:
+        run.close()
+
+
 def test_parity_fused_off_order():
     run = ParityRun(NUMELS, 4, 2, order="off", fused=True)
     try:
