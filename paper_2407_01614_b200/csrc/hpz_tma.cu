@@ -647,9 +647,12 @@ __global__ void __launch_bounds__(32 + kQwConsumers, 1) gather_qwz_kernel(const 
           waited |= 1u << j;
         }
         char* st = smem + (size_t)s * kStage;
-        mbar_expect_tx(&full_bar[s], cnt + cnt / kQwzBlock * 8);
+        // bulk copies move multiples of 16 bytes: a one-block tail carries 8 bytes of
+        // (min, scale) plus 8 padding bytes (inside the 4 KiB-aligned params buffer)
+        const uint32_t pbytes = (cnt / kQwzBlock * 8 + 15) & ~15u;
+        mbar_expect_tx(&full_bar[s], cnt + pbytes);
         tma_load(st, p.src[j] + off, cnt, &full_bar[s]);
-        tma_load(st + kQwChunk, p.qw_params[j] + off / kQwzBlock, cnt / kQwzBlock * 8, &full_bar[s]);
+        tma_load(st + kQwChunk, p.qw_params[j] + off / kQwzBlock, pbytes, &full_bar[s]);
       }
     }
   } else {
