@@ -286,7 +286,7 @@ typedef enum {
                                     bf16; the reduce-scatter converts (exactly) to fp32 and
                                     reduces in fp32 in the R7 order — half the NVLink bytes.
                                     Set before hpz_register_flat_params; not with qgZ. */
-  HPZ_OPT_QWZ = 5                /* 0 (default) or 8: ZeRO++ qwZ ("quantizes weights
+  HPZ_OPT_QWZ = 5,               /* 0 (default) or 8: ZeRO++ qwZ ("quantizes weights
                                     before AllGather"; reading R28): after every
                                     optimizer step (and at load) the owner quantizes its primary
                                     shard blockwise to INT8 (256-element blocks, fp32 min +
@@ -297,6 +297,8 @@ typedef enum {
                                     unchanged and returns the same values.  Needs align_elems
                                     % 256 == 0; not with EXACT verification or ORDER_OFF.  Set
                                     before hpz_register_flat_params. */
+  HPZ_OPT_MAX_CTAS = 6           /* cap on the CTAs of every launch (0 = whole GPU): bounds the SMs
+                                    the collectives occupy while compute overlaps them (f3) */
 } hpz_option;
 /* Copy engine of the gathers and the reduce-scatter: TMA 1-D bulk copies through a
  * shared-memory stage ring (cp.async.bulk, one persistent CTA per SM), or 16-byte

@@ -65,6 +65,7 @@ struct hpz_ctx {
   int qgz_bits = 0;                       // f1: 4 = INT4 quantized gradient all-to-all
   int grad_bytes = 4;                     // f4: 2 = bf16 gradients (fp32 accumulation)
   int qwz_bits = 0;                       // f2: 8 = INT8 blockwise weights in the forward gather
+  int max_ctas = 0;                       // cap on every grid (0 = all SMs)
   std::vector<uint64_t> off_qcodes, off_qparams;   // per grad slot (qgZ)
   std::string err;
 
@@ -135,6 +136,7 @@ int check_layer(hpz_ctx* c, int layer) {
 
 int grid_for(const hpz_ctx* c, int64_t work_items, int per_sm) {
   int64_t g = (int64_t)c->sm_count * per_sm;
+  if (c->max_ctas > 0 && g > c->max_ctas) g = c->max_ctas;   // leave SMs to overlapped compute
   if (work_items < g) g = work_items;
   return g < 1 ? 1 : (int)g;
 }
@@ -946,6 +948,10 @@ int hpz_set_option(hpz_ctx* c, int option, int64_t value) {
       if (value != 0 && value != 4) return fail(c, HPZ_EINVAL, "qgZ bits must be 0 (off) or 4");
       if (value && c->grad_bytes != 4) return fail(c, HPZ_EINVAL, "qgZ quantizes fp32 gradients");
       c->qgz_bits = (int)value;
+      return HPZ_OK;
+    case HPZ_OPT_MAX_CTAS:
+      if (value < 0 || value > 1 << 20) return fail(c, HPZ_EINVAL, "max_ctas must be >= 0");
+      c->max_ctas = (int)value;
       return HPZ_OK;
     case HPZ_OPT_QWZ:
       if (c->registered) return fail(c, HPZ_ESTATE, "qwZ must be chosen before hpz_register_flat_params");
