@@ -38,7 +38,7 @@ def run(order, depth, args, world, rank, local, node_size):
         H.hpz_set_option(rc.ctx, "max_ctas", args.max_ctas)
     s = torch.cuda.current_stream()
     for i in range(args.layers):
-        H.hpz_synth_master(rc.ctx, i, S.stream_key(S.SEED_PARAMS, i, 0, 0), 2.0 ** -7, s)
+        H.hpz_synth_master(rc.ctx, i, S.stream_key(S.SEED_PARAMS, i, 0, 0), args.init_scale, s)
     g = torch.Generator(device="cuda").manual_seed(1234 + rank)
     x = (torch.randn(args.tokens, args.h, device="cuda", generator=g) * 0.5).to(torch.bfloat16)
     y = (torch.randn(args.tokens, args.h, device="cuda", generator=g) * 0.05).to(torch.bfloat16)
@@ -65,7 +65,7 @@ def run(order, depth, args, world, rank, local, node_size):
     return {"order": order, "prefetch_depth": depth, "ms_per_step": round(ms, 3),
             "tokens_per_s": round(tokens / (ms * 1e-3), 1),
             "tokens_per_s_per_node": round(tokens / (ms * 1e-3) / max(1, world // node_size), 1),
-            "loss_first": lv[0], "loss_last": lv[-1],
+            "loss_first": lv[0], "loss_last": lv[-1], "losses": [round(v, 6) for v in lv],
             "nan_loss": any(not math.isfinite(v) for v in lv),
             "fingerprint_mismatched_layers": c["fp_mismatches"], "timeouts": c["timeouts"]}
 
@@ -80,6 +80,7 @@ def main():
     ap.add_argument("--max-ctas", type=int, default=32)
     ap.add_argument("--stock-delay-us", type=int, default=2000)
     ap.add_argument("--configs", default="off:1,fixed:0,fixed:1,stock:1")
+    ap.add_argument("--init-scale", type=float, default=2.0 ** -5, help="uniform init bound (~sqrt(3/h))")
     args = ap.parse_args()
     import torch
     import torch.distributed as dist
