@@ -41,8 +41,8 @@ def run(order, depth, args, world, rank, local, node_size):
         H.hpz_synth_master(rc.ctx, i, S.stream_key(S.SEED_PARAMS, i, 0, 0), args.init_scale, s)
     g = torch.Generator(device="cuda").manual_seed(1234 + rank)
     x = (torch.randn(args.tokens, args.h, device="cuda", generator=g) * 0.5).to(torch.bfloat16)
-    y = (torch.randn(args.tokens, args.h, device="cuda", generator=g) * 0.05).to(torch.bfloat16)
-    tr = PrefetchTrainer(rc, args.h, args.layers, args.tokens, depth=depth)
+    y = (x.float() * 0.05).to(torch.bfloat16)     # learnable target: a scaled copy of the input
+    tr = PrefetchTrainer(rc, args.h, args.layers, args.tokens, depth=depth, lr=args.lr)
     torch.cuda.synchronize()
     losses = []
     for _ in range(args.warmup):
@@ -73,7 +73,7 @@ def run(order, depth, args, world, rank, local, node_size):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--h", type=int, default=4096)
-    ap.add_argument("--layers", type=int, default=16)
+    ap.add_argument("--layers", type=int, default=8)
     ap.add_argument("--tokens", type=int, default=2048)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
@@ -81,6 +81,7 @@ def main():
     ap.add_argument("--stock-delay-us", type=int, default=2000)
     ap.add_argument("--configs", default="off:1,fixed:0,fixed:1,stock:1")
     ap.add_argument("--init-scale", type=float, default=2.0 ** -5, help="uniform init bound (~sqrt(3/h))")
+    ap.add_argument("--lr", type=float, default=1e-5)
     args = ap.parse_args()
     import torch
     import torch.distributed as dist
