@@ -614,11 +614,13 @@ def unpartitioned_train(numels: list[int], world: int, steps: int, hyper: AdamHy
 
 
 def sampled_trajectory(layer: int, numel: int, world: int, idx: np.ndarray, steps: int,
-                       hyper: AdamHyper, param_dtype: str = "bf16", grad_scale: float | None = None):
+                       hyper: AdamHyper, param_dtype: str = "bf16", grad_scale: float | None = None,
+                       fixed_grads: bool = False):
     """Master/m/v/primary at full-layer element indices ``idx`` after ``steps`` steps
     with synthetic gradients: every quantity of the path is elementwise in the
     element index once the layout is fixed, so a sample is computed one element
-    at a time (same functions as the full simulation)."""
+    at a time (same functions as the full simulation).  ``fixed_grads``: every step
+    reuses the step-0 gradients (bench.py keeps its gradients resident)."""
     from synth import inputs as S
     gs = S.GRAD_SCALE if grad_scale is None else grad_scale
     idx = np.asarray(idx, dtype=np.int64)
@@ -626,7 +628,8 @@ def sampled_trajectory(layer: int, numel: int, world: int, idx: np.ndarray, step
     m = np.zeros(idx.size, F32)
     v = np.zeros(idx.size, F32)
     for t in range(steps):
-        grads = [S.values_at(S.SEED_GRADS, layer, t, r, idx, gs, numel) for r in range(world)]
+        tg = 0 if fixed_grads else t
+        grads = [S.values_at(S.SEED_GRADS, layer, tg, r, idx, gs, numel) for r in range(world)]
         g = (pairwise_rank_sum(grads) * F32(1.0 / world)).astype(F32)
         w, m, v = adam_update(w, m, v, g, adam_scalars(hyper, t + 1))
     return w, m, v, refresh_primary(w, param_dtype)
