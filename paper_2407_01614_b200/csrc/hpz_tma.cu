@@ -24,8 +24,7 @@ namespace hpz {
 
 namespace {
 
-constexpr int kGatherChunk = 32768;     // bytes per gather stage
-constexpr int kGatherStages = 4;
+constexpr int kGatherMaxStages = 8;     // stage ring (runtime: GatherParams::tma_stages x tma_chunk bytes)
 constexpr int kFpWarps = 4;             // fingerprint consumer warps
 constexpr int kRsChunk = 1024;          // base shard elements per RS stage
 constexpr int kRsMaxConsumers = 512;    // up to 16 consumer warps (one float4 each per chunk)
@@ -166,11 +165,13 @@ __device__ __forceinline__ uint64_t fp_word(uint32_t gi, const int4& w) {
 // Block = 1 producer warp (+ kFpWarps fingerprint warps when FP).  Dynamic smem =
 // kGatherStages * kGatherChunk.
 template <bool FP>
-__global__ void __launch_bounds__(32 * (1 + kFpWarps), 1)
+__global__ void __launch_bounds__(32 * (1 + kFpWarps))
     gather_tma_kernel(const __grid_constant__ GatherParams p) {
   extern __shared__ __align__(1024) char smem[];
-  __shared__ __align__(8) uint64_t full_bar[kGatherStages];
-  __shared__ __align__(8) uint64_t empty_bar[kGatherStages];
+  __shared__ __align__(8) uint64_t full_bar[kGatherMaxStages];
+  __shared__ __align__(8) uint64_t empty_bar[kGatherMaxStages];
+  const int kGatherChunk = p.tma_chunk;
+  const int kGatherStages = p.tma_stages;
   __shared__ unsigned long long fp_red[kFpWarps];
 
   const int n_src = p.n_src;
@@ -732,12 +733,13 @@ __global__ void __launch_bounds__(32 + kQwConsumers, 1) gather_qwz_kernel(const 
 }  // namespace
 
 cudaError_t launch_gather_tma(const GatherParams& p, int grid, cudaStream_t s) {
-  const int smem = kGatherStages * kGatherChunk;
+  const int smem = p.tma_stages * p.tma_chunk;
   static bool attr_set[2] = {false, false};
   const bool fp = p.fp_acc != nullptr;
   if (!attr_set[fp]) {
-    cudaError_t e = fp ? cudaFuncSetAttribute(gather_tma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)
-                       : cudaFuncSetAttribute(gather_tma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    constexpr int kMaxSmem = 200 * 1024;
+    cudaError_t e = fp ? cudaFuncSetAttribute(gather_tma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem)
+                       : cudaFuncSetAttribute(gather_tma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
     if (e != cudaSuccess) return e;
     attr_set[fp] = true;
   }
