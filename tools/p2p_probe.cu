@@ -126,6 +126,7 @@ int main(int argc, char** argv) {
   int64_t mb = argc > 3 ? atoll(argv[3]) : 256;
   int ctas_per_sm = argc > 4 ? atoi(argv[4]) : 4;
   int chunk = argc > 5 ? atoi(argv[5]) : 32768;
+  const bool with_self = argc > 6 && atoi(argv[6]) != 0;   // also copy the local buffer (like a gather)
   int ndev = 0;
   CK(cudaGetDeviceCount(&ndev));
   if (G > ndev) G = ndev;
@@ -157,7 +158,7 @@ int main(int argc, char** argv) {
     p.n = 0;
     p.bytes = bytes;
     for (int h = 0; h < G; ++h) {
-      if (h == g) continue;
+      if (h == g && !with_self) continue;
       if (pull) {   // g reads peer h's src into its own dst region h
         p.src[p.n] = buf_src[h];
         p.dst[p.n] = buf_dst[g] + (int64_t)h * bytes;
@@ -189,7 +190,7 @@ int main(int argc, char** argv) {
       CK(cudaEventSynchronize(e1[g]));
       float ms = 0;
       CK(cudaEventElapsedTime(&ms, e0[g], e1[g]));
-      double gbs = (double)bytes * (G - 1) / (ms * 1e-3) / 1e9;
+      double gbs = (double)bytes * (G - 1) / (ms * 1e-3) / 1e9;   // peer (NVLink) bytes only
       if (gbs < worst) worst = gbs;
       sum += gbs;
     }
