@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "hpz_device.cuh"
 #include "hpz_internal.h"
 
 namespace hpz {
@@ -52,7 +53,6 @@ __device__ __forceinline__ uint32_t mbar_try(uint64_t* bar, uint32_t parity) {
       : "memory");
   return done;
 }
-__device__ __forceinline__ uint64_t globaltimer_();
 // Bounded mbarrier wait: a pipeline that never completes (lost bulk copy, aborted peer)
 // records a timeout and returns instead of hanging the GPU.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity, const SyncCommon& sc) {
@@ -60,7 +60,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity, const 
   uint64_t t0 = 0;
   while (!mbar_try(bar, parity)) {
     if ((++spins & 4095u) == 0) {          // rare: only a stalled pipeline reaches the clock
-      const uint64_t now = globaltimer_();
+      const uint64_t now = globaltimer();
       if (t0 == 0) {
         t0 = now;
       } else if (now - t0 > sc.timeout_ns) {
@@ -96,74 +96,9 @@ __device__ __forceinline__ void fence_mbar_init() {
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
 
-__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
-  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ uint64_t globaltimer() {
-  uint64_t t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-__device__ __forceinline__ uint64_t globaltimer_() { return globaltimer(); }
-__device__ bool wait_geq(const uint32_t* flag, uint32_t target, const SyncCommon& s) {
-  if (ld_acquire_sys(flag) >= target) return true;
-  if (*(volatile uint32_t*)s.abort_flag) return false;
-  const uint64_t t0 = globaltimer();
-  uint32_t spins = 0;
-  while (ld_acquire_sys(flag) < target) {
-    if ((++spins & 63u) == 0) {
-      if (*(volatile uint32_t*)s.abort_flag) return false;
-      if (globaltimer() - t0 > s.timeout_ns) {
-        atomicAdd(s.timeouts, 1ull);
-        atomicExch(s.abort_flag, 1u);
-        *s.host_err = 1u;
-        __threadfence_system();
-        return false;
-      }
-    }
-    __nanosleep(32);
-  }
-  return true;
-}
-__device__ void wait_all(const WaitList& w, const SyncCommon& s) {
-  for (int k = 0; k < w.n; ++k) wait_geq(w.ptr[k], w.target, s);
-}
-__device__ void release_all(const ReleaseList& r) {
-  for (int k = 0; k < r.n; ++k) st_release_sys(r.ptr[k], r.value);
-}
-__device__ __forceinline__ bool last_cta(uint32_t* ctr) {
-  __syncthreads();
-  bool last = false;
-  if (threadIdx.x == 0) {
-    __threadfence_system();
-    const uint32_t prev = atomicAdd(ctr, 1u);
-    if (prev == gridDim.x - 1) {
-      *ctr = 0u;
-      __threadfence_system();
-      last = true;
-    }
-  }
-  return last;
-}
-__device__ __forceinline__ uint64_t fp_word(uint32_t gi, const int4& w) {
-  uint32_t h = (uint32_t)w.x * 0x85EBCA6Bu ^ (uint32_t)w.y * 0xC2B2AE35u ^ (uint32_t)w.z * 0x27D4EB2Fu ^
-               (uint32_t)w.w * 0x165667B1u ^ gi * 0x9E3779B1u;
-  h ^= h >> 15;
-  h *= 0x2C1B3C6Du;
-  h ^= h >> 12;
-  uint32_t h2 = h * 0x297A2D39u;
-  h2 ^= h2 >> 16;
-  return ((uint64_t)h2 << 32) | h;
-}
-
 // ------------------------------------------------------------------ gather (a2, a4)
 // Block = 1 producer warp (+ kFpWarps fingerprint warps when FP).  Dynamic smem =
-// kGatherStages * kGatherChunk.
+// tma_stages * tma_chunk bytes.
 template <bool FP>
 __global__ void __launch_bounds__(32 * (1 + kFpWarps))
     gather_tma_kernel(const __grid_constant__ GatherParams p) {
@@ -286,27 +221,6 @@ __global__ void __launch_bounds__(32 * (1 + kFpWarps))
 }
 
 // ------------------------------------------------------------------ RS (+ Adam) (a5, a6)
-__device__ __forceinline__ float4 add4(const float4& a, const float4& b) {
-  return make_float4(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y), __fadd_rn(a.z, b.z), __fadd_rn(a.w, b.w));
-}
-template <int P>
-__device__ __forceinline__ float4 pairwise_sum(float4 (&x)[P]) {
-#pragma unroll
-  for (int n = P; n > 1; n = (n + 1) / 2) {
-#pragma unroll
-    for (int k = 0; k < n / 2; ++k) x[k] = add4(x[2 * k], x[2 * k + 1]);
-    if (n & 1) x[n / 2] = x[n - 1];
-  }
-  return x[0];
-}
-__device__ __forceinline__ void adam1(float& w, float& m, float& v, float g, const AdamParams& p) {
-  m = __fadd_rn(__fmul_rn(p.beta1, m), __fmul_rn(p.omb1, g));
-  v = __fadd_rn(__fmul_rn(p.beta2, v), __fmul_rn(__fmul_rn(p.omb2, g), g));
-  const float d = __fadd_rn(__fdiv_rn(__fsqrt_rn(v), p.bc2_sqrt), p.eps);
-  if (p.lr_wd != 0.0f) w = __fsub_rn(w, __fmul_rn(p.lr_wd, w));
-  w = __fsub_rn(w, __fmul_rn(p.step_size, __fdiv_rn(m, d)));
-}
-
 enum RsMode { RS_F32 = 0, RS_BF16 = 1, RS_QGZ = 2 };
 
 template <int P, bool ADAM, int MODE>
