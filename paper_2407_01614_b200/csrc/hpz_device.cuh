@@ -115,5 +115,20 @@ __device__ __forceinline__ void adam1(float& w, float& m, float& v, float g, con
   w = __fsub_rn(w, __fmul_rn(p.step_size, __fdiv_rn(m, d)));
 }
 
+// Blockwise quantization code round-half-even((v - mn) / scale) clamped to [0, maxc] —
+// bit-identical to the IEEE quotient the oracle rounds (R26, R28) but without a division
+// per element: q1 = (v - mn) * RN(1/scale) differs from RN((v - mn)/scale) by less than
+// 1.5 * 2^-23 * q <= 2^-14.4 for q <= 255, so unless q1 lies within `tie_eps` (2^-17 for
+// 4-bit, 2^-13 for 8-bit codes) of a half-integer both round to the same integer; near a
+// tie (or for NaN / inf) the exact quotient is computed.  Caller guarantees scale > 0.
+__device__ __forceinline__ int quant_code(float v, float mn, float scale, float rcp, int maxc, float tie_eps) {
+  const float a = __fsub_rn(v, mn);
+  float q = __fmul_rn(a, rcp);
+  const float fr = __fsub_rn(q, floorf(q));
+  if (!(fabsf(__fsub_rn(fr, 0.5f)) >= tie_eps)) q = __fdiv_rn(a, scale);
+  int c = __float2int_rn(q);
+  return c < 0 ? 0 : (c > maxc ? maxc : c);
+}
+
 }  // namespace
 }  // namespace hpz

@@ -431,17 +431,14 @@ __global__ void __launch_bounds__(256) qgz_quantize_kernel(const __grid_constant
       scale = mn;
     }
     const bool pos = scale > 0.0f;
+    const float rcp = pos ? __frcp_rn(scale) : 0.0f;
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const float e[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
       uint32_t packed = 0;
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        int c = 0;
-        if (pos) {
-          c = __float2int_rn(__fdiv_rn(__fsub_rn(e[k], mn), scale));
-          c = c < 0 ? 0 : (c > 15 ? 15 : c);
-        }
+        const int c = pos ? quant_code(e[k], mn, scale, rcp, 15, 0x1p-17f) : 0;
         packed |= (uint32_t)c << (4 * k);
       }
       c16[b * 16 + sub + 4 * u] = (uint16_t)packed;
@@ -495,13 +492,11 @@ __global__ void __launch_bounds__(256) qwz_quantize_kernel(const __grid_constant
       scale = mn;
     }
     uint32_t lo = 0, hi = 0;
+    const bool pos = scale > 0.0f;
+    const float rcp = pos ? __frcp_rn(scale) : 0.0f;
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
-      int c = 0;
-      if (scale > 0.0f) {
-        c = __float2int_rn(__fdiv_rn(__fsub_rn(v[k], mn), scale));
-        c = c < 0 ? 0 : (c > 255 ? 255 : c);
-      }
+      const int c = pos ? quant_code(v[k], mn, scale, rcp, 255, 0x1p-13f) : 0;
       if (k < 4) lo |= (uint32_t)c << (8 * k);
       else hi |= (uint32_t)c << (8 * (k - 4));
     }

@@ -303,3 +303,63 @@ def test_missing_peer_times_out_instead_of_hanging():
         assert e.value.code == H.HPZ_ETIMEOUT
     finally:
         w.close()
+
+
+@pytest.mark.parametrize("P", [1, 2])
+def test_qgz_quantizer_ties_and_edges(P):
+    """The division-free quantizer (quant_code) must reproduce round-half-even of the IEEE
+    quotient exactly, including exact ties, near-ties, constant blocks, tiny/huge scales."""
+    from paper_2407_01614_b200 import hpz as H
+    from paper_2407_01614_b200.world import EmulatedWorld, buffer_view, run_step
+    rng = np.random.default_rng(3)
+    n = 64 * 64
+    blocks = []
+    for b in range(64):
+        kind = b % 8
+        base = np.zeros(64, np.float32)
+        if kind == 0:   # exact ties: mn 0, mx 15 -> scale 1, values k + 0.5
+            base = (np.arange(64) % 16).astype(np.float32) + np.float32(0.5) * (np.arange(64) % 2)
+            base[0], base[1] = 0.0, 15.0
+        elif kind == 1:  # scaled ties (scale 2^-10)
+            base = ((np.arange(64) % 31) * 0.5).astype(np.float32) * np.float32(2 ** -10)
+            base[0], base[1] = 0.0, 15.0 * 2 ** -10
+        elif kind == 2:  # near ties: one ulp either side of k + 0.5 (scale 1)
+            k = (np.arange(64) % 15).astype(np.float32) + np.float32(0.5)
+            base = np.where(np.arange(64) % 2 == 0, np.nextafter(k, np.float32(0)), np.nextafter(k, np.float32(20)))
+            base = base.astype(np.float32)
+            base[0], base[1] = 0.0, 15.0
+        elif kind == 3:  # constant block
+            base[:] = np.float32(0.3)
+        elif kind == 4:  # tiny dynamic range
+            base = (np.float32(1.0) + rng.integers(0, 16, 64).astype(np.float32) * np.float32(2 ** -23)).astype(np.float32)
+        elif kind == 5:  # huge values
+            base = (rng.standard_normal(64) * 1e30).astype(np.float32)
+        else:
+            base = (rng.standard_normal(64) * 10 ** rng.uniform(-8, 3)).astype(np.float32)
+        blocks.append(base)
+    g_full = np.concatenate(blocks).astype(np.float32)
+    from oracle import hpz_oracle as O
+    w = EmulatedWorld([n], P, 1, qgz=True, timeout_s=10.0)
+    try:
+        s = torch.cuda.current_stream()
+        w0 = torch.zeros(n, dtype=torch.float32, device="cuda")
+        for rc in w.ranks:
+            H.hpz_load_master(rc.ctx, 0, w0.data_ptr(), s)
+        out = [torch.empty(rc.infos[0].numel_pad, dtype=torch.bfloat16, device="cuda") for rc in w.ranks]
+        gs = [torch.from_numpy(g_full * np.float32(r + 1)).cuda() for r in range(P)]
+
+        def grad_fn(rc, i):
+            H.hpz_grad_upload(rc.ctx, i, gs[rc.rank].data_ptr(), n, s)
+
+        run_step(w.ranks, [lambda i, r=r: out[r].data_ptr() for r in range(P)],
+                 [lambda i, r=r: out[r].data_ptr() for r in range(P)], H.make_adam(), stream=s,
+                 grad_fn=grad_fn, emulated=True)
+        torch.cuda.synchronize()
+        lay = O.LayerLayout(n, P, 1, 256)
+        G = [O.pad_full(g_full * np.float32(r + 1), lay) for r in range(P)]
+        for rc in w.ranks:
+            got = buffer_view(rc, 0, "grad_shard", "f32").cpu().numpy()
+            ref = O.qgz_reduce_scatter(G, lay, rc.rank)
+            assert np.array_equal(got.view(np.uint32), ref.view(np.uint32))
+    finally:
+        w.close()
