@@ -33,7 +33,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
            "-Xptxas", "-v" if verbose else "-O3",
            "-o", LIB + ".tmp"] + [os.path.join(CSRC, s) for s in SOURCES]
     # exported C ABI: hidden visibility by default, extern "C" functions re-exported below
-    cmd += ["-Xcompiler", "-Wall"]
+    cmd += ["-Xcompiler", "-Wall"] + os.environ.get("HPZ_NVCC_FLAGS", "").split()
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
