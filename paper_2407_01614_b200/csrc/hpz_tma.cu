@@ -162,7 +162,7 @@ __global__ void __launch_bounds__(32 * (1 + kFpWarps))
       for (int64_t k = 0; k < pre; ++k) issue_load(k);
       for (int64_t k = 0; k < nk; ++k) {
         const int s = (int)(k % kGatherStages);
-        mbar_wait_bounded(&full_bar[s], (uint32_t)((k / kGatherStages) & 1), p.sync);
+        mbar_wait(&full_bar[s], (uint32_t)((k / kGatherStages) & 1));   // issued bulk loads always land
         int j;
         int64_t off;
         uint32_t bytes;
