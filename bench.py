@@ -48,7 +48,6 @@ def parse():
                     help="separate reduce-scatter and Adam kernels (default: fused per-layer RS+Adam)")
     ap.add_argument("--ctas-per-sm", type=int, default=None)
     ap.add_argument("--copy-engine", default="tma", choices=["tma", "ldg"])
-    ap.add_argument("--tma", default=None, help="gather TMA geometry chunk_bytes,stages,ctas_per_sm")
     ap.add_argument("--qgz", action="store_true", help="ZeRO++ qgZ: INT4 gradient all-to-all (SURVEY f1)")
     ap.add_argument("--qwz", action="store_true", help="ZeRO++ qwZ: INT8 weights in the forward gather (SURVEY f2)")
     ap.add_argument("--grad-dtype", default="f32", choices=["f32", "bf16"],
@@ -201,11 +200,6 @@ def main():
     if args.ctas_per_sm:
         H.hpz_set_option(ctx, "ctas_per_sm", args.ctas_per_sm)
     H.hpz_set_option(ctx, "copy_engine", H.COPY[args.copy_engine])
-    if args.tma:
-        ch, st, cp = (int(v) for v in args.tma.split(","))
-        H.hpz_set_option(ctx, "tma_chunk", ch)
-        H.hpz_set_option(ctx, "tma_stages", st)
-        H.hpz_set_option(ctx, "tma_ctas_per_sm", cp)
     stream = torch.cuda.current_stream()
     infos = rc.infos
     # resident inputs: initial params (device generator) and this rank's gradients

@@ -297,12 +297,8 @@ typedef enum {
                                     unchanged and returns the same values.  Needs align_elems
                                     % 256 == 0; not with EXACT verification or ORDER_OFF.  Set
                                     before hpz_register_flat_params. */
-  HPZ_OPT_MAX_CTAS = 6,          /* cap on the CTAs of every launch (0 = whole GPU): bounds the SMs
+  HPZ_OPT_MAX_CTAS = 6           /* cap on the CTAs of every launch (0 = whole GPU): bounds the SMs
                                     the collectives occupy while compute overlaps them (f3) */
-  HPZ_OPT_TMA_CHUNK = 7,         /* gather TMA stage bytes (4..64 KiB, default 32 KiB) */
-  HPZ_OPT_TMA_STAGES = 8,        /* gather TMA ring depth (2..8, default 4) */
-  HPZ_OPT_TMA_CTAS_PER_SM = 9    /* gather TMA CTAs per SM (1..4, default 1); chunk x stages x
-                                    ctas must stay <= 200 KiB of shared memory */
 } hpz_option;
 /* Copy engine of the gathers and the reduce-scatter: TMA 1-D bulk copies through a
  * shared-memory stage ring (cp.async.bulk, one persistent CTA per SM), or 16-byte

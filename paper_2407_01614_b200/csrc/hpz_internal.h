@@ -64,9 +64,6 @@ struct GatherParams {
   // qwZ (f2): src[j] are INT8 codes (1 byte per element, src_bytes = shard elements) and
   // qw_params[j] their (min, scale) per 256 elements; the kernel dequantizes to elem_bytes
   const float2* qw_params[kMaxWorld];
-  // TMA engine geometry (gather_tma_kernel): stage ring of tma_stages x tma_chunk bytes
-  int tma_chunk;
-  int tma_stages;
   SyncCommon sync;
 };
 

@@ -66,7 +66,6 @@ struct hpz_ctx {
   int grad_bytes = 4;                     // f4: 2 = bf16 gradients (fp32 accumulation)
   int qwz_bits = 0;                       // f2: 8 = INT8 blockwise weights in the forward gather
   int max_ctas = 0;                       // cap on every grid (0 = all SMs)
-  int tma_chunk = 32768, tma_stages = 4, tma_ctas_per_sm = 1;   // gather TMA geometry
   std::vector<uint64_t> off_qcodes, off_qparams;   // per grad slot (qgZ)
   std::string err;
 
@@ -148,12 +147,8 @@ uint32_t epoch(int64_t x) { return (uint32_t)x; }
 // verification, or when selected with HPZ_OPT_COPY_ENGINE).
 cudaError_t gather_launch(const hpz_ctx* c, const GatherParams& p, cudaStream_t s) {
   if (c->copy_engine == HPZ_COPY_TMA && p.mism == nullptr) {
-    if ((int64_t)c->tma_chunk * c->tma_stages * c->tma_ctas_per_sm > 200 * 1024) return cudaErrorInvalidConfiguration;
-    GatherParams q = p;
-    q.tma_chunk = c->tma_chunk;
-    q.tma_stages = c->tma_stages;
-    const int64_t chunks = (p.src_bytes + c->tma_chunk - 1) / c->tma_chunk * p.n_src;
-    return launch_gather_tma(q, grid_for(c, chunks, c->tma_ctas_per_sm), s);
+    const int64_t chunks = (p.src_bytes + 32767) / 32768 * p.n_src;
+    return launch_gather_tma(p, grid_for(c, chunks, 1), s);
   }
   const int64_t tiles = (p.src_bytes / 16 + 2047) / 2048 * p.n_src;
   return launch_gather(p, grid_for(c, tiles, c->ctas_per_sm), s);
@@ -953,18 +948,6 @@ int hpz_set_option(hpz_ctx* c, int option, int64_t value) {
       if (value != 0 && value != 4) return fail(c, HPZ_EINVAL, "qgZ bits must be 0 (off) or 4");
       if (value && c->grad_bytes != 4) return fail(c, HPZ_EINVAL, "qgZ quantizes fp32 gradients");
       c->qgz_bits = (int)value;
-      return HPZ_OK;
-    case HPZ_OPT_TMA_CHUNK:
-      if (value < 4096 || value > 65536 || value % 1024) return fail(c, HPZ_EINVAL, "tma_chunk must be 4..64 KiB, a multiple of 1 KiB");
-      c->tma_chunk = (int)value;
-      return HPZ_OK;
-    case HPZ_OPT_TMA_STAGES:
-      if (value < 2 || value > 8) return fail(c, HPZ_EINVAL, "tma_stages must be in [2, 8]");
-      c->tma_stages = (int)value;
-      return HPZ_OK;
-    case HPZ_OPT_TMA_CTAS_PER_SM:
-      if (value < 1 || value > 4) return fail(c, HPZ_EINVAL, "tma_ctas_per_sm must be in [1, 4]");
-      c->tma_ctas_per_sm = (int)value;
       return HPZ_OK;
     case HPZ_OPT_MAX_CTAS:
       if (value < 0 || value > 1 << 20) return fail(c, HPZ_EINVAL, "max_ctas must be >= 0");

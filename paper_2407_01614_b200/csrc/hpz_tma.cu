@@ -25,7 +25,8 @@ namespace hpz {
 
 namespace {
 
-constexpr int kGatherMaxStages = 8;     // stage ring (runtime: GatherParams::tma_stages x tma_chunk bytes)
+constexpr int kGatherChunk = 32768;     // bytes per gather stage (a 4..64 KiB, 1..3 CTA/SM sweep
+constexpr int kGatherStages = 4;        // at N=1 and N=4 found no better geometry; profiles/README.md)
 constexpr int kFpWarps = 4;             // fingerprint consumer warps
 constexpr int kRsChunk = 1024;          // base shard elements per RS stage
 constexpr int kRsMaxConsumers = 512;    // up to 16 consumer warps (one float4 each per chunk)
@@ -106,15 +107,13 @@ __device__ __forceinline__ void fence_mbar_init() {
 
 // ------------------------------------------------------------------ gather (a2, a4)
 // Block = 1 producer warp (+ kFpWarps fingerprint warps when FP).  Dynamic smem =
-// tma_stages * tma_chunk bytes.
+// kGatherStages * kGatherChunk bytes.
 template <bool FP>
-__global__ void __launch_bounds__(32 * (1 + kFpWarps))
+__global__ void __launch_bounds__(32 * (1 + kFpWarps), 1)
     gather_tma_kernel(const __grid_constant__ GatherParams p) {
   extern __shared__ __align__(1024) char smem[];
-  __shared__ __align__(8) uint64_t full_bar[kGatherMaxStages];
-  __shared__ __align__(8) uint64_t empty_bar[kGatherMaxStages];
-  const int kGatherChunk = p.tma_chunk;
-  const int kGatherStages = p.tma_stages;
+  __shared__ __align__(8) uint64_t full_bar[kGatherStages];
+  __shared__ __align__(8) uint64_t empty_bar[kGatherStages];
   __shared__ unsigned long long fp_red[kFpWarps];
 
   const int n_src = p.n_src;
@@ -659,13 +658,12 @@ __global__ void __launch_bounds__(32 + kQwConsumers, 1) gather_qwz_kernel(const 
 }  // namespace
 
 cudaError_t launch_gather_tma(const GatherParams& p, int grid, cudaStream_t s) {
-  const int smem = p.tma_stages * p.tma_chunk;
+  const int smem = kGatherStages * kGatherChunk;
   static bool attr_set[2] = {false, false};
   const bool fp = p.fp_acc != nullptr;
   if (!attr_set[fp]) {
-    constexpr int kMaxSmem = 200 * 1024;
-    cudaError_t e = fp ? cudaFuncSetAttribute(gather_tma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem)
-                       : cudaFuncSetAttribute(gather_tma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
+    cudaError_t e = fp ? cudaFuncSetAttribute(gather_tma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)
+                       : cudaFuncSetAttribute(gather_tma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     attr_set[fp] = true;
   }

@@ -29,7 +29,7 @@ EXPORTED = [
     "hpz_grad_buffer", "hpz_grad_upload", "hpz_synth_grads", "hpz_grads_ready",
     "hpz_reduce_scatter", "hpz_step", "hpz_reduce_scatter_adam", "hpz_set_option",
 ]
-OPT = {"store_grad_shard": 0, "ctas_per_sm": 1, "copy_engine": 2, "qgz": 3, "grad_dtype": 4, "qwz": 5, "max_ctas": 6, "tma_chunk": 7, "tma_stages": 8, "tma_ctas_per_sm": 9}
+OPT = {"store_grad_shard": 0, "ctas_per_sm": 1, "copy_engine": 2, "qgz": 3, "grad_dtype": 4, "qwz": 5, "max_ctas": 6}
 COPY = {"ldg": 0, "tma": 1}
 
 
