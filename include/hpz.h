@@ -78,8 +78,12 @@ typedef enum { HPZ_F32 = 0, HPZ_BF16 = 1 } hpz_dtype;
  *          a separate copy on a side stream after the forward gather, optionally preceded
  *          by a poison fill (torch.empty analog) and a delay, and backward
  *          gathers do not wait for it.
- *  OFF   : no hpZ (plain ZeRO-3) — no secondary; backward gathers over all P primaries. */
-typedef enum { HPZ_ORDER_FIXED = 0, HPZ_ORDER_STOCK = 1, HPZ_ORDER_OFF = 2 } hpz_order;
+ *  OFF   : no hpZ (plain ZeRO-3) — no secondary; backward gathers over all P primaries.
+ *  PAPER : the paper's own fix, literally (Alg. 1 blue lines): the stock side-stream copy,
+ *          then hpz_bwd_gather blocks the HOST until that layer's copy finished before it
+ *          enqueues the gather (plus the device-side acquire of the node peers' copies that
+ *          P2P pulls need).  Correct like FIXED; kept to measure the host stall FIXED avoids. */
+typedef enum { HPZ_ORDER_FIXED = 0, HPZ_ORDER_STOCK = 1, HPZ_ORDER_OFF = 2, HPZ_ORDER_PAPER = 3 } hpz_order;
 
 /* Stale-parameter detection (a7):
  *  NONE        : off.

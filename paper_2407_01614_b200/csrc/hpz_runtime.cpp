@@ -58,6 +58,7 @@ struct hpz_ctx {
   uint32_t* host_err_dev = nullptr;
   cudaStream_t side = nullptr;            // stock-mode copy stream
   cudaEvent_t side_ev = nullptr;
+  std::vector<cudaEvent_t> copy_ev;       // ORDER_PAPER: per-layer "MemcpyD2D finished" host events
   uint64_t launches = 0;
   bool store_grad_shard = true;           // fused RS+Adam also stores the reduced gradient
   int ctas_per_sm = 4;                    // LDG/STG kernels
@@ -378,6 +379,8 @@ int hpz_arena_alloc(hpz_ctx* c, void* ipc_handle_out) {
 static int finish_bind(hpz_ctx* c) {
   HPZ_CUDA(c, cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
   HPZ_CUDA(c, cudaEventCreateWithFlags(&c->side_ev, cudaEventDisableTiming));
+  c->copy_ev.assign(c->n_layers, nullptr);
+  for (auto& ev : c->copy_ev) HPZ_CUDA(c, cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
   c->bound = true;
   return HPZ_OK;
 }
@@ -436,6 +439,8 @@ int hpz_finalize(hpz_ctx* c) {
   if (c->owns_arena && c->arena[c->rank]) cudaFree(c->arena[c->rank]);
   if (c->side) cudaStreamDestroy(c->side);
   if (c->side_ev) cudaEventDestroy(c->side_ev);
+  for (auto ev : c->copy_ev)
+    if (ev) cudaEventDestroy(ev);
   if (c->host_err) cudaFreeHost(c->host_err);
   delete c;
   return HPZ_OK;
@@ -521,7 +526,7 @@ const char* hpz_last_error(const hpz_ctx* c) { return c ? c->err.c_str() : "null
 
 int hpz_set_order(hpz_ctx* c, int order, int stock_delay_us, int stock_poison) {
   if (!c) return HPZ_EINVAL;
-  if (order < HPZ_ORDER_FIXED || order > HPZ_ORDER_OFF || stock_delay_us < 0) return fail(c, HPZ_EINVAL, "bad order");
+  if (order < HPZ_ORDER_FIXED || order > HPZ_ORDER_PAPER || stock_delay_us < 0) return fail(c, HPZ_EINVAL, "bad order");
   c->order = order;
   c->stock_delay_us = stock_delay_us;
   c->stock_poison = stock_poison;
@@ -606,13 +611,23 @@ int hpz_fwd_gather(hpz_ctx* c, int layer, void* full_out, void* stream) {
   }
   if (e != cudaSuccess) return fail(c, HPZ_ECUDA, "fwd gather launch: %s", cudaGetErrorString(e));
   c->launches += 1;
-  if (c->order == HPZ_ORDER_STOCK) {
-    // stock ZeRO++: L_i,second <- empty(); async MemcpyD2D on another stream, no edge to the
-    // backward AllGather
+  if (c->order == HPZ_ORDER_STOCK || c->order == HPZ_ORDER_PAPER) {
+    // L_i,second <- empty(); async MemcpyD2D on another stream.  STOCK:
+    // no edge to the backward AllGather (the race).  PAPER: the copy is
+    // followed by an event the backward gather waits for on the HOST (Alg. 1 blue lines)
     char* sec = c->arena[c->rank] + L.off_secondary;
     const int64_t sec_bytes = L.sec_shard * c->elem;
     HPZ_CUDA(c, cudaEventRecord(c->side_ev, s));
     HPZ_CUDA(c, cudaStreamWaitEvent(c->side, c->side_ev, 0));
+    if (c->order == HPZ_ORDER_PAPER && c->t > 0) {
+      // E4 (P2P needs it; NCCL's rendezvous would cover it): node peers' step t-1 reads done
+      WaitList w{};
+      for (int q = 0; q < c->node_size; ++q) w.ptr[w.n++] = c->flag(c->rank, F_BWD_DONE, layer, nf + q);
+      w.target = epoch(c->t);
+      e = launch_wait(w, c->sync(), c->side);
+      if (e != cudaSuccess) return fail(c, HPZ_ECUDA, "wait launch: %s", cudaGetErrorString(e));
+      c->launches += 1;
+    }
     if (c->stock_poison) {
       e = launch_fill_u32(sec, c->elem == 2 ? 0x7FC07FC0u : 0x7FC00000u, sec_bytes, grid_for(c, sec_bytes / 4096 + 1, 4), c->side);
       if (e != cudaSuccess) return fail(c, HPZ_ECUDA, "poison launch: %s", cudaGetErrorString(e));
@@ -626,6 +641,17 @@ int hpz_fwd_gather(hpz_ctx* c, int layer, void* full_out, void* stream) {
     e = launch_copy(sec, p.out + (int64_t)l * sec_bytes, sec_bytes, grid_for(c, sec_bytes / 4096 + 1, 4), c->side);
     if (e != cudaSuccess) return fail(c, HPZ_ECUDA, "stock copy launch: %s", cudaGetErrorString(e));
     c->launches += 1;
+    if (c->order == HPZ_ORDER_PAPER) {
+      // publish SEC_READY to the node (what the collective's rendezvous does for NCCL) and
+      // record the host-visible "MemcpyD2D finished" event
+      ReleaseList r{};
+      for (int q = 0; q < c->node_size; ++q) r.ptr[r.n++] = c->flag(nf + q, F_SEC_READY, layer, c->rank);
+      r.value = t1;
+      e = launch_release(r, c->side);
+      if (e != cudaSuccess) return fail(c, HPZ_ECUDA, "release launch: %s", cudaGetErrorString(e));
+      c->launches += 1;
+      HPZ_CUDA(c, cudaEventRecord(c->copy_ev[layer], c->side));
+    }
   }
   L.fwd_t = c->t;
   return HPZ_OK;
@@ -638,6 +664,8 @@ int hpz_bwd_gather(hpz_ctx* c, int layer, void* full_out, void* stream) {
   Layer& L = c->layers[layer];
   if (L.fwd_t != c->t) return fail(c, HPZ_ESTATE, "layer %d: backward gather without its forward gather at step %lld", layer, (long long)c->t);
   if (L.bwd_t == c->t) return fail(c, HPZ_ESTATE, "layer %d already backward-gathered at step %lld", layer, (long long)c->t);
+  if (c->order == HPZ_ORDER_PAPER)   // Alg. 1: "Repeat wait Until MemcpyD2D on L_k,second finishes" (host)
+    HPZ_CUDA(c, cudaEventSynchronize(c->copy_ev[layer]));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const uint32_t t1 = epoch(c->t + 1);
   const int nf = c->node_first();
@@ -659,7 +687,7 @@ int hpz_bwd_gather(hpz_ctx* c, int layer, void* full_out, void* stream) {
       p.src[q] = c->arena[nf + q] + L.off_secondary;
       // THE FIX: acquire SEC_READY of the owner for step t.
       // STOCK reproduces the bug: no wait.
-      p.src_flag[q] = c->order == HPZ_ORDER_FIXED ? c->flag(c->rank, F_SEC_READY, layer, nf + q) : nullptr;
+      p.src_flag[q] = c->order != HPZ_ORDER_STOCK ? c->flag(c->rank, F_SEC_READY, layer, nf + q) : nullptr;
     }
   }
   p.src_target = t1;

@@ -14,7 +14,7 @@ LIB_PATH = os.path.join(_HERE, "libhpz.so")
 
 HPZ_OK, HPZ_EINVAL, HPZ_ESTATE, HPZ_ECUDA, HPZ_ETIMEOUT, HPZ_ENOMEM = 0, -1, -2, -3, -4, -5
 HPZ_F32, HPZ_BF16 = 0, 1
-ORDER = {"fixed": 0, "stock": 1, "off": 2}
+ORDER = {"fixed": 0, "stock": 1, "off": 2, "paper": 3}
 VERIFY = {"none": 0, "fingerprint": 1, "exact": 2}
 BUF = {"primary": 0, "master": 1, "m": 2, "v": 3, "grad_shard": 4, "secondary": 5, "grad_slot": 6}
 IPC_HANDLE_BYTES = 64

@@ -39,7 +39,8 @@ class ParityRun:
         self.qgz, self.grad_dtype, self.qwz = qgz, grad_dtype, qwz
         self.w = EmulatedWorld(numels, world, node_size, dtype=dtype, align=align, n_grad_slots=n_grad_slots,
                                timeout_s=10.0, qgz=qgz, grad_dtype=grad_dtype, qwz=qwz)
-        self.o = O.HpzOracle(self.numels, world, node_size, align=align, param_dtype=dtype, order=order,
+        self.o = O.HpzOracle(self.numels, world, node_size, align=align, param_dtype=dtype,
+                             order="fixed" if order == "paper" else order,
                              stock_schedule=stock_schedule, grad_kind=grad_kind, qgz=qgz, grad_dtype=grad_dtype,
                              qwz=qwz)
         self.stream = torch.cuda.current_stream()

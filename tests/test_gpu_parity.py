@@ -41,7 +41,7 @@ def _check_step(run: ParityRun, rec, check_all=True):
         for r, rc in enumerate(run.w.ranks):
             st = run.o.state[i][r]
             # a2 secondary store == oracle's Eq. (1) slice
-            if run.o.order == "fixed":
+            if run.o.order == "fixed":   # (paper maps to fixed)
                 sec = bits_np(buffer_view(rc, i, "secondary", dtype), dtype)
                 assert np.array_equal(sec, O.param_bits(st.sec, dtype)), f"secondary layer {i} rank {r}"
             # a5 reduce-scatter bit-exact in the fixed order
@@ -142,6 +142,20 @@ def test_parity_qwz_fp32_params_and_qgz():
     try:
         for _ in range(2):
             _check_step(run, run.step())
+    finally:
+        run.close()
+
+
+@pytest.mark.parametrize("P,Pp", [(1, 1), (4, 2), (8, 4)])
+def test_parity_paper_order(P, Pp):
+    """ORDER_PAPER (the paper's own host-side wait after a separate MemcpyD2D) is correct:
+    same bits as the oracle's fixed ordering, 0 mismatches."""
+    run = ParityRun(NUMELS, P, Pp, order="paper", verify="exact", fused=True)
+    try:
+        for _ in range(3):
+            _check_step(run, run.step())
+        c = run.counters()
+        assert c["mismatches"] == 0 and c["timeouts"] == 0
     finally:
         run.close()
 

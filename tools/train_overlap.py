@@ -79,7 +79,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--max-ctas", type=int, default=32)
     ap.add_argument("--stock-delay-us", type=int, default=2000)
-    ap.add_argument("--configs", default="off:1,fixed:0,fixed:1,stock:1")
+    ap.add_argument("--configs", default="off:1,fixed:0,fixed:1,paper:1,stock:1")
     ap.add_argument("--init-scale", type=float, default=2.0 ** -5, help="uniform init bound (~sqrt(3/h))")
     ap.add_argument("--lr", type=float, default=1e-5)
     args = ap.parse_args()
