@@ -324,8 +324,8 @@ def main():
             bound, peak, unit = "nvlink", 770.0, "GB/s"
     achieved = alg / (share[dom] * 1e-3) / 1e9          # per-launch bytes / per-launch time, summed over L launches
     traffic = traffic_alg = traffic_src = None
-    tr = ncu_traffic().get(f"{args.model}_P{world}_{dom}")
-    if tr and not args.qgz:
+    tr = ncu_traffic().get(f"P{world}_{dom}")
+    if tr and not (args.qgz or args.qwz or args.grad_dtype != "f32"):
         # DRAM bytes of ONE captured launch (ncu --set full) next to that launch's algorithmic bytes
         traffic, traffic_alg, traffic_src = tr["dram_bytes_per_launch"], tr["launch_alg_bytes"], tr["source"]
     roofline = {"bound": bound, "kernel": dom, "achieved": round(achieved, 1), "peak": peak, "unit": unit,
