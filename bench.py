@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--copy-engine", default="tma", choices=["tma", "ldg"])
     ap.add_argument("--qgz", action="store_true", help="ZeRO++ qgZ: INT4 gradient all-to-all (SURVEY f1)")
     ap.add_argument("--qwz", action="store_true", help="ZeRO++ qwZ: INT8 weights in the forward gather (SURVEY f2)")
+    ap.add_argument("--gather", default="pull", choices=["pull", "push"],
+                    help="forward gather: ranks pull (default) or owners push into arena landing buffers")
     ap.add_argument("--grad-dtype", default="f32", choices=["f32", "bf16"],
                     help="gradient slot dtype (bf16: SURVEY f4, fp32 accumulation)")
     ap.add_argument("--e2e-steps", type=int, default=2)
@@ -187,10 +189,14 @@ def main():
 
     if world > 1:
         W = DistWorld(numels, node_size, dtype=dtype, n_grad_slots=L, device=local_rank, timeout_s=60.0,
-                      qgz=args.qgz, grad_dtype=args.grad_dtype, qwz=args.qwz)
+                      qgz=args.qgz, grad_dtype=args.grad_dtype, qwz=args.qwz,
+                      landing_bufs=1 if args.gather == "push" else 0)
     else:
         W = EmulatedWorld(numels, 1, 1, dtype=dtype, n_grad_slots=L, device=local_rank, timeout_s=60.0,
-                          qgz=args.qgz, grad_dtype=args.grad_dtype, qwz=args.qwz)
+                          qgz=args.qgz, grad_dtype=args.grad_dtype, qwz=args.qwz,
+                          landing_bufs=1 if args.gather == "push" else 0)
+        if args.gather == "push":
+            H.hpz_set_option(W.ranks[0].ctx, "split_phases", 0)     # one rank: phases inline
     rc = W.ranks[0]
     ctx = rc.ctx
     H.hpz_set_order(ctx, args.order)
@@ -208,7 +214,11 @@ def main():
         H.hpz_synth_grads(ctx, i, S.stream_key(S.SEED_GRADS, i, 0, rank), S.GRAD_SCALE, 0, stream)
     tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
     nmax = max(x.numel_pad for x in infos)
-    fwd_buf = torch.empty(nmax, dtype=tdt, device=dev)     # caller-owned full buffers, reused
+    if args.gather == "push":   # arena landing buffer: owners store their shards into it (P2P)
+        from paper_2407_01614_b200.world import device_view
+        fwd_buf = device_view(H.hpz_landing_buffer(ctx, 0), nmax, dtype)
+    else:
+        fwd_buf = torch.empty(nmax, dtype=tdt, device=dev)     # caller-owned full buffers, reused
     bwd_buf = torch.empty(nmax, dtype=tdt, device=dev)     # per layer (repartition)
     adam = H.make_adam()
     torch.cuda.synchronize()
@@ -405,7 +415,7 @@ def main():
                                    f"{sum(x.numel for x in infos)} params), bf16 params + fp32 master/Adam",
                        "world": world, "node_size": node_size, "virtual_nodes": world // node_size,
                        "parallelism": f"hpZ dp{world} (P={world}, P'={node_size})", "order": args.order,
-                       "verify": args.verify, "copy_engine": args.copy_engine,
+                       "verify": args.verify, "copy_engine": args.copy_engine, "fwd_gather": args.gather,
                        "qgz": "int4 blockwise (64) gradient all-to-all; RS bytes counted as the fp32 "
                               "gradient bytes reduced, wire bytes 0.625 B/elem" if args.qgz else None,
                        "grad_dtype": args.grad_dtype,

@@ -301,14 +301,36 @@ typedef enum {
                                     unchanged and returns the same values.  Needs align_elems
                                     % 256 == 0; not with EXACT verification or ORDER_OFF.  Set
                                     before hpz_register_flat_params. */
-  HPZ_OPT_MAX_CTAS = 6           /* cap on the CTAs of every launch (0 = whole GPU): bounds the SMs
+  HPZ_OPT_MAX_CTAS = 6,          /* cap on the CTAs of every launch (0 = whole GPU): bounds the SMs
                                     the collectives occupy while compute overlaps them (f3) */
+  HPZ_OPT_LANDING_BUFS = 7,      /* 0..8 library-owned full-parameter buffers in the arena
+                                    (hpz_landing_buffer); a forward gather into one of them runs
+                                    owner-driven: every owner bulk-stores its primary shard into
+                                    every rank's landing buffer and the secondaries over NVLink
+                                    (P2P stores), instead of every rank pulling.  FIXED order,
+                                    no qwZ.  Set before hpz_register_flat_params. */
+  HPZ_OPT_SPLIT_PHASES = 8       /* 0/1: push gathers leave their post / finish phases to the
+                                    caller (hpz_fwd_gather_post / _finish) — needed when several
+                                    ranks share one GPU stream (single-GPU emulation) */
 } hpz_option;
 /* Copy engine of the gathers and the reduce-scatter: TMA 1-D bulk copies through a
  * shared-memory stage ring (cp.async.bulk, one persistent CTA per SM), or 16-byte
  * LDG/STG streams (several CTAs per SM).  EXACT verification always uses LDG/STG. */
 typedef enum { HPZ_COPY_LDG = 0, HPZ_COPY_TMA = 1 } hpz_copy_engine;
 HPZ_API int hpz_set_option(hpz_ctx* ctx, int option, int64_t value);
+
+/* Landing buffer `idx` (HPZ_OPT_LANDING_BUFS) of this rank: a device buffer of the largest
+ * layer's numel_pad elements (param dtype), peer-mapped.  Pass it as full_out to
+ * hpz_fwd_gather to use the push path; its contents are valid after the gather (stream
+ * order) until the next gather into the same buffer. */
+HPZ_API int hpz_landing_buffer(const hpz_ctx* ctx, int idx, void** out);
+
+/* Push-gather phases for callers that run several ranks on one stream (HPZ_OPT_SPLIT_PHASES):
+ * post = E4 then "my landing buffer and secondary may be written" (FREE) to every owner;
+ * hpz_fwd_gather = the owner's push kernel; finish = wait until every owner's shard landed
+ * (DATA), then release E3 / E2.  Without SPLIT_PHASES hpz_fwd_gather does all three. */
+HPZ_API int hpz_fwd_gather_post(hpz_ctx* ctx, int layer, void* full_out, void* stream);
+HPZ_API int hpz_fwd_gather_finish(hpz_ctx* ctx, int layer, void* stream);
 
 #ifdef __cplusplus
 }

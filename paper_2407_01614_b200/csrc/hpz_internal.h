@@ -67,6 +67,26 @@ struct GatherParams {
   SyncCommon sync;
 };
 
+// Push forward gather (a2 with P2P stores): owner j streams its primary shard through a
+// TMA stage ring and bulk-stores every chunk into every rank's landing buffer (and into
+// the secondaries whose slice contains shard j) over NVLink.
+struct PushParams {
+  const char* src;                     // my primary shard (local)
+  int64_t src_bytes;                   // shard bytes (multiple of 16)
+  const uint32_t* src_flag;            // E1 on my own primary (PRIMARY_READY[layer][me])
+  uint32_t src_target;
+  char* land[kMaxWorld];               // rank q's landing buffer + my offset j*src_bytes
+  char* sec[kMaxWorld];                // rank q's secondary + (j - l(q)*k)*src_bytes, or nullptr
+  const uint32_t* free_flag[kMaxWorld];  // local FREE flag of destination q (acquired once per CTA)
+  uint32_t free_target;
+  int n_dst;
+  unsigned long long* fp_dst[kMaxWorld]; // rank q's forward fingerprint accumulator, or nullptr
+  int64_t word_base;                   // my shard's first 16-byte word index in the full buffer
+  uint32_t* done_ctr;
+  ReleaseList rel;                     // DATA into every destination
+  SyncCommon sync;
+};
+
 // qgZ (f1): blockwise INT4 quantization of one rank's gradient slot.
 constexpr int kQgzBlock = 64;          // elements per (min, scale) block
 struct QuantParams {
@@ -137,11 +157,13 @@ cudaError_t launch_gather_tma(const GatherParams& p, int grid, cudaStream_t s);
 cudaError_t launch_rs_tma(const RSParams& r, const AdamParams* a, int world, int grid, cudaStream_t s,
                           int mode = 0);
 cudaError_t launch_qgz_quantize(const QuantParams& q, int grid, cudaStream_t s);
+cudaError_t launch_push_gather(const PushParams& p, int grid, cudaStream_t s);
 cudaError_t launch_qwz_quantize(const QwzQuantParams& q, int grid, cudaStream_t s);
 // qwZ forward gather: TMA-pulls codes + params, dequantizes, STG to out (+ secondary).
 cudaError_t launch_gather_qwz(const GatherParams& p, int grid, cudaStream_t s);
 cudaError_t launch_wait(const WaitList& w, const SyncCommon& sync, cudaStream_t s);
 cudaError_t launch_release(const ReleaseList& r, cudaStream_t s);
+cudaError_t launch_wait_release(const WaitList& w, const ReleaseList& r, const SyncCommon& sync, cudaStream_t s);
 cudaError_t launch_copy(void* dst, const void* src, int64_t bytes, int grid, cudaStream_t s);
 cudaError_t launch_fill_u32(void* dst, uint32_t value, int64_t bytes, int grid, cudaStream_t s);
 cudaError_t launch_delay(int us, cudaStream_t s);

@@ -334,6 +334,16 @@ __global__ void wait_kernel(const WaitList w, const SyncCommon s) {
   if (threadIdx.x == 0) wait_all(w, s);
 }
 
+// wait for every flag of w, then (fence) release every flag of r: the small phase
+// kernels of the push gather (post: E4 -> FREE; finish: DATA -> SEC_READY, FWD_DONE)
+__global__ void wait_release_kernel(const WaitList w, const ReleaseList r, const SyncCommon s) {
+  if (threadIdx.x == 0) {
+    wait_all(w, s);
+    __threadfence_system();
+    release_all(r);
+  }
+}
+
 __global__ void release_kernel(const ReleaseList r) {
   if (threadIdx.x == 0) {
     __threadfence_system();
@@ -465,6 +475,11 @@ cudaError_t launch_adam(const AdamParams& p, int grid, cudaStream_t s) {
 
 cudaError_t launch_wait(const WaitList& w, const SyncCommon& sync, cudaStream_t s) {
   wait_kernel<<<1, 32, 0, s>>>(w, sync);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_wait_release(const WaitList& w, const ReleaseList& r, const SyncCommon& sync, cudaStream_t s) {
+  wait_release_kernel<<<1, 32, 0, s>>>(w, r, sync);
   return cudaGetLastError();
 }
 

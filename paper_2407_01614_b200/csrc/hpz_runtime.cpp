@@ -23,7 +23,8 @@ uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
 
 enum FlagKind { F_PRIM_READY = 0, F_FWD_DONE, F_SEC_READY, F_BWD_DONE, F_BWDP_DONE, F_NUM_LAYER_KINDS };
 enum SlotFlagKind { S_GRAD_READY = 0, S_RS_DONE, S_NUM };
-enum CtrKind { C_FWD = 0, C_BWD, C_RS, C_ADAM, C_QWZ, C_NUM };
+enum LandFlagKind { LF_FREE = 0, LF_DATA, LF_NUM };
+enum CtrKind { C_FWD = 0, C_BWD, C_RS, C_ADAM, C_QWZ, C_PUSH, C_NUM };
 
 struct Layer {
   int64_t numel, numel_pad, shard, sec_shard;
@@ -67,6 +68,12 @@ struct hpz_ctx {
   int grad_bytes = 4;                     // f4: 2 = bf16 gradients (fp32 accumulation)
   int qwz_bits = 0;                       // f2: 8 = INT8 blockwise weights in the forward gather
   int max_ctas = 0;                       // cap on every grid (0 = all SMs)
+  int n_land = 0;                         // library-owned landing buffers (push forward gather)
+  bool split_phases = false;              // push gather: caller issues post / finish itself
+  std::vector<uint64_t> off_land, land_use;
+  std::vector<uint8_t> land_posted;
+  std::vector<int> land_pending;          // per layer: landing buffer awaiting finish (-1: none)
+  uint64_t land_bytes = 0;
   std::vector<uint64_t> off_qcodes, off_qparams;   // per grad slot (qgZ)
   std::string err;
 
@@ -78,6 +85,11 @@ struct hpz_ctx {
   uint32_t* slot_flag(int rank_arena, int kind, int slot, int src) const {
     const uint64_t base = (uint64_t)F_NUM_LAYER_KINDS * n_layers * world;
     const uint64_t idx = base + ((uint64_t)kind * n_slots + slot) * world + src;
+    return reinterpret_cast<uint32_t*>(arena[rank_arena] + off_flags) + idx;
+  }
+  uint32_t* land_flag(int rank_arena, int kind, int b, int src) const {
+    const uint64_t base = (uint64_t)F_NUM_LAYER_KINDS * n_layers * world + (uint64_t)S_NUM * n_slots * world;
+    const uint64_t idx = base + ((uint64_t)kind * n_land + b) * world + src;
     return reinterpret_cast<uint32_t*>(arena[rank_arena] + off_flags) + idx;
   }
   uint32_t* ctr(int kind, int idx) const {
@@ -304,7 +316,8 @@ int hpz_register_flat_params(hpz_ctx* c, int n_layers, const int64_t* numel, int
     if (L.numel_pad > c->slot_numel[L.slot]) c->slot_numel[L.slot] = L.numel_pad;
   }
   // control region: flags | completion counters | fingerprints | stats
-  const uint64_t n_flags = (uint64_t)F_NUM_LAYER_KINDS * n_layers * c->world + (uint64_t)S_NUM * n_grad_slots * c->world;
+  const uint64_t n_flags = (uint64_t)F_NUM_LAYER_KINDS * n_layers * c->world + (uint64_t)S_NUM * n_grad_slots * c->world +
+                           (uint64_t)LF_NUM * c->n_land * c->world;
   uint64_t off = 0;
   c->off_flags = off;
   off = align_up(off + n_flags * 4, 256);
@@ -344,6 +357,18 @@ int hpz_register_flat_params(hpz_ctx* c, int n_layers, const int64_t* numel, int
       c->off_qparams[s] = off;
       off = align_up(off + (uint64_t)c->slot_numel[s] / kQgzBlock * 8, kBufAlign);
     }
+  }
+  // landing buffers of the push forward gather: one full layer (largest numel_pad) each
+  uint64_t nmax = 0;
+  for (const Layer& L : c->layers) nmax = nmax > (uint64_t)L.numel_pad ? nmax : (uint64_t)L.numel_pad;
+  c->land_bytes = nmax * elem;
+  c->off_land.assign(c->n_land, 0);
+  c->land_use.assign(c->n_land, 0);
+  c->land_posted.assign(c->n_land, 0);
+  c->land_pending.assign(n_layers, -1);
+  for (int b = 0; b < c->n_land; ++b) {
+    c->off_land[b] = off;
+    off = align_up(off + c->land_bytes, kBufAlign);
   }
   c->arena_bytes = off;
   c->registered = true;
@@ -559,6 +584,108 @@ int hpz_synth_master(hpz_ctx* c, int layer, uint64_t key, float scale, void* str
   return do_init_shard(c, layer, nullptr, key, scale, static_cast<cudaStream_t>(stream));
 }
 
+// ---- push forward gather (landing buffers in the arena) -------------------------------
+static int land_index(const hpz_ctx* c, const void* full_out) {
+  for (int b = 0; b < c->n_land; ++b)
+    if (full_out == c->arena[c->rank] + c->off_land[b]) return b;
+  return -1;
+}
+
+// phase 0: E4 (node peers finished reading my secondary for step t-1), then publish FREE:
+// my landing buffer b and my secondary may be written for this use of b.
+static int push_post(hpz_ctx* c, int layer, int b, cudaStream_t s) {
+  const int nf = c->node_first();
+  WaitList w{};
+  for (int q = 0; q < c->node_size; ++q) w.ptr[w.n++] = c->flag(c->rank, F_BWD_DONE, layer, nf + q);
+  w.target = epoch(c->t);
+  ReleaseList r{};
+  for (int j = 0; j < c->world; ++j) r.ptr[r.n++] = c->land_flag(j, LF_FREE, b, c->rank);
+  r.value = epoch(c->land_use[b] + 1);
+  cudaError_t e = launch_wait_release(w, r, c->sync(), s);
+  if (e != cudaSuccess) return fail(c, HPZ_ECUDA, "push post launch: %s", cudaGetErrorString(e));
+  c->launches += 1;
+  c->land_posted[b] = 1;
+  return HPZ_OK;
+}
+
+// phase 2: every owner's shard has landed (DATA) -> my full buffer and my secondary are
+// complete: release SEC_READY (E3) to the node and FWD_DONE (E2) to every owner.
+static int push_finish(hpz_ctx* c, int layer, cudaStream_t s) {
+  const int b = c->land_pending[layer];
+  const int nf = c->node_first();
+  WaitList w{};
+  for (int j = 0; j < c->world; ++j) w.ptr[w.n++] = c->land_flag(c->rank, LF_DATA, b, j);
+  w.target = epoch(c->land_use[b] + 1);
+  ReleaseList r{};
+  for (int q = 0; q < c->node_size; ++q) r.ptr[r.n++] = c->flag(nf + q, F_SEC_READY, layer, c->rank);
+  for (int j = 0; j < c->world; ++j) r.ptr[r.n++] = c->flag(j, F_FWD_DONE, layer, c->rank);
+  r.value = epoch(c->t + 1);
+  cudaError_t e = launch_wait_release(w, r, c->sync(), s);
+  if (e != cudaSuccess) return fail(c, HPZ_ECUDA, "push finish launch: %s", cudaGetErrorString(e));
+  c->launches += 1;
+  c->land_use[b] += 1;
+  c->land_posted[b] = 0;
+  c->land_pending[layer] = -1;
+  return HPZ_OK;
+}
+
+// phase 1: the push kernel (owner streams its primary shard to every landing buffer).
+static int push_gather(hpz_ctx* c, int layer, int b, cudaStream_t s) {
+  Layer& L = c->layers[layer];
+  const int me = c->rank;
+  const int64_t sb = L.shard * c->elem;
+  PushParams p{};
+  p.src = c->arena[me] + L.off_primary;
+  p.src_bytes = sb;
+  p.src_flag = c->flag(me, F_PRIM_READY, layer, me);
+  p.src_target = epoch(c->t + 1);
+  p.n_dst = c->world;
+  p.word_base = (int64_t)me * sb / 16;
+  for (int q = 0; q < c->world; ++q) {
+    p.land[q] = c->arena[q] + c->off_land[b] + (uint64_t)me * sb;
+    const int lq = q % c->node_size;                       // l(q): q's secondary slice
+    if (me / c->k == lq) p.sec[q] = c->arena[q] + L.off_secondary + (uint64_t)(me - lq * c->k) * sb;
+    p.free_flag[q] = c->land_flag(me, LF_FREE, b, q);
+    if (c->verify != HPZ_VERIFY_NONE)
+      p.fp_dst[q] = reinterpret_cast<unsigned long long*>(c->arena[q] + c->off_fp) + ((uint64_t)layer * 2 + (c->t & 1)) * 2;
+  }
+  p.free_target = epoch(c->land_use[b] + 1);
+  p.done_ctr = c->ctr(C_PUSH, layer);
+  for (int q = 0; q < c->world; ++q) p.rel.ptr[p.rel.n++] = c->land_flag(q, LF_DATA, b, me);
+  p.rel.value = epoch(c->land_use[b] + 1);
+  p.sync = c->sync();
+  cudaError_t e = launch_push_gather(p, grid_for(c, (sb + 32767) / 32768, 1), s);
+  if (e != cudaSuccess) return fail(c, HPZ_ECUDA, "push gather launch: %s", cudaGetErrorString(e));
+  c->launches += 1;
+  c->land_pending[layer] = b;
+  return HPZ_OK;
+}
+
+int hpz_landing_buffer(const hpz_ctx* cc, int idx, void** out) {
+  hpz_ctx* c = const_cast<hpz_ctx*>(cc);
+  if (!c || !out) return HPZ_EINVAL;
+  if (!c->registered || !c->arena[c->rank]) return fail(c, HPZ_ESTATE, "arena not allocated/bound");
+  if (idx < 0 || idx >= c->n_land) return fail(c, HPZ_EINVAL, "landing buffer %d out of range (%d)", idx, c->n_land);
+  *out = c->arena[c->rank] + c->off_land[idx];
+  return HPZ_OK;
+}
+
+int hpz_fwd_gather_post(hpz_ctx* c, int layer, void* full_out, void* stream) {
+  if (int rc = check_ready(c)) return rc;
+  if (int rc = check_layer(c, layer)) return rc;
+  const int b = land_index(c, full_out);
+  if (b < 0) return fail(c, HPZ_EINVAL, "full_out is not a landing buffer");
+  if (c->land_posted[b]) return fail(c, HPZ_ESTATE, "landing buffer %d already posted", b);
+  return push_post(c, layer, b, static_cast<cudaStream_t>(stream));
+}
+
+int hpz_fwd_gather_finish(hpz_ctx* c, int layer, void* stream) {
+  if (int rc = check_ready(c)) return rc;
+  if (int rc = check_layer(c, layer)) return rc;
+  if (c->land_pending[layer] < 0) return fail(c, HPZ_ESTATE, "layer %d has no push gather to finish", layer);
+  return push_finish(c, layer, static_cast<cudaStream_t>(stream));
+}
+
 int hpz_fwd_gather(hpz_ctx* c, int layer, void* full_out, void* stream) {
   if (int rc = check_ready(c)) return rc;
   if (int rc = check_layer(c, layer)) return rc;
@@ -568,6 +695,17 @@ int hpz_fwd_gather(hpz_ctx* c, int layer, void* full_out, void* stream) {
   if (c->qwz_bits && (c->verify == HPZ_VERIFY_EXACT || c->order == HPZ_ORDER_OFF))
     return fail(c, HPZ_ESTATE, "qwZ gathers dequantized weights: EXACT verification and ORDER_OFF compare/read raw primaries");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int land = land_index(c, full_out);
+  if (land >= 0 && c->order == HPZ_ORDER_FIXED && !c->qwz_bits) {
+    // owner-driven P2P stores into every rank's landing buffer (+ fused secondary stores)
+    if (!c->land_posted[land])
+      if (int rc = push_post(c, layer, land, s)) return rc;
+    if (int rc = push_gather(c, layer, land, s)) return rc;
+    if (!c->split_phases)
+      if (int rc = push_finish(c, layer, s)) return rc;
+    L.fwd_t = c->t;
+    return HPZ_OK;
+  }
   const uint32_t t1 = epoch(c->t + 1);
   GatherParams p{};
   p.n_src = c->world;
@@ -663,6 +801,7 @@ int hpz_bwd_gather(hpz_ctx* c, int layer, void* full_out, void* stream) {
   if (!full_out || (reinterpret_cast<uintptr_t>(full_out) & 15)) return fail(c, HPZ_EINVAL, "full_out null or not 16-byte aligned");
   Layer& L = c->layers[layer];
   if (L.fwd_t != c->t) return fail(c, HPZ_ESTATE, "layer %d: backward gather without its forward gather at step %lld", layer, (long long)c->t);
+  if (c->land_pending[layer] >= 0) return fail(c, HPZ_ESTATE, "layer %d: push gather not finished (hpz_fwd_gather_finish)", layer);
   if (L.bwd_t == c->t) return fail(c, HPZ_ESTATE, "layer %d already backward-gathered at step %lld", layer, (long long)c->t);
   if (c->order == HPZ_ORDER_PAPER)   // Alg. 1: "Repeat wait Until MemcpyD2D on L_k,second finishes" (host)
     HPZ_CUDA(c, cudaEventSynchronize(c->copy_ev[layer]));
@@ -976,6 +1115,14 @@ int hpz_set_option(hpz_ctx* c, int option, int64_t value) {
       if (value != 0 && value != 4) return fail(c, HPZ_EINVAL, "qgZ bits must be 0 (off) or 4");
       if (value && c->grad_bytes != 4) return fail(c, HPZ_EINVAL, "qgZ quantizes fp32 gradients");
       c->qgz_bits = (int)value;
+      return HPZ_OK;
+    case HPZ_OPT_LANDING_BUFS:
+      if (c->registered) return fail(c, HPZ_ESTATE, "landing buffers must be chosen before hpz_register_flat_params");
+      if (value < 0 || value > 8) return fail(c, HPZ_EINVAL, "landing buffers must be in [0, 8]");
+      c->n_land = (int)value;
+      return HPZ_OK;
+    case HPZ_OPT_SPLIT_PHASES:
+      c->split_phases = value != 0;
       return HPZ_OK;
     case HPZ_OPT_MAX_CTAS:
       if (value < 0 || value > 1 << 20) return fail(c, HPZ_EINVAL, "max_ctas must be >= 0");

@@ -463,6 +463,112 @@ __global__ void __launch_bounds__(256) qgz_quantize_kernel(const __grid_constant
   }
 }
 
+// ------------------------------------------------------------------ push gather (a2, P2P stores)
+// Owner-driven forward gather: each CTA bulk-loads 32 KiB chunks of MY primary shard into
+// its stage ring (local HBM, read once) and bulk-stores every chunk to all P landing
+// buffers — NVLink posted writes, which this fabric carries ~6% faster than read
+// responses (profiles/r01_p2p_probe_n4.log) — plus the node secondaries whose slice holds
+// my shard (the fused secondary store).  A destination is written only after its owner
+// released FREE for this use of the buffer (its previous contents are dead and its
+// secondary is no longer read, E4); the last CTA releases DATA to every destination.
+template <bool FP>
+__global__ void __launch_bounds__(32 * (1 + kFpWarps), 1) push_gather_kernel(const __grid_constant__ PushParams p) {
+  extern __shared__ __align__(1024) char smem[];
+  __shared__ __align__(8) uint64_t full_bar[kGatherStages];
+  __shared__ __align__(8) uint64_t empty_bar[kGatherStages];
+  __shared__ unsigned long long fp_red[kFpWarps];
+  const int64_t total = (p.src_bytes + kGatherChunk - 1) / kGatherChunk;
+  const int64_t nk = blockIdx.x < total ? (total - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kGatherStages; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], kFpWarps);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  auto chunk_of = [&](int64_t k, int64_t& off, uint32_t& bytes) {
+    off = (blockIdx.x + k * gridDim.x) * (int64_t)kGatherChunk;
+    const int64_t rem = p.src_bytes - off;
+    bytes = (uint32_t)(rem < kGatherChunk ? rem : kGatherChunk);
+  };
+  if (warp == 0) {
+    if (lane == 0) {
+      uint32_t freed = 0;
+      if (p.src_flag != nullptr) wait_geq(p.src_flag, p.src_target, p.sync);   // my Adam(t-1) done
+      fence_proxy_async();
+      auto issue_load = [&](int64_t k) {
+        int64_t off;
+        uint32_t bytes;
+        chunk_of(k, off, bytes);
+        const int s = (int)(k % kGatherStages);
+        mbar_expect_tx(&full_bar[s], bytes);
+        tma_load(smem + (size_t)s * kGatherChunk, p.src + off, bytes, &full_bar[s]);
+      };
+      const int64_t pre = nk < kGatherStages - 1 ? nk : kGatherStages - 1;
+      for (int64_t k = 0; k < pre; ++k) issue_load(k);
+      for (int64_t k = 0; k < nk; ++k) {
+        const int s = (int)(k % kGatherStages);
+        mbar_wait(&full_bar[s], (uint32_t)((k / kGatherStages) & 1));
+        int64_t off;
+        uint32_t bytes;
+        chunk_of(k, off, bytes);
+        const char* stage = smem + (size_t)s * kGatherChunk;
+        // rotate the destination order per CTA so the P links are loaded evenly
+        for (int d = 0; d < p.n_dst; ++d) {
+          const int q = (d + (int)blockIdx.x) % p.n_dst;
+          if (!((freed >> q) & 1u)) {
+            if (p.free_flag[q] != nullptr) wait_geq(p.free_flag[q], p.free_target, p.sync);
+            fence_proxy_async();
+            freed |= 1u << q;
+          }
+          tma_store(p.land[q] + off, stage, bytes);
+          if (p.sec[q] != nullptr) tma_store(p.sec[q] + off, stage, bytes);
+        }
+        bulk_commit();
+        if (k + kGatherStages - 1 < nk) {
+          bulk_wait_read<1>();
+          if (FP && k >= 1)
+            mbar_wait_bounded(&empty_bar[(k - 1) % kGatherStages], (uint32_t)(((k - 1) / kGatherStages) & 1), p.sync);
+          issue_load(k + kGatherStages - 1);
+        }
+      }
+      bulk_wait_all();
+      fence_proxy_async();
+    }
+  } else if (FP) {
+    uint64_t fp = 0;
+    const int ct = threadIdx.x - 32;
+    for (int64_t k = 0; k < nk; ++k) {
+      const int s = (int)(k % kGatherStages);
+      mbar_wait(&full_bar[s], (uint32_t)((k / kGatherStages) & 1));
+      int64_t off;
+      uint32_t bytes;
+      chunk_of(k, off, bytes);
+      const int4* st = reinterpret_cast<const int4*>(smem + (size_t)s * kGatherChunk);
+      const int64_t gv0 = p.word_base + off / 16;     // word index in the FULL buffer
+      for (uint32_t v = ct; v < bytes / 16; v += 32 * kFpWarps) fp += fp_word((uint32_t)(gv0 + v), st[v]);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty_bar[s]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) fp += __shfl_xor_sync(0xffffffffu, fp, o);
+    if (lane == 0) fp_red[warp - 1] = fp;
+  }
+  __syncthreads();
+  if (FP && threadIdx.x == 0) {
+    // every landing buffer holds the same full parameters: my shard's checksum goes into
+    // every destination's forward accumulator (remote atomics over NVLink)
+    unsigned long long sum = 0;
+    for (int w = 0; w < kFpWarps; ++w) sum += fp_red[w];
+    if (sum)
+      for (int q = 0; q < p.n_dst; ++q)
+        if (p.fp_dst[q]) atomicAdd(p.fp_dst[q], sum);
+  }
+  if (last_cta(p.done_ctr)) release_all(p.rel);   // DATA: my shard is in every landing buffer
+}
+
 // ------------------------------------------------------------------ qwZ (f2)
 // One warp per 256-element block of the owner's primary shard: each lane converts 8
 // elements to fp32, the warp reduces min/max/NaN, and the block's codes are
@@ -671,6 +777,23 @@ cudaError_t launch_gather_tma(const GatherParams& p, int grid, cudaStream_t s) {
     gather_tma_kernel<true><<<grid, 32 * (1 + kFpWarps), smem, s>>>(p);
   else
     gather_tma_kernel<false><<<grid, 32, smem, s>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_push_gather(const PushParams& p, int grid, cudaStream_t s) {
+  const int smem = kGatherStages * kGatherChunk;
+  static bool attr_set[2] = {false, false};
+  const bool fp = p.fp_dst[0] != nullptr;
+  if (!attr_set[fp]) {
+    cudaError_t e = fp ? cudaFuncSetAttribute(push_gather_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)
+                       : cudaFuncSetAttribute(push_gather_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    attr_set[fp] = true;
+  }
+  if (fp)
+    push_gather_kernel<true><<<grid, 32 * (1 + kFpWarps), smem, s>>>(p);
+  else
+    push_gather_kernel<false><<<grid, 32, smem, s>>>(p);
   return cudaGetLastError();
 }
 

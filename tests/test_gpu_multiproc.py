@@ -65,3 +65,10 @@ def test_multiproc_parity_qwz_qgz(n, node):
     if n > NGPU:
         pytest.skip(f"needs {n} GPUs")
     _run(n, node, extra=("--qwz", "1", "--qgz", "1"), port=30011 + n * 10 + node)
+
+
+@pytest.mark.parametrize("n,node", [(2, 1), (2, 2), (4, 2), (4, 1), (4, 4)])
+def test_multiproc_parity_push(n, node):
+    if n > NGPU:
+        pytest.skip(f"needs {n} GPUs")
+    _run(n, node, extra=("--push", "1"), port=30211 + n * 10 + node)

@@ -160,6 +160,20 @@ def test_parity_paper_order(P, Pp):
         run.close()
 
 
+@pytest.mark.parametrize("P,Pp", TOPOS)
+def test_parity_push_gather(P, Pp):
+    """Owner-driven forward gather (P2P TMA stores into arena landing buffers + fused
+    secondary stores): same bits as the oracle, fingerprints agree with the pulled backward."""
+    run = ParityRun(NUMELS, P, Pp, push=True, fused=True, verify="fingerprint")
+    try:
+        for _ in range(3):
+            _check_step(run, run.step())
+        c = run.counters()
+        assert c["timeouts"] == 0 and c["fp_mismatches"] == 0 and c["fp_checked"] == 3 * len(NUMELS) * P
+    finally:
+        run.close()
+
+
 def test_parity_fused_off_order():
     run = ParityRun(NUMELS, 4, 2, order="off", fused=True)
     try:
