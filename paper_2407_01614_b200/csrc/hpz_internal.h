@@ -164,6 +164,8 @@ cudaError_t launch_gather_qwz(const GatherParams& p, int grid, cudaStream_t s);
 cudaError_t launch_wait(const WaitList& w, const SyncCommon& sync, cudaStream_t s);
 cudaError_t launch_release(const ReleaseList& r, cudaStream_t s);
 cudaError_t launch_wait_release(const WaitList& w, const ReleaseList& r, const SyncCommon& sync, cudaStream_t s);
+cudaError_t launch_wait_copy_release(void* dst, const void* src, int64_t bytes, const WaitList& w, uint32_t* done_ctr,
+                                     const ReleaseList& r, const SyncCommon& sync, int grid, cudaStream_t s);
 cudaError_t launch_copy(void* dst, const void* src, int64_t bytes, int grid, cudaStream_t s);
 cudaError_t launch_fill_u32(void* dst, uint32_t value, int64_t bytes, int grid, cudaStream_t s);
 cudaError_t launch_delay(int us, cudaStream_t s);

@@ -24,7 +24,7 @@ uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
 enum FlagKind { F_PRIM_READY = 0, F_FWD_DONE, F_SEC_READY, F_BWD_DONE, F_BWDP_DONE, F_NUM_LAYER_KINDS };
 enum SlotFlagKind { S_GRAD_READY = 0, S_RS_DONE, S_NUM };
 enum LandFlagKind { LF_FREE = 0, LF_DATA, LF_NUM };
-enum CtrKind { C_FWD = 0, C_BWD, C_RS, C_ADAM, C_QWZ, C_PUSH, C_NUM };
+enum CtrKind { C_FWD = 0, C_BWD, C_RS, C_ADAM, C_QWZ, C_PUSH, C_FIN, C_NUM };
 
 struct Layer {
   int64_t numel, numel_pad, shard, sec_shard;
@@ -608,11 +608,14 @@ static int push_post(hpz_ctx* c, int layer, int b, cudaStream_t s) {
   return HPZ_OK;
 }
 
-// phase 2: every owner's shard has landed (DATA) -> my full buffer and my secondary are
-// complete: release SEC_READY (E3) to the node and FWD_DONE (E2) to every owner.
+// phase 2: every owner's shard has landed (DATA) -> my full buffer is complete; my
+// secondary slice l(r) is copied from it locally (pushing it from the owners would cost
+// NVLink bytes the pull design gets for free), then SEC_READY (E3) to the node and
+// FWD_DONE (E2) to every owner.
 static int push_finish(hpz_ctx* c, int layer, cudaStream_t s) {
   const int b = c->land_pending[layer];
   const int nf = c->node_first();
+  const Layer& L = c->layers[layer];
   WaitList w{};
   for (int j = 0; j < c->world; ++j) w.ptr[w.n++] = c->land_flag(c->rank, LF_DATA, b, j);
   w.target = epoch(c->land_use[b] + 1);
@@ -620,7 +623,11 @@ static int push_finish(hpz_ctx* c, int layer, cudaStream_t s) {
   for (int q = 0; q < c->node_size; ++q) r.ptr[r.n++] = c->flag(nf + q, F_SEC_READY, layer, c->rank);
   for (int j = 0; j < c->world; ++j) r.ptr[r.n++] = c->flag(j, F_FWD_DONE, layer, c->rank);
   r.value = epoch(c->t + 1);
-  cudaError_t e = launch_wait_release(w, r, c->sync(), s);
+  const int64_t sec_bytes = L.sec_shard * c->elem;
+  char* land = c->arena[c->rank] + c->off_land[b];
+  cudaError_t e = launch_wait_copy_release(c->arena[c->rank] + L.off_secondary, land + (int64_t)c->local() * sec_bytes,
+                                           sec_bytes, w, c->ctr(C_FIN, layer), r, c->sync(),
+                                           grid_for(c, (sec_bytes / 16 + 255) / 256, 4), s);
   if (e != cudaSuccess) return fail(c, HPZ_ECUDA, "push finish launch: %s", cudaGetErrorString(e));
   c->launches += 1;
   c->land_use[b] += 1;
@@ -643,8 +650,7 @@ static int push_gather(hpz_ctx* c, int layer, int b, cudaStream_t s) {
   p.word_base = (int64_t)me * sb / 16;
   for (int q = 0; q < c->world; ++q) {
     p.land[q] = c->arena[q] + c->off_land[b] + (uint64_t)me * sb;
-    const int lq = q % c->node_size;                       // l(q): q's secondary slice
-    if (me / c->k == lq) p.sec[q] = c->arena[q] + L.off_secondary + (uint64_t)(me - lq * c->k) * sb;
+    p.sec[q] = nullptr;   // secondaries are filled locally by each receiver (push_finish)
     p.free_flag[q] = c->land_flag(me, LF_FREE, b, q);
     if (c->verify != HPZ_VERIFY_NONE)
       p.fp_dst[q] = reinterpret_cast<unsigned long long*>(c->arena[q] + c->off_fp) + ((uint64_t)layer * 2 + (c->t & 1)) * 2;
