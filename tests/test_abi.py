@@ -146,3 +146,18 @@ def test_options_host_only(H):
         H.hpz_finalize(ctx)
     # qgZ adds int4 codes (N̂/2 B) + (min, scale) per 64 elements (N̂/8 B) per gradient slot
     assert a_q - a >= (1_001_472 + 2048) * 0.625 - 4 * 4096
+
+
+def test_c_client_compiles_and_links(H, tmp_path):
+    """include/hpz.h is plain C: a C99 program includes it, links libhpz.so and checks a layout."""
+    import subprocess
+    exe = tmp_path / "layout_check"
+    src = os.path.join(ROOT, "tests", "c_abi", "layout_check.c")
+    libdir = os.path.dirname(H.LIB_PATH)
+    r = subprocess.run(["gcc", "-std=c99", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"), src,
+                        "-L", libdir, "-lhpz", f"-Wl,-rpath,{libdir}", "-o", str(exe)],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    out = subprocess.run([str(exe)], capture_output=True, text=True)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "numel_pad=207071232" in out.stdout
