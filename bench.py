@@ -54,6 +54,10 @@ def parse():
                     help="forward gather: ranks pull (default) or owners push into arena landing buffers")
     ap.add_argument("--grad-dtype", default="f32", choices=["f32", "bf16"],
                     help="gradient slot dtype (bf16: SURVEY f4, fp32 accumulation)")
+    ap.add_argument("--grad-slots", type=int, default=0,
+                    help="gradient slots (0 = one per layer, resident).  Fewer slots (large models) "
+                         "regenerate each layer's gradient on the device inside the step (timed, "
+                         "reported as grad_synth)")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -188,11 +192,12 @@ def main():
     L = len(numels)
 
     if world > 1:
-        W = DistWorld(numels, node_size, dtype=dtype, n_grad_slots=L, device=local_rank, timeout_s=60.0,
+    n_slots = args.grad_slots if 0 < args.grad_slots < L else L
+        W = DistWorld(numels, node_size, dtype=dtype, n_grad_slots=n_slots, device=local_rank, timeout_s=60.0,
                       qgz=args.qgz, grad_dtype=args.grad_dtype, qwz=args.qwz,
                       landing_bufs=1 if args.gather == "push" else 0)
     else:
-        W = EmulatedWorld(numels, 1, 1, dtype=dtype, n_grad_slots=L, device=local_rank, timeout_s=60.0,
+        W = EmulatedWorld(numels, 1, 1, dtype=dtype, n_grad_slots=n_slots, device=local_rank, timeout_s=60.0,
                           qgz=args.qgz, grad_dtype=args.grad_dtype, qwz=args.qwz,
                           landing_bufs=1 if args.gather == "push" else 0)
         if args.gather == "push":
@@ -211,7 +216,8 @@ def main():
     # resident inputs: initial params (device generator) and this rank's gradients
     for i in range(L):
         H.hpz_synth_master(ctx, i, S.stream_key(S.SEED_PARAMS, i, 0, 0), S.PARAM_SCALE, stream)
-        H.hpz_synth_grads(ctx, i, S.stream_key(S.SEED_GRADS, i, 0, rank), S.GRAD_SCALE, 0, stream)
+        if n_slots == L:
+            H.hpz_synth_grads(ctx, i, S.stream_key(S.SEED_GRADS, i, 0, rank), S.GRAD_SCALE, 0, stream)
     tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
     nmax = max(x.numel_pad for x in infos)
     if args.gather == "push":   # arena landing buffer: owners store their shards into it (P2P)
@@ -257,6 +263,10 @@ def main():
             rec("bwd1")
             if grads_from is not None:
                 stream.wait_event(up[i])
+            elif n_slots < L:    # shared slots: this layer's gradient is produced in the step
+                rec("g0")
+                H.hpz_synth_grads(ctx, i, S.stream_key(S.SEED_GRADS, i, 0, rank), S.GRAD_SCALE, 0, stream)
+                rec("g1")
             if args.qgz:
                 rec("q0")
                 H.hpz_grads_ready(ctx, i, stream)      # qgZ: INT4-quantize my slot, publish E5
@@ -281,7 +291,7 @@ def main():
     barrier()
     if rank == 0:
         clocks.start()
-    evs = {k: [] for k in ("fwd0", "fwd1", "bwd0", "bwd1", "rs0", "rs1", "adam0", "adam1", "q0", "q1")}
+    evs = {k: [] for k in ("fwd0", "fwd1", "bwd0", "bwd1", "rs0", "rs1", "adam0", "adam1", "q0", "q1", "g0", "g1")}
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
     t_start.record(stream)
@@ -296,7 +306,7 @@ def main():
     K = args.steps
     step_ms = t_start.elapsed_time(t_end) / K
     tot = {k: sum(a.elapsed_time(b) for a, b in zip(evs[k + "0"], evs[k + "1"])) / K
-           for k in ("fwd", "bwd", "rs", "adam", "q")}
+           for k in ("fwd", "bwd", "rs", "adam", "q", "g")}
     # bytes per rank per step (algbw: AG output bytes, RS input bytes)
     ag_bytes = sum(x.numel_pad for x in infos) * e
     rs_bytes = sum(x.numel_pad for x in infos) * 4
@@ -311,10 +321,10 @@ def main():
     adam_bytes = sum(x.shard for x in infos) * (30 if dtype == "bf16" else 32)
 
     vals = max_over_ranks([step_ms, tot["fwd"], tot["bwd"], tot["rs"], tot["adam"],
-                           tot["fwd"] + tot["bwd"] + tot["rs"] + tot["q"], tot["q"]], device=dev)
+                           tot["fwd"] + tot["bwd"] + tot["rs"] + tot["q"], tot["q"], tot["g"]], device=dev)
     stats = sum_over_ranks([cnt["fp_mismatches"], cnt["mismatches"], cnt["nan_reads"], cnt["timeouts"],
                             cnt["fp_checked"], launches], device=dev)
-    step_ms, fwd_ms, bwd_ms, rs_ms, adam_ms, coll_ms, q_ms = vals
+    step_ms, fwd_ms, bwd_ms, rs_ms, adam_ms, coll_ms, q_ms, g_ms = vals
     # whole-job throughput of the step: the collectives' algorithmic bytes of all ranks per
     # step / the max-over-ranks time of the whole step (incl. the optimizer)
     value = world * coll_bytes / (step_ms * 1e-3) / 1e9
@@ -418,7 +428,7 @@ def main():
                        "verify": args.verify, "copy_engine": args.copy_engine, "fwd_gather": args.gather,
                        "qgz": "int4 blockwise (64) gradient all-to-all; RS bytes counted as the fp32 "
                               "gradient bytes reduced, wire bytes 0.625 B/elem" if args.qgz else None,
-                       "grad_dtype": args.grad_dtype,
+                       "grad_dtype": args.grad_dtype, "grad_slots": n_slots,
                        "qwz": "int8 blockwise (256) weights in the forward gather; AG bytes counted as the "
                               "bf16 parameter bytes delivered" if args.qwz else None,
                        "l2": "no flush: per-step working set >> 126 MB L2 (every layer buffer is "
@@ -431,7 +441,7 @@ def main():
                                        "layers_checked": int(stats[4])},
             "breakdown_ms_per_step": {"fwd_gather": round(fwd_ms, 3), "bwd_gather": round(bwd_ms, 3),
                                       rs_name: round(rs_ms, 3), "adam": round(adam_ms, 3),
-                                      "qgz_quantize": round(q_ms, 3),
+                                      "qgz_quantize": round(q_ms, 3), "grad_synth": round(g_ms, 3),
                                       "collectives": round(coll_ms, 3)},
             "fused_rs_adam": fused,
             "nvlink_ingress_GBps_per_gpu": round(ingress / (step_ms * 1e-3) / 1e9, 2) if world > 1 else None,
