@@ -191,8 +191,8 @@ def main():
     e = 2 if dtype == "bf16" else 4
     L = len(numels)
 
-    if world > 1:
     n_slots = args.grad_slots if 0 < args.grad_slots < L else L
+    if world > 1:
         W = DistWorld(numels, node_size, dtype=dtype, n_grad_slots=n_slots, device=local_rank, timeout_s=60.0,
                       qgz=args.qgz, grad_dtype=args.grad_dtype, qwz=args.qwz,
                       landing_bufs=1 if args.gather == "push" else 0)
