@@ -17,13 +17,11 @@ ranks a process owns.
 """
 from __future__ import annotations
 
-import os
 from dataclasses import dataclass, field
 
 import torch
 
 from . import hpz as H
-from .shapes import PARAM_DTYPE
 
 DTYPES = {"bf16": (H.HPZ_BF16, torch.bfloat16, 2), "f32": (H.HPZ_F32, torch.float32, 4)}
 

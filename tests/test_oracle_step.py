@@ -4,7 +4,6 @@ import numpy as np
 import pytest
 
 from oracle import hpz_oracle as O
-from synth import inputs as S
 
 SMALL = [3000, 1234, 777]
 
