@@ -214,6 +214,14 @@ HPZ_API int hpz_load_master(hpz_ctx* ctx, int layer, const float* full_fp32, voi
  * for e < numel, 0 in padding); key is the 64-bit stream key computed by the caller. */
 HPZ_API int hpz_synth_master(hpz_ctx* ctx, int layer, uint64_t key, float scale, void* stream);
 
+/* Resume from a checkpoint: this rank's master / Adam m / Adam v shards of
+ * `layer` (fp32, `shard` elements each, host or device pointers, as read through
+ * hpz_buffer) and the number of Adam steps already taken (bias corrections continue from
+ * adam_steps_done + 1).  Refreshes the primary (RNE) and releases E1 like hpz_load_master;
+ * must precede the layer's first gather on this context. */
+HPZ_API int hpz_load_state(hpz_ctx* ctx, int layer, const float* master, const float* m, const float* v,
+                           int64_t adam_steps_done, void* stream);
+
 /* ---- hot path ------------------------------------------------------------------------ */
 
 /* Forward gather of layer `layer` at the current step t (Alg. 1 PAPER.md:101,

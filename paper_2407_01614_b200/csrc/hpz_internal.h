@@ -167,6 +167,7 @@ cudaError_t launch_wait_release(const WaitList& w, const ReleaseList& r, const S
 cudaError_t launch_wait_copy_release(void* dst, const void* src, int64_t bytes, const WaitList& w, uint32_t* done_ctr,
                                      const ReleaseList& r, const SyncCommon& sync, int grid, cudaStream_t s);
 cudaError_t launch_copy(void* dst, const void* src, int64_t bytes, int grid, cudaStream_t s);
+cudaError_t launch_refresh_primary(const float* master, void* prim, int prim_bf16, int64_t n, int grid, cudaStream_t s);
 cudaError_t launch_fill_u32(void* dst, uint32_t value, int64_t bytes, int grid, cudaStream_t s);
 cudaError_t launch_delay(int us, cudaStream_t s);
 // Seeded generator; e0 = global element index of dst[0]; values for

@@ -439,7 +439,23 @@ __global__ void __launch_bounds__(kThreads) init_shard_kernel(float* master, flo
   }
 }
 
+// primary = RNE(master) (resume from a checkpoint)
+__global__ void __launch_bounds__(kThreads) refresh_primary_kernel(const float* master, void* prim, int prim_bf16,
+                                                                   int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n; i += (int64_t)gridDim.x * kThreads) {
+    if (prim_bf16)
+      reinterpret_cast<__nv_bfloat16*>(prim)[i] = __float2bfloat16_rn(master[i]);
+    else
+      reinterpret_cast<float*>(prim)[i] = master[i];
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_refresh_primary(const float* master, void* prim, int prim_bf16, int64_t n, int grid, cudaStream_t s) {
+  refresh_primary_kernel<<<grid, kThreads, 0, s>>>(master, prim, prim_bf16, n);
+  return cudaGetLastError();
+}
 
 // ------------------------------------------------------------------ launchers
 cudaError_t launch_gather(const GatherParams& p, int grid, cudaStream_t s) {

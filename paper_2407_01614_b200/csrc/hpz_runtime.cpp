@@ -51,7 +51,8 @@ struct hpz_ctx {
   bool registered = false, bound = false, owns_arena = false;
   char* arena[kMaxWorld] = {};            // mapped arena base of every rank
   bool opened[kMaxWorld] = {};            // arena[j] was opened via IPC here
-  int64_t t = 0;                          // current step
+  int64_t t = 0;                          // current step (flag epochs)
+  int64_t adam_base = 0;                  // Adam steps done before this context (resume)
   int order = HPZ_ORDER_FIXED, stock_delay_us = 0, stock_poison = 0;
   int verify = HPZ_VERIFY_NONE;
   double timeout_s = 20.0;
@@ -578,6 +579,34 @@ int hpz_load_master(hpz_ctx* c, int layer, const float* full, void* stream) {
   return do_init_shard(c, layer, full, 0, 0.f, static_cast<cudaStream_t>(stream));
 }
 
+int hpz_load_state(hpz_ctx* c, int layer, const float* master, const float* m, const float* v,
+                   int64_t adam_steps_done, void* stream) {
+  if (int rc = check_ready(c)) return rc;
+  if (int rc = check_layer(c, layer)) return rc;
+  if (!master || !m || !v || adam_steps_done < 0) return fail(c, HPZ_EINVAL, "bad checkpoint arguments");
+  Layer& L = c->layers[layer];
+  if (L.fwd_t >= 0) return fail(c, HPZ_ESTATE, "layer %d already in use; load state before the first gather", layer);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  char* a = c->arena[c->rank];
+  const size_t bytes = (size_t)L.shard * 4;
+  HPZ_CUDA(c, cudaMemcpyAsync(a + L.off_master, master, bytes, cudaMemcpyDefault, s));
+  HPZ_CUDA(c, cudaMemcpyAsync(a + L.off_m, m, bytes, cudaMemcpyDefault, s));
+  HPZ_CUDA(c, cudaMemcpyAsync(a + L.off_v, v, bytes, cudaMemcpyDefault, s));
+  cudaError_t e = launch_refresh_primary(reinterpret_cast<const float*>(a + L.off_master), a + L.off_primary,
+                                         c->dtype == HPZ_BF16, L.shard, grid_for(c, (L.shard + 255) / 256, 8), s);
+  if (e != cudaSuccess) return fail(c, HPZ_ECUDA, "refresh launch: %s", cudaGetErrorString(e));
+  c->launches += 1;
+  c->adam_base = adam_steps_done;
+  if (c->qwz_bits) return qwz_quantize(c, layer, epoch(c->t + 1), s);
+  ReleaseList r{};
+  for (int j = 0; j < c->world; ++j) r.ptr[r.n++] = c->flag(j, F_PRIM_READY, layer, c->rank);
+  r.value = epoch(c->t + 1);
+  e = launch_release(r, s);
+  if (e != cudaSuccess) return fail(c, HPZ_ECUDA, "release launch: %s", cudaGetErrorString(e));
+  c->launches += 1;
+  return HPZ_OK;
+}
+
 int hpz_synth_master(hpz_ctx* c, int layer, uint64_t key, float scale, void* stream) {
   if (int rc = check_ready(c)) return rc;
   if (int rc = check_layer(c, layer)) return rc;
@@ -1010,7 +1039,7 @@ static int check_adam(hpz_ctx* c, const hpz_adam* a) {
 
 static void build_adam(hpz_ctx* c, int layer, const hpz_adam* a, AdamParams& p) {
   Layer& L = c->layers[layer];
-  const int64_t tad = a->step > 0 ? a->step : c->t + 1;    // 1-based Adam count (R24)
+  const int64_t tad = a->step > 0 ? a->step : c->adam_base + c->t + 1;    // 1-based Adam count (R24)
   const double bc1 = 1.0 - std::pow(a->beta1, (double)tad);
   const double bc2 = 1.0 - std::pow(a->beta2, (double)tad);
   char* ar = c->arena[c->rank];

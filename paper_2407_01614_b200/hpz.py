@@ -28,7 +28,7 @@ EXPORTED = [
     "hpz_set_timeout", "hpz_load_master", "hpz_synth_master", "hpz_fwd_gather", "hpz_bwd_gather",
     "hpz_grad_buffer", "hpz_grad_upload", "hpz_synth_grads", "hpz_grads_ready",
     "hpz_reduce_scatter", "hpz_step", "hpz_reduce_scatter_adam", "hpz_set_option",
-    "hpz_landing_buffer", "hpz_fwd_gather_post", "hpz_fwd_gather_finish",
+    "hpz_landing_buffer", "hpz_fwd_gather_post", "hpz_fwd_gather_finish", "hpz_load_state",
 ]
 OPT = {"store_grad_shard": 0, "ctas_per_sm": 1, "copy_engine": 2, "qgz": 3, "grad_dtype": 4, "qwz": 5, "max_ctas": 6, "landing_bufs": 7, "split_phases": 8}
 COPY = {"ldg": 0, "tma": 1}
@@ -95,6 +95,7 @@ def _load() -> ctypes.CDLL:
         "hpz_landing_buffer": (c_int, [P, c_int, POINTER(c_void_p)]),
         "hpz_fwd_gather_post": (c_int, [P, c_int, c_void_p, c_void_p]),
         "hpz_fwd_gather_finish": (c_int, [P, c_int, c_void_p]),
+        "hpz_load_state": (c_int, [P, c_int, c_void_p, c_void_p, c_void_p, c_int64, c_void_p]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -280,3 +281,8 @@ def hpz_fwd_gather_post(ctx, layer: int, full_out_ptr: int, stream=None):
 
 def hpz_fwd_gather_finish(ctx, layer: int, stream=None):
     _check(ctx, "hpz_fwd_gather_finish", LIB.hpz_fwd_gather_finish(ctx, layer, _stream(stream)))
+
+
+def hpz_load_state(ctx, layer: int, master_ptr: int, m_ptr: int, v_ptr: int, adam_steps_done: int, stream=None):
+    _check(ctx, "hpz_load_state", LIB.hpz_load_state(ctx, layer, c_void_p(master_ptr), c_void_p(m_ptr),
+                                                     c_void_p(v_ptr), c_int64(adam_steps_done), _stream(stream)))

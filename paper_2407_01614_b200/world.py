@@ -226,3 +226,27 @@ def buffer_view(rc: RankCtx, layer: int, kind: str, dtype: str) -> torch.Tensor:
     if kind in ("primary", "secondary"):
         return device_view(ptr, n, "u32")
     return device_view(ptr, n, "f32")
+
+
+def save_checkpoint(rc: RankCtx, adam_steps_done: int) -> dict:
+    """This rank's optimizer state (SURVEY §5 checkpoint/resume): fp32 master, Adam m and v
+    shards of every layer (CPU tensors) + the Adam step count."""
+    torch.cuda.synchronize()
+    state = {"rank": rc.rank, "world": rc.world, "node_size": rc.node_size, "numels": list(rc.numels),
+             "adam_steps_done": int(adam_steps_done), "layers": []}
+    for i in range(len(rc.numels)):
+        state["layers"].append({k: buffer_view(rc, i, k, "f32").cpu().clone() for k in ("master", "m", "v")})
+    return state
+
+
+def load_checkpoint(rc: RankCtx, state: dict, stream=None):
+    """Restore a save_checkpoint() state into a fresh context of the same layout/rank."""
+    if state["rank"] != rc.rank or state["world"] != rc.world or list(state["numels"]) != list(rc.numels):
+        raise ValueError("checkpoint was written for a different rank / world / model")
+    keep = []
+    for i, L in enumerate(state["layers"]):
+        ts = [L[k].contiguous().cuda() for k in ("master", "m", "v")]
+        keep += ts
+        H.hpz_load_state(rc.ctx, i, ts[0].data_ptr(), ts[1].data_ptr(), ts[2].data_ptr(),
+                         state["adam_steps_done"], stream)
+    torch.cuda.synchronize()

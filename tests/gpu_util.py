@@ -29,7 +29,7 @@ class ParityRun:
     def __init__(self, numels, world, node_size, dtype="bf16", align=256, order="fixed",
                  verify="exact", grad_kind="uniform", n_grad_slots=None, stock_schedule="program",
                  fused=False, store_grad_shard=True, copy_engine="tma", qgz=False, grad_dtype="f32",
-                 qwz=False, push=False):
+                 qwz=False, push=False, load_initial=True):
         from paper_2407_01614_b200 import hpz as H
         from paper_2407_01614_b200.world import EmulatedWorld
         self.H = H
@@ -60,7 +60,7 @@ class ParityRun:
             self.fwd = [[torch.zeros(rc.infos[i].numel_pad, dtype=tdt, device="cuda") for i in range(L)]
                         for rc in self.w.ranks]
         self.bwd = [[torch.zeros(rc.infos[i].numel_pad, dtype=tdt, device="cuda") for i in range(L)] for rc in self.w.ranks]
-        for i, n in enumerate(self.numels):
+        for i, n in enumerate(self.numels if load_initial else []):
             w0 = torch.from_numpy(S.layer_params(i, n)).cuda()
             for rc in self.w.ranks:
                 H.hpz_load_master(rc.ctx, i, w0.data_ptr(), self.stream)
@@ -75,14 +75,14 @@ class ParityRun:
         self.H.hpz_grad_upload(rc.ctx, i, g.data_ptr(), lay.numel, self.stream)
         self._keep.append(g)
 
-    def step(self):
+    def step(self, run_oracle=True):
         from paper_2407_01614_b200.world import run_step
         self._keep = []
         run_step(self.w.ranks, [lambda i, r=r: self.fwd[r][i].data_ptr() for r in range(self.P)],
                  [lambda i, r=r: self.bwd[r][i].data_ptr() for r in range(self.P)], self.adam,
                  stream=self.stream, grad_fn=self.grad_fn, emulated=True, fused=self.fused, push=self.push)
         torch.cuda.synchronize()
-        rec = self.o.step()
+        rec = self.o.step() if run_oracle else None
         self.t += 1
         return rec
 

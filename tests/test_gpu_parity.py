@@ -391,3 +391,40 @@ def test_qgz_quantizer_ties_and_edges(P):
             assert np.array_equal(got.view(np.uint32), ref.view(np.uint32))
     finally:
         w.close()
+
+
+def test_checkpoint_resume_is_bit_identical():
+    """Checkpoint/resume: 2 steps, save (master, m, v, Adam count), fresh world,
+    load, 1 step == 3 uninterrupted steps, bit for bit (and == the oracle)."""
+    from paper_2407_01614_b200.world import load_checkpoint, save_checkpoint
+    ref = ParityRun(NUMELS, 4, 2, fused=True, verify="fingerprint")
+    try:
+        for _ in range(3):
+            rec = ref.step()
+        _check_step(ref, rec)
+        want = [[buffer_view_f32(rc, i) for i in range(len(NUMELS))] for rc in ref.w.ranks]
+    finally:
+        ref.close()
+    a = ParityRun(NUMELS, 4, 2, fused=True, verify="fingerprint")
+    try:
+        for _ in range(2):
+            a.step()
+        ckpts = [save_checkpoint(rc, 2) for rc in a.w.ranks]
+    finally:
+        a.close()
+    b = ParityRun(NUMELS, 4, 2, fused=True, verify="fingerprint", load_initial=False)
+    try:
+        for rc, ck in zip(b.w.ranks, ckpts):
+            load_checkpoint(rc, ck, b.stream)
+        b.t = 2                       # the gradient generator continues at step 2
+        b.step(run_oracle=False)
+        for r, rc in enumerate(b.w.ranks):
+            for i in range(len(NUMELS)):
+                assert np.array_equal(buffer_view_f32(rc, i), want[r][i])
+    finally:
+        b.close()
+
+
+def buffer_view_f32(rc, i):
+    from paper_2407_01614_b200.world import buffer_view
+    return buffer_view(rc, i, "master", "f32").cpu().numpy().view(np.uint32).copy()
