@@ -18,6 +18,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <utility>
+
 #include "hpz_device.cuh"
 #include "hpz_internal.h"
 
@@ -101,6 +103,22 @@ __device__ __forceinline__ void bulk_wait_read() {
 }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+// Programmatic dependent launch (sm_90+): a kernel launched with programmatic stream
+// serialization may start while the previous kernel of the stream drains; it must
+// `griddep_wait` before touching memory that kernel produced.  Everything our kernels read
+// from a previous kernel is additionally ordered by release/acquire flags, except the
+// caller-written gradient slots (the RS waits first thing) and buffer reuse (the gather
+// waits before its first store).
+__device__ __forceinline__ void griddep_wait() {
+#ifndef HPZ_NO_PDL
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
+__device__ __forceinline__ void griddep_launch_dependents() {
+#ifndef HPZ_NO_PDL
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
 __device__ __forceinline__ void fence_mbar_init() {
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
@@ -159,6 +177,7 @@ __global__ void __launch_bounds__(32 * (1 + kFpWarps), 1)
       };
       const int64_t pre = nk < kGatherStages - 1 ? nk : kGatherStages - 1;
       for (int64_t k = 0; k < pre; ++k) issue_load(k);
+      griddep_wait();   // the previous kernel of the stream may still write `out` / the secondary
       for (int64_t k = 0; k < nk; ++k) {
         const int s = (int)(k % kGatherStages);
         mbar_wait(&full_bar[s], (uint32_t)((k / kGatherStages) & 1));   // issued bulk loads always land
@@ -185,6 +204,7 @@ __global__ void __launch_bounds__(32 * (1 + kFpWarps), 1)
           issue_load(k + kGatherStages - 1);
         }
       }
+      griddep_launch_dependents();   // every load and store of this CTA is issued
       bulk_wait_all();       // all bulk stores performed
       fence_proxy_async();   // ... and ordered before the generic-proxy release below
     }
@@ -265,6 +285,7 @@ __global__ void __launch_bounds__(32 + RsCfg<P, ADAM, MODE>::kConsumers, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
+    griddep_wait();                      // the caller's gradient writes (previous kernel) are done
     if (r.ready.n) {
       __threadfence_system();
       release_all(r.ready);              // E5
@@ -311,6 +332,7 @@ __global__ void __launch_bounds__(32 + RsCfg<P, ADAM, MODE>::kConsumers, 1)
           tma_load(wmv + 2 * C::kChunk, a.v + e0, bytes, &full_bar[s]);
         }
       }
+      griddep_launch_dependents();
     }
   } else {
     for (int64_t k = 0; k < nk; ++k) {
@@ -393,6 +415,27 @@ __global__ void __launch_bounds__(32 + RsCfg<P, ADAM, MODE>::kConsumers, 1)
   }
 }
 
+// Launch with programmatic stream serialization (PDL): the kernel may begin while the
+// previous kernel in the stream finishes its tail.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), int grid, int block, int smem, cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+#ifdef HPZ_NO_PDL
+  cfg.numAttrs = 0;
+#else
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+#endif
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
 template <int P, bool ADAM, int MODE>
 cudaError_t launch_rs_tma_t(const RSParams& r, const AdamParams& a, int grid, cudaStream_t s) {
   using C = RsCfg<P, ADAM, MODE>;
@@ -404,8 +447,7 @@ cudaError_t launch_rs_tma_t(const RSParams& r, const AdamParams& a, int grid, cu
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  rs_tma_kernel<P, ADAM, MODE><<<grid, 32 + C::kConsumers, smem, s>>>(r, a);
-  return cudaGetLastError();
+  return launch_pdl(rs_tma_kernel<P, ADAM, MODE>, grid, 32 + C::kConsumers, smem, s, r, a);
 }
 
 // qgZ quantizer: 4 threads per 64-element block, each holding 4 float4s (elements
@@ -773,11 +815,8 @@ cudaError_t launch_gather_tma(const GatherParams& p, int grid, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     attr_set[fp] = true;
   }
-  if (fp)
-    gather_tma_kernel<true><<<grid, 32 * (1 + kFpWarps), smem, s>>>(p);
-  else
-    gather_tma_kernel<false><<<grid, 32, smem, s>>>(p);
-  return cudaGetLastError();
+  return fp ? launch_pdl(gather_tma_kernel<true>, grid, 32 * (1 + kFpWarps), smem, s, p)
+            : launch_pdl(gather_tma_kernel<false>, grid, 32, smem, s, p);
 }
 
 cudaError_t launch_push_gather(const PushParams& p, int grid, cudaStream_t s) {
