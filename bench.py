@@ -301,6 +301,7 @@ def main():
     t_end.record(stream)
     barrier()
     clk = clocks.stop() if rank == 0 else None
+    barrier()        # rank 0 spent ~0.25 s stopping the sampler: realign before the breakdown steps
     cnt = H.hpz_counters(ctx)
     launches = cnt["launches"] - launches0
     K = args.steps
