@@ -428,3 +428,18 @@ def test_checkpoint_resume_is_bit_identical():
 def buffer_view_f32(rc, i):
     from paper_2407_01614_b200.world import buffer_view
     return buffer_view(rc, i, "master", "f32").cpu().numpy().view(np.uint32).copy()
+
+
+def test_order_switch_between_steps():
+    """hpz_set_order may change between steps (all ranks alike): fixed -> off -> paper ->
+    fixed trains exactly like fixed throughout (all orders compute the same values)."""
+    from paper_2407_01614_b200 import hpz as H
+    run = ParityRun(NUMELS, 4, 2, fused=True, verify="fingerprint")
+    try:
+        for order in ("fixed", "off", "paper", "fixed"):
+            for rc in run.w.ranks:
+                H.hpz_set_order(rc.ctx, order)
+            _check_step(run, run.step())
+        assert run.counters()["timeouts"] == 0
+    finally:
+        run.close()

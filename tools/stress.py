@@ -26,16 +26,18 @@ def run(order, args, world, rank, local, node_size, numels):
     from paper_2407_01614_b200 import hpz as H
     from paper_2407_01614_b200.world import DistWorld, EmulatedWorld, sum_over_ranks
     from synth import inputs as S
+    kw = dict(n_grad_slots=2, timeout_s=60.0, qgz=args.qgz, qwz=args.qwz, grad_dtype=args.grad_dtype)
     if world > 1:
-        W = DistWorld(numels, node_size, n_grad_slots=2, device=local, timeout_s=60.0)
+        W = DistWorld(numels, node_size, device=local, **kw)
     else:
-        W = EmulatedWorld(numels, 1, 1, n_grad_slots=2, device=local, timeout_s=60.0)
+        W = EmulatedWorld(numels, 1, 1, device=local, **kw)
     rc = W.ranks[0]
     ctx = rc.ctx
     s = torch.cuda.current_stream()
     H.hpz_set_order(ctx, order, stock_delay_us=args.stock_delay_us if order == "stock" else 0,
                     stock_poison=order == "stock")
-    H.hpz_set_verify(ctx, "exact")
+    # EXACT compares against raw primaries: not meaningful with qwZ (dequantized gathers)
+    H.hpz_set_verify(ctx, "fingerprint" if (args.qwz or args.verify == "fingerprint") else "exact")
     L = len(numels)
     for i in range(L):
         H.hpz_synth_master(ctx, i, S.stream_key(S.SEED_PARAMS, i, 0, 0), S.PARAM_SCALE, s)
@@ -71,6 +73,10 @@ def main():
     ap.add_argument("--stock-steps", type=int, default=3)
     ap.add_argument("--stock-delay-us", type=int, default=20000)
     ap.add_argument("--model", default="llama2_70b_layers")
+    ap.add_argument("--qgz", action="store_true")
+    ap.add_argument("--qwz", action="store_true")
+    ap.add_argument("--grad-dtype", default="f32")
+    ap.add_argument("--verify", default="exact", choices=["exact", "fingerprint"])
     args = ap.parse_args()
     import torch
     import torch.distributed as dist
@@ -88,6 +94,7 @@ def main():
         res.append(run("stock", args, world, rank, local, node_size, numels))
     if rank == 0:
         out = {"config": f"C5 stress: {args.model} ({len(numels)} x {numels[0]} elements), P={world}, P'={node_size}",
+               "options": {"qgz": args.qgz, "qwz": args.qwz, "grad_dtype": args.grad_dtype},
                "runs": res,
                "pass": res[0]["mismatched_elements"] == 0 and res[0]["fingerprint_mismatched_layers"] == 0
                and res[0]["timeouts"] == 0 and (len(res) < 2 or res[1]["mismatched_elements"] > 0)}
