@@ -885,8 +885,9 @@ int hpz_bwd_gather(hpz_ctx* c, int layer, void* full_out, void* stream) {
     p.fp_checked = c->stat(3);
   }
   p.done_ctr = c->ctr(C_BWD, layer);
-  if (c->order != HPZ_ORDER_OFF)
-    for (int q = 0; q < c->node_size; ++q) p.rel.ptr[p.rel.n++] = c->flag(nf + q, F_BWD_DONE, layer, c->rank);   // E4
+  // E4 (released in every order, so the order may change between steps: the next step's
+  // secondary writes wait for it even after an OFF step that read no secondary)
+  for (int q = 0; q < c->node_size; ++q) p.rel.ptr[p.rel.n++] = c->flag(nf + q, F_BWD_DONE, layer, c->rank);
   if (reads_prim)
     for (int j = 0; j < c->world; ++j) p.rel.ptr[p.rel.n++] = c->flag(j, F_BWDP_DONE, layer, c->rank);
   p.rel.value = t1;
