@@ -23,7 +23,7 @@ NUMELS = [300_007, 65_536, 4_099, 77]
 TOPOS = [(1, 1), (2, 1), (2, 2), (4, 1), (4, 2), (4, 4), (8, 1), (8, 2), (8, 4), (8, 8)]
 
 
-def _check_step(run: ParityRun, rec, check_all=True):
+def _check_step(run: ParityRun, rec, check_all=True, check_secondary=True):
     P, dtype = run.P, run.dtype
     for i, lay in enumerate(run.o.layouts):
         W = O.param_bits(rec.W[i], dtype)
@@ -41,7 +41,7 @@ def _check_step(run: ParityRun, rec, check_all=True):
         for r, rc in enumerate(run.w.ranks):
             st = run.o.state[i][r]
             # a2 secondary store == oracle's Eq. (1) slice
-            if run.o.order == "fixed":   # (paper maps to fixed)
+            if run.o.order == "fixed" and check_secondary:   # (paper maps to fixed)
                 sec = bits_np(buffer_view(rc, i, "secondary", dtype), dtype)
                 assert np.array_equal(sec, O.param_bits(st.sec, dtype)), f"secondary layer {i} rank {r}"
             # a5 reduce-scatter bit-exact in the fixed order
@@ -102,7 +102,8 @@ def test_parity_qgz(P, Pp, fused):
     run = ParityRun(NUMELS, P, Pp, qgz=True, fused=fused, verify="fingerprint")
     try:
         for _ in range(3):
-            _check_step(run, run.step())
+            # an OFF step writes no secondary (plain ZeRO-3): its content is step t-1's
+            _check_step(run, run.step(), check_secondary=order != "off")
         assert run.counters()["timeouts"] == 0
     finally:
         run.close()
@@ -115,7 +116,8 @@ def test_parity_bf16_grads(P, Pp, fused):
     run = ParityRun(NUMELS, P, Pp, grad_dtype="bf16", fused=fused, verify="fingerprint")
     try:
         for _ in range(3):
-            _check_step(run, run.step())
+            # an OFF step writes no secondary (plain ZeRO-3): its content is step t-1's
+            _check_step(run, run.step(), check_secondary=order != "off")
         assert run.counters()["timeouts"] == 0
     finally:
         run.close()
@@ -439,7 +441,8 @@ def test_order_switch_between_steps():
         for order in ("fixed", "off", "paper", "fixed"):
             for rc in run.w.ranks:
                 H.hpz_set_order(rc.ctx, order)
-            _check_step(run, run.step())
+            # an OFF step writes no secondary (plain ZeRO-3): its content is step t-1's
+            _check_step(run, run.step(), check_secondary=order != "off")
         assert run.counters()["timeouts"] == 0
     finally:
         run.close()
