@@ -52,6 +52,8 @@ def parse():
     ap.add_argument("--qwz", action="store_true", help="ZeRO++ qwZ: INT8 weights in the forward gather (SURVEY f2)")
     ap.add_argument("--gather", default="pull", choices=["pull", "push"],
                     help="forward gather: ranks pull (default) or owners push into arena landing buffers")
+    ap.add_argument("--rs", default="pull", choices=["pull", "push"],
+                    help="reduce-scatter: owners pull slices (default) or ranks push them into owners' landing slots")
     ap.add_argument("--grad-dtype", default="f32", choices=["f32", "bf16"],
                     help="gradient slot dtype (bf16: SURVEY f4, fp32 accumulation)")
     ap.add_argument("--grad-slots", type=int, default=0,
@@ -195,7 +197,7 @@ def main():
     if world > 1:
         W = DistWorld(numels, node_size, dtype=dtype, n_grad_slots=n_slots, device=local_rank, timeout_s=60.0,
                       qgz=args.qgz, grad_dtype=args.grad_dtype, qwz=args.qwz,
-                      landing_bufs=1 if args.gather == "push" else 0)
+                      landing_bufs=1 if args.gather == "push" else 0, rs_push=args.rs == "push")
     else:
         W = EmulatedWorld(numels, 1, 1, dtype=dtype, n_grad_slots=n_slots, device=local_rank, timeout_s=60.0,
                           qgz=args.qgz, grad_dtype=args.grad_dtype, qwz=args.qwz,
@@ -434,6 +436,7 @@ def main():
                        "world": world, "node_size": node_size, "virtual_nodes": world // node_size,
                        "parallelism": f"hpZ dp{world} (P={world}, P'={node_size})", "order": args.order,
                        "verify": args.verify, "copy_engine": args.copy_engine, "fwd_gather": args.gather,
+                       "reduce_scatter": args.rs if world > 1 else "local",
                        "qgz": "int4 blockwise (64) gradient all-to-all; RS bytes counted as the fp32 "
                               "gradient bytes reduced, wire bytes 0.625 B/elem" if args.qgz else None,
                        "grad_dtype": args.grad_dtype, "grad_slots": n_slots,

@@ -317,9 +317,20 @@ typedef enum {
                                     every rank's landing buffer and the secondaries over NVLink
                                     (P2P stores), instead of every rank pulling.  FIXED order,
                                     no qwZ.  Set before hpz_register_flat_params. */
-  HPZ_OPT_SPLIT_PHASES = 8       /* 0/1: push gathers leave their post / finish phases to the
+  HPZ_OPT_SPLIT_PHASES = 8,      /* 0/1: push gathers leave their post / finish phases to the
                                     caller (hpz_fwd_gather_post / _finish) — needed when several
-                                    ranks share one GPU stream (single-GPU emulation) */
+                                    ranks share one GPU stream (single-GPU emulation); with
+                                    HPZ_OPT_RS_PUSH, hpz_grads_ready runs the push phase */
+  HPZ_OPT_RS_PUSH = 9            /* 0 (default) or 1, P >= 2, fp32 or bf16 gradients (not qgZ):
+                                    owner-driven reduce-scatter.  Every rank bulk-stores the
+                                    slices of its gradient slot into the owners' landing slots
+                                    over NVLink (posted writes, one chunk counter per 2048 or
+                                    1024 elements incremented per source) and each owner reduces
+                                    from its local landing slot as the chunks arrive, in the
+                                    same R7 order (same bits as the pull).  One kernel per layer
+                                    does both (a push warp beside the reduce pipeline); two
+                                    landing slots of P x max-shard gradient elements are added
+                                    to the arena.  Set before hpz_register_flat_params. */
 } hpz_option;
 /* Copy engine of the gathers and the reduce-scatter: TMA 1-D bulk copies through a
  * shared-memory stage ring (cp.async.bulk, one persistent CTA per SM), or 16-byte

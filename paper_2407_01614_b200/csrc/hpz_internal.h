@@ -124,7 +124,20 @@ struct RSParams {
   ReleaseList ready;                   // E5 release (may be empty if already released)
   WaitList ready_wait;                 // E5 acquire of every rank
   uint32_t* done_ctr;
-  ReleaseList rel;                     // E6 release
+  ReleaseList rel;                     // E6 release (push: landing slot free, to every pusher)
+  // push reduce-scatter (HPZ_OPT_RS_PUSH): src[j != self] are then my LOCAL landing slot's
+  // slices (written by rank j), src[self] my own gradient slot's slice
+  int push_on, reduce_on, self;
+  const char* push_src;                // my gradient slot (local); owner q's slice at q * push_shard_bytes
+  int64_t push_shard_bytes;            // shard * gradient bytes
+  char* push_dst[kMaxWorld];           // owner q's landing slot + my slice (nullptr for q == self)
+  uint32_t* push_ctr[kMaxWorld];       // owner q's chunk counters of that landing slot
+  const uint32_t* push_free[kMaxWorld];  // local: owner q released the slot's previous use
+  uint32_t push_free_target;
+  uint32_t* chunk_ctr;                 // reduce: my chunk counters of the landing slot (reset to 0
+                                       // once consumed: layers of different sizes share a slot)
+  uint32_t chunk_target;               // P - 1
+  ReleaseList rel2;                    // push: E6 of my own gradient slot (local flags)
   SyncCommon sync;
 };
 
@@ -155,7 +168,9 @@ cudaError_t launch_rs_adam(const RSParams& r, const AdamParams& a, int world, in
 cudaError_t launch_gather_tma(const GatherParams& p, int grid, cudaStream_t s);
 // mode: 0 fp32 gradients, 1 bf16 gradients (fp32 accumulation), 2 qgZ INT4 codes
 cudaError_t launch_rs_tma(const RSParams& r, const AdamParams* a, int world, int grid, cudaStream_t s,
-                          int mode = 0);
+                          int mode = 0, bool push = false);
+// Chunk (elements of a shard) of the push reduce-scatter: one landing counter per chunk.
+int rs_push_chunk_elems(int world);
 cudaError_t launch_qgz_quantize(const QuantParams& q, int grid, cudaStream_t s);
 cudaError_t launch_push_gather(const PushParams& p, int grid, cudaStream_t s);
 cudaError_t launch_qwz_quantize(const QwzQuantParams& q, int grid, cudaStream_t s);

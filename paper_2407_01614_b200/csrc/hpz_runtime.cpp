@@ -31,6 +31,8 @@ struct Layer {
   uint64_t off_primary, off_master, off_m, off_v, off_gshard, off_secondary;
   uint64_t off_qw_codes = 0, off_qw_params = 0;   // qwZ (f2)
   int slot;
+  int rsl = -1;          // push RS: landing slot of the layer's pending reduce (-1: none)
+  uint64_t rsl_use = 0;  // ... and that slot's use index
   // host bookkeeping of the step t the layer's ops were issued for (-1: never)
   int64_t fwd_t = -1, bwd_t = -1, rs_t = -1, step_t = -1;
 };
@@ -76,6 +78,13 @@ struct hpz_ctx {
   std::vector<int> land_pending;          // per layer: landing buffer awaiting finish (-1: none)
   uint64_t land_bytes = 0;
   std::vector<uint64_t> off_qcodes, off_qparams;   // per grad slot (qgZ)
+  // push reduce-scatter (HPZ_OPT_RS_PUSH): kRsl landing slots of world x max-shard gradient
+  // elements, one chunk counter per rs_push_chunk_elems elements of a shard per slot
+  static constexpr int kRsl = 2;
+  bool rs_push = false;
+  uint64_t off_rsl[kRsl] = {}, rsl_stride = 0, off_rsc = 0;
+  int64_t rsc_chunks = 0;
+  uint64_t rs_seq = 0;                    // pushes issued (identical on every rank: SPMD order)
   std::string err;
 
   // ---- arena addressing (identical on every rank) ----
@@ -92,6 +101,15 @@ struct hpz_ctx {
     const uint64_t base = (uint64_t)F_NUM_LAYER_KINDS * n_layers * world + (uint64_t)S_NUM * n_slots * world;
     const uint64_t idx = base + ((uint64_t)kind * n_land + b) * world + src;
     return reinterpret_cast<uint32_t*>(arena[rank_arena] + off_flags) + idx;
+  }
+  // RL_FREE: owner `src` finished reducing from landing slot b (value = use + 1)
+  uint32_t* rl_flag(int rank_arena, int b, int src) const {
+    const uint64_t base = (uint64_t)F_NUM_LAYER_KINDS * n_layers * world + (uint64_t)S_NUM * n_slots * world +
+                          (uint64_t)LF_NUM * n_land * world;
+    return reinterpret_cast<uint32_t*>(arena[rank_arena] + off_flags) + base + (uint64_t)b * world + src;
+  }
+  uint32_t* rsc(int rank_arena, int b) const {
+    return reinterpret_cast<uint32_t*>(arena[rank_arena] + off_rsc) + (uint64_t)b * rsc_chunks;
   }
   uint32_t* ctr(int kind, int idx) const {
     return reinterpret_cast<uint32_t*>(arena[rank] + off_ctr) + (uint64_t)kind * (n_layers + n_slots) + idx;
@@ -169,6 +187,10 @@ cudaError_t gather_launch(const hpz_ctx* c, const GatherParams& p, cudaStream_t 
 }
 
 cudaError_t rs_launch(const hpz_ctx* c, const RSParams& r, const AdamParams* a, cudaStream_t s) {
+  if (c->rs_push) {
+    const int64_t ch = rs_push_chunk_elems(c->world);
+    return launch_rs_tma(r, a, c->world, grid_for(c, (r.n_vec * 4 + ch - 1) / ch, 1), s, c->grad_bytes == 2 ? 1 : 0, true);
+  }
   if (c->qgz_bits || c->grad_bytes == 2)   // qgZ codes / bf16 gradients: TMA engine only
     return launch_rs_tma(r, a, c->world, grid_for(c, (r.n_vec * 4 + 1023) / 1024, 1), s, c->qgz_bits ? 2 : 1);
   if (c->copy_engine == HPZ_COPY_TMA)
@@ -317,8 +339,16 @@ int hpz_register_flat_params(hpz_ctx* c, int n_layers, const int64_t* numel, int
     if (L.numel_pad > c->slot_numel[L.slot]) c->slot_numel[L.slot] = L.numel_pad;
   }
   // control region: flags | completion counters | fingerprints | stats
+  if (c->world == 1) c->rs_push = false;   // nothing to push
+  int64_t smax = 0;
+  for (int i = 0; i < n_layers; ++i) {
+    const Layer& L = c->layers[i];
+    smax = L.shard > smax ? L.shard : smax;
+  }
+  const int64_t push_chunk = c->rs_push ? rs_push_chunk_elems(c->world) : 1;
+  c->rsc_chunks = c->rs_push ? (smax + push_chunk - 1) / push_chunk : 0;
   const uint64_t n_flags = (uint64_t)F_NUM_LAYER_KINDS * n_layers * c->world + (uint64_t)S_NUM * n_grad_slots * c->world +
-                           (uint64_t)LF_NUM * c->n_land * c->world;
+                           (uint64_t)LF_NUM * c->n_land * c->world + (uint64_t)hpz_ctx::kRsl * c->world;
   uint64_t off = 0;
   c->off_flags = off;
   off = align_up(off + n_flags * 4, 256);
@@ -328,6 +358,8 @@ int hpz_register_flat_params(hpz_ctx* c, int n_layers, const int64_t* numel, int
   off = align_up(off + (uint64_t)n_layers * 4 * 8, 256);
   c->off_stats = off;
   off = align_up(off + 8 * 8, 256);
+  c->off_rsc = off;
+  off = align_up(off + (uint64_t)hpz_ctx::kRsl * c->rsc_chunks * 4, 256);
   c->ctrl_bytes = align_up(off, kCtrlAlign);
   off = c->ctrl_bytes;
   for (int i = 0; i < n_layers; ++i) {
@@ -370,6 +402,13 @@ int hpz_register_flat_params(hpz_ctx* c, int n_layers, const int64_t* numel, int
   for (int b = 0; b < c->n_land; ++b) {
     c->off_land[b] = off;
     off = align_up(off + c->land_bytes, kBufAlign);
+  }
+  if (c->rs_push) {   // landing slots: rank j's slice for me at j * max-shard
+    c->rsl_stride = (uint64_t)smax * c->grad_bytes;
+    for (int b = 0; b < hpz_ctx::kRsl; ++b) {
+      c->off_rsl[b] = off;
+      off = align_up(off + c->rsl_stride * c->world, kBufAlign);
+    }
   }
   c->arena_bytes = off;
   c->registered = true;
@@ -968,11 +1007,19 @@ static int qgz_quantize(hpz_ctx* c, int layer, cudaStream_t s) {
   return HPZ_OK;
 }
 
+static int rs_push_phase(hpz_ctx* c, int layer, cudaStream_t s);
+
 int hpz_grads_ready(hpz_ctx* c, int layer, void* stream) {
   if (int rc = check_ready(c)) return rc;
   if (int rc = check_layer(c, layer)) return rc;
   const int slot = c->layers[layer].slot;
   if (c->slot_ready_sent[slot]) return fail(c, HPZ_ESTATE, "grads_ready already published for this use of the slot");
+  if (c->rs_push) {   // the owners never read my slot: nothing to publish, except the push itself
+    if (c->split_phases)
+      if (int rc = rs_push_phase(c, layer, static_cast<cudaStream_t>(stream))) return rc;
+    c->slot_ready_sent[slot] = 1;
+    return HPZ_OK;
+  }
   if (c->qgz_bits)
     if (int rc = qgz_quantize(c, layer, static_cast<cudaStream_t>(stream))) return rc;
   cudaError_t e = launch_release(grad_ready_list(c, slot), static_cast<cudaStream_t>(stream));
@@ -982,10 +1029,77 @@ int hpz_grads_ready(hpz_ctx* c, int layer, void* stream) {
   return HPZ_OK;
 }
 
+// Push RS: the landing slot (and its use index) a layer's push / reduce pair goes through;
+// assigned by the push, in the same order on every rank.
+static void rsl_assign(hpz_ctx* c, int layer) {
+  Layer& L = c->layers[layer];
+  if (L.rsl >= 0) return;
+  L.rsl = (int)(c->rs_seq % hpz_ctx::kRsl);
+  L.rsl_use = c->rs_seq / hpz_ctx::kRsl;
+  c->rs_seq += 1;
+}
+
+// Push RS parameters: push_on = my slices go out, reduce_on = I reduce my landing slot.
+static void build_rs_push(hpz_ctx* c, int layer, RSParams& p, bool push_on, bool reduce_on) {
+  Layer& L = c->layers[layer];
+  const int slot = L.slot;
+  const int b = L.rsl;
+  const uint64_t gb = (uint64_t)c->grad_bytes;
+  p = RSParams{};
+  p.push_on = push_on;
+  p.reduce_on = reduce_on;
+  p.self = c->rank;
+  for (int j = 0; j < c->world; ++j)
+    p.src[j] = reinterpret_cast<const float*>(
+        j == c->rank ? c->arena[c->rank] + c->off_slot[slot] + (uint64_t)c->rank * L.shard * gb
+                     : c->arena[c->rank] + c->off_rsl[b] + (uint64_t)j * c->rsl_stride);
+  p.out = reinterpret_cast<float*>(c->arena[c->rank] + L.off_gshard);
+  p.n_vec = L.shard / 4;
+  p.inv_p = (float)(1.0 / c->world);
+  p.chunk_ctr = c->rsc(c->rank, b);
+  p.chunk_target = (uint32_t)(c->world - 1);
+  p.push_src = c->arena[c->rank] + c->off_slot[slot];
+  p.push_shard_bytes = L.shard * (int64_t)gb;
+  for (int q = 0; q < c->world; ++q) {
+    if (q == c->rank) continue;
+    p.push_dst[q] = c->arena[q] + c->off_rsl[b] + (uint64_t)c->rank * c->rsl_stride;
+    p.push_ctr[q] = c->rsc(q, b);
+    p.push_free[q] = c->rl_flag(c->rank, b, q);
+  }
+  p.push_free_target = epoch(L.rsl_use);
+  p.done_ctr = c->ctr(C_RS, c->n_layers + slot);
+  if (reduce_on) {   // my landing slot b may be refilled by every pusher
+    for (int j = 0; j < c->world; ++j)
+      if (j != c->rank) p.rel.ptr[p.rel.n++] = c->rl_flag(j, b, c->rank);
+    p.rel.value = epoch(L.rsl_use + 1);
+  }
+  if (push_on) {     // E6 of my gradient slot: every read of it (the pushes) is complete
+    for (int j = 0; j < c->world; ++j) p.rel2.ptr[p.rel2.n++] = c->slot_flag(c->rank, S_RS_DONE, slot, j);
+    p.rel2.value = epoch(c->slot_use[slot] + 1);
+  }
+  p.sync = c->sync();
+}
+
+static int rs_push_phase(hpz_ctx* c, int layer, cudaStream_t s) {
+  rsl_assign(c, layer);
+  RSParams p;
+  build_rs_push(c, layer, p, true, false);
+  cudaError_t e = rs_launch(c, p, nullptr, s);
+  if (e != cudaSuccess) return fail(c, HPZ_ECUDA, "push reduce-scatter launch: %s", cudaGetErrorString(e));
+  c->launches += 1;
+  return HPZ_OK;
+}
+
 static void build_rs(hpz_ctx* c, int layer, RSParams& p) {
   Layer& L = c->layers[layer];
   const int slot = L.slot;
   const uint32_t u1 = epoch(c->slot_use[slot] + 1);
+  if (c->rs_push) {   // fused push + reduce, or the reduce after a split push phase
+    const bool pushed = L.rsl >= 0;
+    rsl_assign(c, layer);
+    build_rs_push(c, layer, p, !pushed, true);
+    return;
+  }
   p = RSParams{};
   for (int j = 0; j < c->world; ++j)
     p.src[j] = reinterpret_cast<const float*>(c->arena[j] + c->off_slot[slot] + (uint64_t)c->rank * L.shard * c->grad_bytes);
@@ -1009,6 +1123,7 @@ static void build_rs(hpz_ctx* c, int layer, RSParams& p) {
 
 static void rs_issued(hpz_ctx* c, int layer) {
   Layer& L = c->layers[layer];
+  L.rsl = -1;
   c->slot_use[L.slot] += 1;
   c->slot_ready_sent[L.slot] = 0;
   L.rs_t = c->t;
@@ -1150,6 +1265,7 @@ int hpz_set_option(hpz_ctx* c, int option, int64_t value) {
       if (c->registered) return fail(c, HPZ_ESTATE, "qgZ must be chosen before hpz_register_flat_params");
       if (value != 0 && value != 4) return fail(c, HPZ_EINVAL, "qgZ bits must be 0 (off) or 4");
       if (value && c->grad_bytes != 4) return fail(c, HPZ_EINVAL, "qgZ quantizes fp32 gradients");
+      if (value && c->rs_push) return fail(c, HPZ_EINVAL, "qgZ is not available with the push reduce-scatter");
       c->qgz_bits = (int)value;
       return HPZ_OK;
     case HPZ_OPT_LANDING_BUFS:
@@ -1174,6 +1290,12 @@ int hpz_set_option(hpz_ctx* c, int option, int64_t value) {
       if (value != HPZ_F32 && value != HPZ_BF16) return fail(c, HPZ_EINVAL, "gradient dtype must be HPZ_F32 or HPZ_BF16");
       if (value == HPZ_BF16 && c->qgz_bits) return fail(c, HPZ_EINVAL, "qgZ quantizes fp32 gradients");
       c->grad_bytes = value == HPZ_BF16 ? 2 : 4;
+      return HPZ_OK;
+    case HPZ_OPT_RS_PUSH:
+      if (c->registered) return fail(c, HPZ_ESTATE, "the push reduce-scatter must be chosen before hpz_register_flat_params");
+      if (value != 0 && value != 1) return fail(c, HPZ_EINVAL, "rs_push must be 0 or 1");
+      if (value && c->qgz_bits) return fail(c, HPZ_EINVAL, "the push reduce-scatter carries fp32 / bf16 gradients, not qgZ codes");
+      c->rs_push = value != 0;
       return HPZ_OK;
     case HPZ_OPT_COPY_ENGINE:
       if (value != HPZ_COPY_LDG && value != HPZ_COPY_TMA) return fail(c, HPZ_EINVAL, "copy engine must be 0 (LDG) or 1 (TMA)");

@@ -250,35 +250,62 @@ __global__ void __launch_bounds__(32 * (1 + kFpWarps), 1)
 // ------------------------------------------------------------------ RS (+ Adam) (a5, a6)
 enum RsMode { RS_F32 = 0, RS_BF16 = 1, RS_QGZ = 2 };
 
-template <int P, bool ADAM, int MODE>
+// Push reduce-scatter (HPZ_OPT_RS_PUSH) geometry: landing counters count chunks of this size.
+__host__ __device__ constexpr int rs_push_chunk(int P) { return P <= 4 ? 2048 : 1024; }
+
+template <int P, bool ADAM, int MODE, bool PUSH = false>
 struct RsCfg {
   static constexpr bool QGZ = MODE == RS_QGZ;
   // per stage: P gradient slices (fp32, or qgZ int4 codes + (min, scale) per 64) (+ w, m, v);
   // qgZ chunks are longer so its small code/param copies stay >= 1 KiB / 256 B
   // P=1 (local, HBM-bound): 1024-element chunks keep 6 stages in flight; 2 <= P <= 8: 2048
-  static constexpr int kChunk = (P >= 2 && P <= 8 ? 2 : 1) * (QGZ ? 2 * kRsChunk : kRsChunk);
+  static constexpr int kChunk =
+      PUSH ? rs_push_chunk(P) : (P >= 2 && P <= 8 ? 2 : 1) * (QGZ ? 2 * kRsChunk : kRsChunk);
+  static constexpr int kGradBytes = MODE == RS_BF16 ? 2 : 4;
   static constexpr int kCodeBytes = kChunk / 2;
   static constexpr int kParamBytes = kChunk / kQgzBlock * 8;
-  static constexpr int kSrcBytes = QGZ ? kCodeBytes + kParamBytes : kChunk * (MODE == RS_BF16 ? 2 : 4);
+  static constexpr int kSrcBytes = QGZ ? kCodeBytes + kParamBytes : kChunk * kGradBytes;
   static constexpr int kWmvOff = P * kSrcBytes;
   static constexpr int kStageBytes = kWmvOff + (ADAM ? 3 * kChunk * 4 : 0);
-  static constexpr int kStages = (200 * 1024) / kStageBytes >= 6 ? 6 : (200 * 1024) / kStageBytes;
+  // push ring: one unit = one chunk slice for one owner.  A stage is refilled as soon as its
+  // bulk store has READ it (kPushStages - 1 loads run ahead); up to kPushLag stores stay in
+  // flight before the oldest one's completion is awaited and the owner's chunk counter is
+  // incremented (remote write completion takes tens of microseconds under load)
+  static constexpr int kPushStages = 8;
+  static constexpr int kPushLag = 24;
+  static constexpr int kPushBatch = 16;
+  static constexpr int kPushUnit = kChunk * kGradBytes;
+  static constexpr int kPushBytes = PUSH ? kPushStages * kPushUnit : 0;
+  static constexpr int kBudget = PUSH ? 216 * 1024 - kPushBytes : 200 * 1024;
+  static constexpr int kStages = kBudget / kStageBytes >= 6 ? 6 : kBudget / kStageBytes;
   // consumer threads: one float4 per thread per chunk, at most 16 warps (idle polling
   // warps would steal issue slots from the working ones)
   static constexpr int kConsumers = kChunk / 4 < kRsMaxConsumers ? kChunk / 4 : kRsMaxConsumers;
+  static constexpr int kLead = PUSH ? 64 : 32;   // producer warp (+ push warp)
 };
 
-// Block = 1 producer warp + 8 consumer warps.  Dynamic smem = kStages * kStageBytes.
-template <int P, bool ADAM, int MODE>
-__global__ void __launch_bounds__(32 + RsCfg<P, ADAM, MODE>::kConsumers, 1)
+__device__ __forceinline__ void red_relaxed_sys_add(uint32_t* p, uint32_t v) {
+  asm volatile("red.relaxed.sys.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait() {
+  asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// Block = 1 producer warp (+ 1 push warp) + consumer warps.  Dynamic smem = kStages *
+// kStageBytes (+ the push ring).
+template <int P, bool ADAM, int MODE, bool PUSH>
+__global__ void __launch_bounds__(RsCfg<P, ADAM, MODE, PUSH>::kLead + RsCfg<P, ADAM, MODE, PUSH>::kConsumers, 1)
     rs_tma_kernel(const __grid_constant__ RSParams r, const __grid_constant__ AdamParams a) {
-  using C = RsCfg<P, ADAM, MODE>;
+  using C = RsCfg<P, ADAM, MODE, PUSH>;
   constexpr bool QGZ = C::QGZ;
   constexpr bool BF16 = MODE == RS_BF16;
   static_assert(C::kStages >= 2, "stage ring too small");
+  static_assert(!(PUSH && QGZ), "push RS carries fp32 / bf16 gradients");
   extern __shared__ __align__(1024) char smem[];
   __shared__ __align__(8) uint64_t full_bar[C::kStages];
   __shared__ __align__(8) uint64_t empty_bar[C::kStages];
+  __shared__ __align__(8) uint64_t push_bar[PUSH ? C::kPushStages : 1];
   const int64_t n = r.n_vec * 4;   // shard elements (multiple of 256)
   const int64_t total = (n + C::kChunk - 1) / C::kChunk;
   const int64_t nk = blockIdx.x < total ? (total - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
@@ -286,27 +313,109 @@ __global__ void __launch_bounds__(32 + RsCfg<P, ADAM, MODE>::kConsumers, 1)
 
   if (threadIdx.x == 0) {
     griddep_wait();                      // the caller's gradient writes (previous kernel) are done
-    if (r.ready.n) {
-      __threadfence_system();
-      release_all(r.ready);              // E5
+    if constexpr (!PUSH) {
+      if (r.ready.n) {
+        __threadfence_system();
+        release_all(r.ready);            // E5
+      }
+      wait_all(r.ready_wait, r.sync);    // E5: every rank's gradient slot is written
+      if (ADAM) wait_all(a.wait, a.sync);  // E2 (+E7): nobody still reads my primary
+      fence_proxy_async();
     }
-    wait_all(r.ready_wait, r.sync);      // E5: every rank's gradient slot is written
-    if (ADAM) wait_all(a.wait, a.sync);  // E2 (+E7): nobody still reads my primary
-    fence_proxy_async();
     for (int s = 0; s < C::kStages; ++s) {
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], C::kConsumers / 32);
     }
+    if constexpr (PUSH)
+      for (int s = 0; s < C::kPushStages; ++s) mbar_init(&push_bar[s], 1);
     fence_mbar_init();
   }
   __syncthreads();
 
-  if (warp == 0) {
-    if (lane == 0) {
+  if (PUSH && warp == 1) {
+    // push warp: my gradient slot's slice of every chunk this CTA owns, for every other
+    // owner q: local bulk load -> smem -> bulk store into q's landing slot; once the store
+    // is complete, q's chunk counter is incremented (release, system scope)
+    if (lane == 0 && r.push_on) {
+      for (int q = 0; q < P; ++q)
+        if (r.push_free[q] != nullptr) wait_geq(r.push_free[q], r.push_free_target, r.sync);
+      fence_proxy_async();
+      char* ring = smem + (size_t)C::kStages * C::kStageBytes;
+      const int64_t nu = nk * (P - 1);
+      auto unit = [&](int64_t x, int& q, int64_t& w, uint32_t& bytes) {
+        const int64_t k = x / (P - 1);
+        const int d = (int)(x % (P - 1));
+        q = (r.self + 1 + (d + (int)(blockIdx.x % (P - 1))) % (P - 1)) % P;   // never self; rotated per CTA
+        w = blockIdx.x + k * gridDim.x;                                       // global chunk index
+        const int64_t rem = n - w * C::kChunk;
+        bytes = (uint32_t)((rem < C::kChunk ? rem : C::kChunk) * C::kGradBytes);
+      };
+      auto issue = [&](int64_t x) {
+        int q;
+        int64_t w;
+        uint32_t bytes;
+        unit(x, q, w, bytes);
+        const int s = (int)(x % C::kPushStages);
+        mbar_expect_tx(&push_bar[s], bytes);
+        tma_load(ring + (size_t)s * C::kPushUnit, r.push_src + q * r.push_shard_bytes + w * C::kChunk * C::kGradBytes,
+                 bytes, &push_bar[s]);
+      };
+      // Completed units are signalled in batches of kPushBatch: one system-scope fence
+      // (which drains this thread's outstanding writes: measured 63 ms/step at N=2 with a
+      // release per unit vs 28 ms batched) then relaxed remote increments.
+      int64_t sig_from = 0;   // units [sig_from, x] are complete but not yet signalled
+      auto signal_upto = [&](int64_t x) {
+        fence_proxy_async();
+        __threadfence_system();
+        for (int64_t y = sig_from; y <= x; ++y) {
+          int q;
+          int64_t w;
+          uint32_t bytes;
+          unit(y, q, w, bytes);
+          red_relaxed_sys_add(r.push_ctr[q] + w, 1u);
+        }
+        sig_from = x + 1;
+      };
+      constexpr int kAhead = C::kPushStages - 1;
+      for (int64_t x = 0; x < nu && x < kAhead; ++x) issue(x);
+      for (int64_t x = 0; x < nu; ++x) {
+        const int s = (int)(x % C::kPushStages);
+        mbar_wait(&push_bar[s], (uint32_t)((x / C::kPushStages) & 1));
+        int q;
+        int64_t w;
+        uint32_t bytes;
+        unit(x, q, w, bytes);
+        tma_store(r.push_dst[q] + w * C::kChunk * C::kGradBytes, ring + (size_t)s * C::kPushUnit, bytes);
+        bulk_commit();
+        if (x >= C::kPushLag && (x - C::kPushLag + 1) % C::kPushBatch == 0) {
+          bulk_wait<C::kPushLag>();   // units up to x - lag have landed in their owners' memory
+          signal_upto(x - C::kPushLag);
+        }
+        if (x + kAhead < nu) {
+          bulk_wait_read<1>();        // the stage of unit x - 1 has been read by its store
+          issue(x + kAhead);
+        }
+      }
+      bulk_wait_all();
+      if (nu > 0) signal_upto(nu - 1);
+    }
+  } else if (warp == 0) {
+    if (lane == 0 && (!PUSH || r.reduce_on)) {
+      if constexpr (PUSH) {
+        if (ADAM) wait_all(a.wait, a.sync);   // E2 (+E7)
+        fence_proxy_async();
+      }
       for (int64_t k = 0; k < nk; ++k) {
         const int s = (int)(k % C::kStages);
         if (k >= C::kStages) mbar_wait_bounded(&empty_bar[s], (uint32_t)(((k / C::kStages) - 1) & 1), r.sync);
         const int64_t e0 = (blockIdx.x + k * gridDim.x) * (int64_t)C::kChunk;
+        if constexpr (PUSH) {
+          // every other rank's slice of this chunk has landed in my landing slot
+          uint32_t* ctr = r.chunk_ctr + (blockIdx.x + k * gridDim.x);
+          wait_geq(ctr, r.chunk_target, r.sync);
+          *ctr = 0u;   // re-armed for the slot's next use (ordered before the RL_FREE release)
+          fence_proxy_async();
+        }
         const int64_t rem = n - e0;
         const uint32_t cnt = (uint32_t)(rem < C::kChunk ? rem : C::kChunk);
         const uint32_t bytes = cnt * 4;
@@ -334,7 +443,7 @@ __global__ void __launch_bounds__(32 + RsCfg<P, ADAM, MODE>::kConsumers, 1)
       }
       griddep_launch_dependents();
     }
-  } else {
+  } else if (!PUSH || r.reduce_on) {
     for (int64_t k = 0; k < nk; ++k) {
       const int s = (int)(k % C::kStages);
       mbar_wait(&full_bar[s], (uint32_t)((k / C::kStages) & 1));
@@ -400,18 +509,19 @@ __global__ void __launch_bounds__(32 + RsCfg<P, ADAM, MODE>::kConsumers, 1)
       // chunk holds more float4s than there are consumers).  The single-pass form is a
       // separate branch: compiled as a loop it measured ~13% slower.
       if constexpr (C::kConsumers * 4 == C::kChunk) {
-        const int ct = threadIdx.x - 32;
+        const int ct = threadIdx.x - C::kLead;
         if (ct * 4 < cnt) process(ct);
       } else {
-        for (int ct = threadIdx.x - 32; ct * 4 < cnt; ct += C::kConsumers) process(ct);
+        for (int ct = threadIdx.x - C::kLead; ct * 4 < cnt; ct += C::kConsumers) process(ct);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty_bar[s]);
     }
   }
   if (last_cta(r.done_ctr)) {
-    release_all(r.rel);              // E6
-    if (ADAM) release_all(a.rel);    // E1 (t+1)
+    release_all(r.rel);              // E6 (push: my landing slot is free again)
+    if (PUSH) release_all(r.rel2);   // push: E6 of my gradient slot (every push completed)
+    if (ADAM && (!PUSH || r.reduce_on)) release_all(a.rel);   // E1 (t+1)
   }
 }
 
@@ -437,18 +547,18 @@ cudaError_t launch_pdl(void (*kernel)(KArgs...), int grid, int block, int smem, 
   return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
-template <int P, bool ADAM, int MODE>
+template <int P, bool ADAM, int MODE, bool PUSH = false>
 cudaError_t launch_rs_tma_t(const RSParams& r, const AdamParams& a, int grid, cudaStream_t s) {
-  using C = RsCfg<P, ADAM, MODE>;
-  const int smem = C::kStages * C::kStageBytes;
+  using C = RsCfg<P, ADAM, MODE, PUSH>;
+  const int smem = C::kStages * C::kStageBytes + C::kPushBytes;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e =
-        cudaFuncSetAttribute(rs_tma_kernel<P, ADAM, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(rs_tma_kernel<P, ADAM, MODE, PUSH>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  return launch_pdl(rs_tma_kernel<P, ADAM, MODE>, grid, 32 + C::kConsumers, smem, s, r, a);
+  return launch_pdl(rs_tma_kernel<P, ADAM, MODE, PUSH>, grid, C::kLead + C::kConsumers, smem, s, r, a);
 }
 
 // qgZ quantizer: 4 threads per 64-element block, each holding 4 float4s (elements
@@ -860,8 +970,19 @@ cudaError_t launch_qgz_quantize(const QuantParams& q, int grid, cudaStream_t s) 
 }
 
 template <int P>
-cudaError_t launch_rs_tma_p(const RSParams& r, const AdamParams* a, int grid, cudaStream_t s, int mode) {
+cudaError_t launch_rs_tma_p(const RSParams& r, const AdamParams* a, int grid, cudaStream_t s, int mode, bool push) {
   AdamParams none{};
+  if constexpr (P >= 2) {
+    if (push) {
+      switch (mode) {
+        case RS_F32: return a ? launch_rs_tma_t<P, true, RS_F32, true>(r, *a, grid, s) : launch_rs_tma_t<P, false, RS_F32, true>(r, none, grid, s);
+        case RS_BF16: return a ? launch_rs_tma_t<P, true, RS_BF16, true>(r, *a, grid, s) : launch_rs_tma_t<P, false, RS_BF16, true>(r, none, grid, s);
+        default: return cudaErrorInvalidValue;
+      }
+    }
+  } else {
+    if (push) return cudaErrorInvalidValue;
+  }
   switch (mode) {
     case RS_F32: return a ? launch_rs_tma_t<P, true, RS_F32>(r, *a, grid, s) : launch_rs_tma_t<P, false, RS_F32>(r, none, grid, s);
     case RS_BF16: return a ? launch_rs_tma_t<P, true, RS_BF16>(r, *a, grid, s) : launch_rs_tma_t<P, false, RS_BF16>(r, none, grid, s);
@@ -870,10 +991,13 @@ cudaError_t launch_rs_tma_p(const RSParams& r, const AdamParams* a, int grid, cu
   }
 }
 
-cudaError_t launch_rs_tma(const RSParams& r, const AdamParams* a, int world, int grid, cudaStream_t s, int mode) {
+int rs_push_chunk_elems(int world) { return rs_push_chunk(world); }
+
+cudaError_t launch_rs_tma(const RSParams& r, const AdamParams* a, int world, int grid, cudaStream_t s, int mode,
+                          bool push) {
   switch (world) {
 #define HPZ_RST_CASE(P) \
-  case P: return launch_rs_tma_p<P>(r, a, grid, s, mode);
+  case P: return launch_rs_tma_p<P>(r, a, grid, s, mode, push);
     HPZ_RST_CASE(1) HPZ_RST_CASE(2) HPZ_RST_CASE(3) HPZ_RST_CASE(4) HPZ_RST_CASE(5) HPZ_RST_CASE(6)
     HPZ_RST_CASE(7) HPZ_RST_CASE(8) HPZ_RST_CASE(9) HPZ_RST_CASE(10) HPZ_RST_CASE(11) HPZ_RST_CASE(12)
     HPZ_RST_CASE(13) HPZ_RST_CASE(14) HPZ_RST_CASE(15) HPZ_RST_CASE(16)

@@ -75,7 +75,10 @@ def sum_over_ranks(values: list[float], device=None) -> list[float]:
     return t.tolist()
 
 
-def _register(ctx, numels, dtype, align, n_grad_slots, qgz=False, grad_dtype="f32", qwz=False, landing_bufs=0):
+def _register(ctx, numels, dtype, align, n_grad_slots, qgz=False, grad_dtype="f32", qwz=False, landing_bufs=0,
+              rs_push=False):
+    if rs_push:
+        H.hpz_set_option(ctx, "rs_push", 1)    # sizes the arena (landing slots): before register
     if landing_bufs:
         H.hpz_set_option(ctx, "landing_bufs", landing_bufs)
     if qgz:
@@ -93,14 +96,15 @@ class EmulatedWorld:
     """P ranks on one GPU in one process (test harness for the multi-rank protocol)."""
 
     def __init__(self, numels, world, node_size, dtype="bf16", align=256, n_grad_slots=None,
-                 device=0, timeout_s=20.0, qgz=False, grad_dtype="f32", qwz=False, landing_bufs=0):
+                 device=0, timeout_s=20.0, qgz=False, grad_dtype="f32", qwz=False, landing_bufs=0,
+                 rs_push=False):
         self.world, self.node_size, self.dtype = world, node_size, dtype
         self.numels = list(numels)
         self.ranks: list[RankCtx] = []
         for r in range(world):
             ctx = H.hpz_init(world, node_size, r, device)
-            _register(ctx, self.numels, dtype, align, n_grad_slots, qgz, grad_dtype, qwz, landing_bufs)
-            if landing_bufs:
+            _register(ctx, self.numels, dtype, align, n_grad_slots, qgz, grad_dtype, qwz, landing_bufs, rs_push)
+            if landing_bufs or rs_push:
                 H.hpz_set_option(ctx, "split_phases", 1)   # ranks share one stream: phases by hand
             H.hpz_arena_alloc(ctx)
             H.hpz_set_timeout(ctx, timeout_s)
@@ -121,7 +125,8 @@ class DistWorld:
     """This process's single rank of a torch.distributed world (one GPU per process)."""
 
     def __init__(self, numels, node_size, dtype="bf16", align=256, n_grad_slots=None, device=None,
-                 group=None, timeout_s=20.0, qgz=False, grad_dtype="f32", qwz=False, landing_bufs=0):
+                 group=None, timeout_s=20.0, qgz=False, grad_dtype="f32", qwz=False, landing_bufs=0,
+                 rs_push=False):
         import torch.distributed as dist
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
@@ -131,7 +136,7 @@ class DistWorld:
         dev = torch.cuda.current_device() if device is None else device
         ctx = H.hpz_init(self.world, node_size, self.rank, dev)
         self.arena_bytes = _register(ctx, self.numels, dtype, align, n_grad_slots, qgz, grad_dtype, qwz,
-                                     landing_bufs)
+                                     landing_bufs, rs_push)
         handle = H.hpz_arena_alloc(ctx)
         H.hpz_set_timeout(ctx, timeout_s)
         virtual_nodes(self.world, node_size)         # validates the topology early

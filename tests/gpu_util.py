@@ -29,7 +29,7 @@ class ParityRun:
     def __init__(self, numels, world, node_size, dtype="bf16", align=256, order="fixed",
                  verify="exact", grad_kind="uniform", n_grad_slots=None, stock_schedule="program",
                  fused=False, store_grad_shard=True, copy_engine="tma", qgz=False, grad_dtype="f32",
-                 qwz=False, push=False, load_initial=True):
+                 qwz=False, push=False, load_initial=True, rs_push=False):
         from paper_2407_01614_b200 import hpz as H
         from paper_2407_01614_b200.world import EmulatedWorld
         self.H = H
@@ -39,7 +39,7 @@ class ParityRun:
         self.qgz, self.grad_dtype, self.qwz, self.push = qgz, grad_dtype, qwz, push
         self.w = EmulatedWorld(numels, world, node_size, dtype=dtype, align=align, n_grad_slots=n_grad_slots,
                                timeout_s=10.0, qgz=qgz, grad_dtype=grad_dtype, qwz=qwz,
-                               landing_bufs=len(numels) if push else 0)
+                               landing_bufs=len(numels) if push else 0, rs_push=rs_push)
         self.o = O.HpzOracle(self.numels, world, node_size, align=align, param_dtype=dtype,
                              order="fixed" if order == "paper" else order,
                              stock_schedule=stock_schedule, grad_kind=grad_kind, qgz=qgz, grad_dtype=grad_dtype,

@@ -36,6 +36,8 @@ def main():
     ap.add_argument("--grad-dtype", default="f32")
     ap.add_argument("--qwz", type=int, default=0)
     ap.add_argument("--push", type=int, default=0)
+    ap.add_argument("--rs-push", type=int, default=0)
+    ap.add_argument("--grad-slots", type=int, default=0)
     args = ap.parse_args()
     local = int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
@@ -46,7 +48,8 @@ def main():
     numels = [int(x) for x in args.numels.split(",")]
     P, r = dist.get_world_size(), dist.get_rank()
     W = DistWorld(numels, args.node_size, timeout_s=20.0, qgz=bool(args.qgz), grad_dtype=args.grad_dtype,
-                  qwz=bool(args.qwz), landing_bufs=len(numels) if args.push else 0)
+                  qwz=bool(args.qwz), landing_bufs=len(numels) if args.push else 0, rs_push=bool(args.rs_push),
+                  n_grad_slots=args.grad_slots or None)
     rc = W.ranks[0]
     s = torch.cuda.current_stream()
     H.hpz_set_order(rc.ctx, args.order, stock_delay_us=args.stock_delay_us, stock_poison=args.order == "stock")
