@@ -274,6 +274,7 @@ struct RsCfg {
   static constexpr int kPushStages = 8;
   static constexpr int kPushLag = 24;
   static constexpr int kPushBatch = 16;
+  static constexpr int kPushWarps = 1;   // 2 measured: N=2 28.9 vs 27.2 ms, N=4 33.9 vs 34.3
   static constexpr int kPushUnit = kChunk * kGradBytes;
   static constexpr int kPushBytes = PUSH ? kPushStages * kPushUnit : 0;
   static constexpr int kBudget = PUSH ? 216 * 1024 - kPushBytes : 200 * 1024;
@@ -281,7 +282,7 @@ struct RsCfg {
   // consumer threads: one float4 per thread per chunk, at most 16 warps (idle polling
   // warps would steal issue slots from the working ones)
   static constexpr int kConsumers = kChunk / 4 < kRsMaxConsumers ? kChunk / 4 : kRsMaxConsumers;
-  static constexpr int kLead = PUSH ? 64 : 32;   // producer warp (+ push warp)
+  static constexpr int kLead = PUSH ? 32 * (1 + kPushWarps) : 32;   // producer warp (+ push warps)
 };
 
 __device__ __forceinline__ void red_relaxed_sys_add(uint32_t* p, uint32_t v) {
@@ -332,17 +333,26 @@ __global__ void __launch_bounds__(RsCfg<P, ADAM, MODE, PUSH>::kLead + RsCfg<P, A
   }
   __syncthreads();
 
-  if (PUSH && warp == 1) {
-    // push warp: my gradient slot's slice of every chunk this CTA owns, for every other
+  if (PUSH && warp >= 1 && warp <= C::kPushWarps) {
+    // push warps: my gradient slot's slice of every chunk this CTA owns, for every other
     // owner q: local bulk load -> smem -> bulk store into q's landing slot; once the store
-    // is complete, q's chunk counter is incremented (release, system scope)
+    // is complete, q's chunk counter is incremented.  Push warp pw takes every
+    // kPushWarps-th unit with its own stage ring, so one can sit in a fence while the
+    // other keeps issuing.
     if (lane == 0 && r.push_on) {
+      constexpr int PW = C::kPushWarps;
+      constexpr int SP = C::kPushStages / PW;   // stages per push warp
+      constexpr int LAG = C::kPushLag / PW, BATCH = C::kPushBatch / PW;
+      const int pw = warp - 1;
       for (int q = 0; q < P; ++q)
         if (r.push_free[q] != nullptr) wait_geq(r.push_free[q], r.push_free_target, r.sync);
       fence_proxy_async();
-      char* ring = smem + (size_t)C::kStages * C::kStageBytes;
-      const int64_t nu = nk * (P - 1);
-      auto unit = [&](int64_t x, int& q, int64_t& w, uint32_t& bytes) {
+      char* ring = smem + (size_t)C::kStages * C::kStageBytes + (size_t)pw * SP * C::kPushUnit;
+      uint64_t* bar = push_bar + pw * SP;
+      const int64_t nu_all = nk * (P - 1);
+      const int64_t nu = nu_all > pw ? (nu_all - pw + PW - 1) / PW : 0;   // my units i -> x = i*PW + pw
+      auto unit = [&](int64_t i, int& q, int64_t& w, uint32_t& bytes) {
+        const int64_t x = i * PW + pw;
         const int64_t k = x / (P - 1);
         const int d = (int)(x % (P - 1));
         q = (r.self + 1 + (d + (int)(blockIdx.x % (P - 1))) % (P - 1)) % P;   // never self; rotated per CTA
@@ -350,50 +360,50 @@ __global__ void __launch_bounds__(RsCfg<P, ADAM, MODE, PUSH>::kLead + RsCfg<P, A
         const int64_t rem = n - w * C::kChunk;
         bytes = (uint32_t)((rem < C::kChunk ? rem : C::kChunk) * C::kGradBytes);
       };
-      auto issue = [&](int64_t x) {
+      auto issue = [&](int64_t i) {
         int q;
         int64_t w;
         uint32_t bytes;
-        unit(x, q, w, bytes);
-        const int s = (int)(x % C::kPushStages);
-        mbar_expect_tx(&push_bar[s], bytes);
+        unit(i, q, w, bytes);
+        const int s = (int)(i % SP);
+        mbar_expect_tx(&bar[s], bytes);
         tma_load(ring + (size_t)s * C::kPushUnit, r.push_src + q * r.push_shard_bytes + w * C::kChunk * C::kGradBytes,
-                 bytes, &push_bar[s]);
+                 bytes, &bar[s]);
       };
-      // Completed units are signalled in batches of kPushBatch: one system-scope fence
-      // (which drains this thread's outstanding writes: measured 63 ms/step at N=2 with a
-      // release per unit vs 28 ms batched) then relaxed remote increments.
-      int64_t sig_from = 0;   // units [sig_from, x] are complete but not yet signalled
-      auto signal_upto = [&](int64_t x) {
+      // Completed units are signalled in batches: one system-scope fence (it drains this
+      // thread's outstanding writes: measured 63 ms/step at N=2 with a release per unit vs
+      // 28 ms batched) then relaxed remote increments.
+      int64_t sig_from = 0;   // my units [sig_from, i] are complete but not yet signalled
+      auto signal_upto = [&](int64_t i) {
         fence_proxy_async();
         __threadfence_system();
-        for (int64_t y = sig_from; y <= x; ++y) {
+        for (int64_t y = sig_from; y <= i; ++y) {
           int q;
           int64_t w;
           uint32_t bytes;
           unit(y, q, w, bytes);
           red_relaxed_sys_add(r.push_ctr[q] + w, 1u);
         }
-        sig_from = x + 1;
+        sig_from = i + 1;
       };
-      constexpr int kAhead = C::kPushStages - 1;
-      for (int64_t x = 0; x < nu && x < kAhead; ++x) issue(x);
-      for (int64_t x = 0; x < nu; ++x) {
-        const int s = (int)(x % C::kPushStages);
-        mbar_wait(&push_bar[s], (uint32_t)((x / C::kPushStages) & 1));
+      constexpr int kAhead = SP - 1;
+      for (int64_t i = 0; i < nu && i < kAhead; ++i) issue(i);
+      for (int64_t i = 0; i < nu; ++i) {
+        const int s = (int)(i % SP);
+        mbar_wait(&bar[s], (uint32_t)((i / SP) & 1));
         int q;
         int64_t w;
         uint32_t bytes;
-        unit(x, q, w, bytes);
+        unit(i, q, w, bytes);
         tma_store(r.push_dst[q] + w * C::kChunk * C::kGradBytes, ring + (size_t)s * C::kPushUnit, bytes);
         bulk_commit();
-        if (x >= C::kPushLag && (x - C::kPushLag + 1) % C::kPushBatch == 0) {
-          bulk_wait<C::kPushLag>();   // units up to x - lag have landed in their owners' memory
-          signal_upto(x - C::kPushLag);
+        if (i >= LAG && (i - LAG + 1) % BATCH == 0) {
+          bulk_wait<LAG>();           // my units up to i - LAG have landed in their owners' memory
+          signal_upto(i - LAG);
         }
-        if (x + kAhead < nu) {
-          bulk_wait_read<1>();        // the stage of unit x - 1 has been read by its store
-          issue(x + kAhead);
+        if (i + kAhead < nu) {
+          bulk_wait_read<1>();        // the stage of unit i - 1 has been read by its store
+          issue(i + kAhead);
         }
       }
       bulk_wait_all();
