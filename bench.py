@@ -54,6 +54,9 @@ def parse():
                     help="forward gather: ranks pull (default) or owners push into arena landing buffers")
     ap.add_argument("--rs", default="pull", choices=["pull", "push"],
                     help="reduce-scatter: owners pull slices (default) or ranks push them into owners' landing slots")
+    ap.add_argument("--overlap-bwd", type=int, default=0,
+                    help="run each layer's backward gather on a second stream, capped at this many CTAs, "
+                         "beside the previous layer's reduce-scatter (capped at the remaining SMs); 0 = one stream")
     ap.add_argument("--grad-dtype", default="f32", choices=["f32", "bf16"],
                     help="gradient slot dtype (bf16: SURVEY f4, fp32 accumulation)")
     ap.add_argument("--grad-slots", type=int, default=0,
@@ -214,6 +217,11 @@ def main():
         H.hpz_set_option(ctx, "ctas_per_sm", args.ctas_per_sm)
     H.hpz_set_option(ctx, "copy_engine", H.COPY[args.copy_engine])
     stream = torch.cuda.current_stream()
+    gstream = torch.cuda.Stream(device=dev) if args.overlap_bwd else stream   # backward gathers
+    if args.overlap_bwd:
+        n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
+        H.hpz_set_option(ctx, "bwd_ctas", args.overlap_bwd)
+        H.hpz_set_option(ctx, "rs_ctas", n_sm - args.overlap_bwd)
     infos = rc.infos
     # resident inputs: initial params (device generator) and this rank's gradients
     for i in range(L):
@@ -227,7 +235,9 @@ def main():
         fwd_buf = device_view(H.hpz_landing_buffer(ctx, 0), nmax, dtype)
     else:
         fwd_buf = torch.empty(nmax, dtype=tdt, device=dev)     # caller-owned full buffers, reused
-    bwd_buf = torch.empty(nmax, dtype=tdt, device=dev)     # per layer (repartition)
+    # per layer (repartition); with --overlap-bwd the gathers run ahead of the
+    # reduce-scatters, so a small ring of buffers stands in for the backward compute's reads
+    bwd_bufs = [torch.empty(nmax, dtype=tdt, device=dev) for _ in range(2 if args.overlap_bwd else 1)]
     adam = H.make_adam()
     torch.cuda.synchronize()
 
@@ -243,10 +253,10 @@ def main():
         uploaded into every layer's gradient slot (end-to-end arm): the uploads run on a
         copy stream from the start of the step, in backward order, each reduce-scatter
         waiting only for its own layer's upload."""
-        def rec(k):
+        def rec(k, st=None):
             if ev is not None:
                 x = torch.cuda.Event(enable_timing=True)
-                x.record(stream)
+                x.record(stream if st is None else st)
                 ev[k].append(x)
         up = {}
         if grads_from is not None:
@@ -259,10 +269,20 @@ def main():
             rec("fwd0")
             H.hpz_fwd_gather(ctx, i, fwd_buf.data_ptr(), stream)
             rec("fwd1")
+        if gstream is not stream:
+            gstream.wait_stream(stream)
+        rs_done = {}
         for i in reversed(range(L)):
-            rec("bwd0")
-            H.hpz_bwd_gather(ctx, i, bwd_buf.data_ptr(), stream)
-            rec("bwd1")
+            if gstream is not stream and i + len(bwd_bufs) in rs_done:
+                # buffer reuse: layer i+2's backward (here: its reduce-scatter) is done with it
+                gstream.wait_event(rs_done[i + len(bwd_bufs)])
+            rec("bwd0", gstream)
+            H.hpz_bwd_gather(ctx, i, bwd_bufs[i % len(bwd_bufs)].data_ptr(), gstream)
+            rec("bwd1", gstream)
+            if gstream is not stream:      # the layer's gradient exists only after its bwd gather
+                done = torch.cuda.Event()
+                done.record(gstream)
+                stream.wait_event(done)
             if grads_from is not None:
                 stream.wait_event(up[i])
             elif n_slots < L:    # shared slots: this layer's gradient is produced in the step
@@ -279,6 +299,11 @@ def main():
             else:
                 H.hpz_reduce_scatter(ctx, i, stream)
             rec("rs1")
+            if gstream is not stream:
+                rs_done[i] = torch.cuda.Event()
+                rs_done[i].record(stream)
+        if gstream is not stream:
+            stream.wait_stream(gstream)
         if not fused:
             for i in range(L):
                 rec("adam0")
@@ -437,6 +462,8 @@ def main():
                        "parallelism": f"hpZ dp{world} (P={world}, P'={node_size})", "order": args.order,
                        "verify": args.verify, "copy_engine": args.copy_engine, "fwd_gather": args.gather,
                        "reduce_scatter": args.rs if world > 1 else "local",
+                       "overlap_bwd": (f"backward gathers on a second stream ({args.overlap_bwd} CTAs) beside "
+                                       f"the reduce-scatters") if args.overlap_bwd else None,
                        "qgz": "int4 blockwise (64) gradient all-to-all; RS bytes counted as the fp32 "
                               "gradient bytes reduced, wire bytes 0.625 B/elem" if args.qgz else None,
                        "grad_dtype": args.grad_dtype, "grad_slots": n_slots,

@@ -321,7 +321,7 @@ typedef enum {
                                     caller (hpz_fwd_gather_post / _finish) — needed when several
                                     ranks share one GPU stream (single-GPU emulation); with
                                     HPZ_OPT_RS_PUSH, hpz_grads_ready runs the push phase */
-  HPZ_OPT_RS_PUSH = 9            /* 0 (default) or 1, P >= 2, fp32 or bf16 gradients (not qgZ):
+  HPZ_OPT_RS_PUSH = 9,           /* 0 (default) or 1, P >= 2, fp32 or bf16 gradients (not qgZ):
                                     owner-driven reduce-scatter.  Every rank bulk-stores the
                                     slices of its gradient slot into the owners' landing slots
                                     over NVLink (posted writes, one chunk counter per 2048 or
@@ -331,6 +331,11 @@ typedef enum {
                                     does both (a push warp beside the reduce pipeline); two
                                     landing slots of P x max-shard gradient elements are added
                                     to the arena.  Set before hpz_register_flat_params. */
+  HPZ_OPT_BWD_CTAS = 10,         /* CTA cap of the backward gathers (0 = none) and ... */
+  HPZ_OPT_RS_CTAS = 11           /* ... of the reduce-scatters: with caps summing to at most the
+                                    SM count, a backward gather on one stream and a
+                                    reduce-scatter on another run side by side (no kernel of
+                                    either waits on the other, so they may share the GPU) */
 } hpz_option;
 /* Copy engine of the gathers and the reduce-scatter: TMA 1-D bulk copies through a
  * shared-memory stage ring (cp.async.bulk, one persistent CTA per SM), or 16-byte

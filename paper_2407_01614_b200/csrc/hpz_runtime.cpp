@@ -71,6 +71,7 @@ struct hpz_ctx {
   int grad_bytes = 4;                     // f4: 2 = bf16 gradients (fp32 accumulation)
   int qwz_bits = 0;                       // f2: 8 = INT8 blockwise weights in the forward gather
   int max_ctas = 0;                       // cap on every grid (0 = all SMs)
+  int bwd_ctas = 0, rs_ctas = 0;          // caps of the backward gathers / reduce-scatters (overlap)
   int n_land = 0;                         // library-owned landing buffers (push forward gather)
   bool split_phases = false;              // push gather: caller issues post / finish itself
   std::vector<uint64_t> off_land, land_use;
@@ -166,9 +167,10 @@ int check_layer(hpz_ctx* c, int layer) {
   return HPZ_OK;
 }
 
-int grid_for(const hpz_ctx* c, int64_t work_items, int per_sm) {
+int grid_for(const hpz_ctx* c, int64_t work_items, int per_sm, int cap = 0) {
   int64_t g = (int64_t)c->sm_count * per_sm;
   if (c->max_ctas > 0 && g > c->max_ctas) g = c->max_ctas;   // leave SMs to overlapped compute
+  if (cap > 0 && g > cap) g = cap;                            // per-collective cap (overlap)
   if (work_items < g) g = work_items;
   return g < 1 ? 1 : (int)g;
 }
@@ -177,25 +179,25 @@ uint32_t epoch(int64_t x) { return (uint32_t)x; }
 
 // Pick the gather kernel: TMA bulk pipeline (one CTA/SM) or the LDG/STG kernel (EXACT
 // verification, or when selected with HPZ_OPT_COPY_ENGINE).
-cudaError_t gather_launch(const hpz_ctx* c, const GatherParams& p, cudaStream_t s) {
+cudaError_t gather_launch(const hpz_ctx* c, const GatherParams& p, cudaStream_t s, int cap = 0) {
   if (c->copy_engine == HPZ_COPY_TMA && p.mism == nullptr) {
     const int64_t chunks = (p.src_bytes + 32767) / 32768 * p.n_src;
-    return launch_gather_tma(p, grid_for(c, chunks, 1), s);
+    return launch_gather_tma(p, grid_for(c, chunks, 1, cap), s);
   }
   const int64_t tiles = (p.src_bytes / 16 + 2047) / 2048 * p.n_src;
-  return launch_gather(p, grid_for(c, tiles, c->ctas_per_sm), s);
+  return launch_gather(p, grid_for(c, tiles, c->ctas_per_sm, cap > 0 ? cap * c->ctas_per_sm : 0), s);
 }
 
 cudaError_t rs_launch(const hpz_ctx* c, const RSParams& r, const AdamParams* a, cudaStream_t s) {
   if (c->rs_push) {
     const int64_t ch = rs_push_chunk_elems(c->world);
-    return launch_rs_tma(r, a, c->world, grid_for(c, (r.n_vec * 4 + ch - 1) / ch, 1), s, c->grad_bytes == 2 ? 1 : 0, true);
+    return launch_rs_tma(r, a, c->world, grid_for(c, (r.n_vec * 4 + ch - 1) / ch, 1, c->rs_ctas), s, c->grad_bytes == 2 ? 1 : 0, true);
   }
   if (c->qgz_bits || c->grad_bytes == 2)   // qgZ codes / bf16 gradients: TMA engine only
-    return launch_rs_tma(r, a, c->world, grid_for(c, (r.n_vec * 4 + 1023) / 1024, 1), s, c->qgz_bits ? 2 : 1);
+    return launch_rs_tma(r, a, c->world, grid_for(c, (r.n_vec * 4 + 1023) / 1024, 1, c->rs_ctas), s, c->qgz_bits ? 2 : 1);
   if (c->copy_engine == HPZ_COPY_TMA)
-    return launch_rs_tma(r, a, c->world, grid_for(c, (r.n_vec * 4 + 1023) / 1024, 1), s);
-  const int grid = grid_for(c, (r.n_vec + 511) / 512, c->ctas_per_sm);
+    return launch_rs_tma(r, a, c->world, grid_for(c, (r.n_vec * 4 + 1023) / 1024, 1, c->rs_ctas), s);
+  const int grid = grid_for(c, (r.n_vec + 511) / 512, c->ctas_per_sm, c->rs_ctas > 0 ? c->rs_ctas * c->ctas_per_sm : 0);
   return a ? launch_rs_adam(r, *a, c->world, grid, s) : launch_reduce_scatter(r, c->world, grid, s);
 }
 
@@ -943,7 +945,7 @@ int hpz_bwd_gather(hpz_ctx* c, int layer, void* full_out, void* stream) {
       c->launches += 1;
     }
   }
-  cudaError_t e = gather_launch(c, p, s);
+  cudaError_t e = gather_launch(c, p, s, c->bwd_ctas);
   if (e != cudaSuccess) return fail(c, HPZ_ECUDA, "bwd gather launch: %s", cudaGetErrorString(e));
   c->launches += 1;
   L.bwd_t = c->t;
@@ -1290,6 +1292,11 @@ int hpz_set_option(hpz_ctx* c, int option, int64_t value) {
       if (value != HPZ_F32 && value != HPZ_BF16) return fail(c, HPZ_EINVAL, "gradient dtype must be HPZ_F32 or HPZ_BF16");
       if (value == HPZ_BF16 && c->qgz_bits) return fail(c, HPZ_EINVAL, "qgZ quantizes fp32 gradients");
       c->grad_bytes = value == HPZ_BF16 ? 2 : 4;
+      return HPZ_OK;
+    case HPZ_OPT_BWD_CTAS:
+    case HPZ_OPT_RS_CTAS:
+      if (value < 0 || value > 1 << 20) return fail(c, HPZ_EINVAL, "CTA caps must be >= 0");
+      (option == HPZ_OPT_BWD_CTAS ? c->bwd_ctas : c->rs_ctas) = (int)value;
       return HPZ_OK;
     case HPZ_OPT_RS_PUSH:
       if (c->registered) return fail(c, HPZ_ESTATE, "the push reduce-scatter must be chosen before hpz_register_flat_params");

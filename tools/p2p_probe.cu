@@ -146,14 +146,21 @@ int main(int argc, char** argv) {
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
   const bool pull = strstr(mode, "pull") != nullptr;
   const bool tma = strstr(mode, "tma") != nullptr;
-  cudaStream_t st[kMaxG];
-  cudaEvent_t e0[kMaxG], e1[kMaxG];
-  Ptrs P[kMaxG];
+  // pull_mix / push_mix: a TMA kernel (1 CTA/SM) moves the first `mix_pct`% of every peer
+  // buffer while an LDG/STG kernel (ctas_per_sm CTAs/SM) moves the rest, concurrently on two
+  // streams: does mixing the two request paths exceed either alone?
+  const bool mix = strstr(mode, "mix") != nullptr;
+  const int mix_pct = argc > 7 ? atoi(argv[7]) : 50;
+  cudaStream_t st[kMaxG], st2[kMaxG];
+  cudaEvent_t e0[kMaxG], e1[kMaxG], e2[kMaxG];
+  Ptrs P[kMaxG], PA[kMaxG], PB[kMaxG];
   for (int g = 0; g < G; ++g) {
     CK(cudaSetDevice(g));
     CK(cudaStreamCreateWithFlags(&st[g], cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&st2[g], cudaStreamNonBlocking));
     CK(cudaEventCreate(&e0[g]));
     CK(cudaEventCreate(&e1[g]));
+    CK(cudaEventCreate(&e2[g]));
     Ptrs& p = P[g];
     p.n = 0;
     p.bytes = bytes;
@@ -168,16 +175,33 @@ int main(int argc, char** argv) {
       }
       p.n++;
     }
-    if (tma) {
+    if (tma || mix) {
       int smem = 4 * chunk;
       CK(cudaFuncSetAttribute(copy_tma<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    }
+    if (mix) {   // split every peer buffer: [0, a) by TMA, [a, bytes) by LDG/STG
+      const int64_t a = (bytes * mix_pct / 100) / 4096 * 4096;
+      PA[g] = p;
+      PB[g] = p;
+      PA[g].bytes = a;
+      PB[g].bytes = bytes - a;
+      for (int k = 0; k < p.n; ++k) {
+        PB[g].src[k] = p.src[k] + a;
+        PB[g].dst[k] = p.dst[k] + a;
+      }
     }
   }
   for (int it = 0; it < 4; ++it) {
     for (int g = 0; g < G; ++g) {
       CK(cudaSetDevice(g));
       CK(cudaEventRecord(e0[g], st[g]));
-      if (tma)
+      if (mix) {
+        CK(cudaStreamWaitEvent(st2[g], e0[g], 0));
+        copy_tma<4><<<sms, 32, 4 * chunk, st[g]>>>(PA[g], chunk);
+        copy_ldg<8><<<sms * ctas_per_sm, 256, 0, st2[g]>>>(PB[g]);
+        CK(cudaEventRecord(e2[g], st2[g]));
+        CK(cudaStreamWaitEvent(st[g], e2[g], 0));
+      } else if (tma)
         copy_tma<4><<<sms * ctas_per_sm, 32, 4 * chunk, st[g]>>>(P[g], chunk);
       else
         copy_ldg<8><<<sms * ctas_per_sm, 256, 0, st[g]>>>(P[g]);
