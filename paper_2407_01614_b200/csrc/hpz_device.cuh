@@ -130,5 +130,34 @@ __device__ __forceinline__ int quant_code(float v, float mn, float scale, float 
   return c < 0 ? 0 : (c > maxc ? maxc : c);
 }
 
+// quant_code for N elements of one block at once, same results element by element: the
+// fast quotient for all N, one (rarely taken) branch that recomputes the elements near a
+// tie with the IEEE division — instead of a divergent branch per element, which measured
+// ~38 issued instructions per element in the qgZ quantizer (ncu: issue-bound at 77%).
+template <int N>
+__device__ __forceinline__ void quant_codes(const float (&e)[N], float mn, float scale, float rcp, int maxc,
+                                            float tie_eps, int (&c)[N]) {
+  float q[N];
+  bool near = false;
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    q[k] = __fmul_rn(__fsub_rn(e[k], mn), rcp);
+    const float fr = __fsub_rn(q[k], floorf(q[k]));
+    near |= !(fabsf(__fsub_rn(fr, 0.5f)) >= tie_eps);
+  }
+  if (near) {
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      const float fr = __fsub_rn(q[k], floorf(q[k]));
+      if (!(fabsf(__fsub_rn(fr, 0.5f)) >= tie_eps)) q[k] = __fdiv_rn(__fsub_rn(e[k], mn), scale);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    const int ci = __float2int_rn(q[k]);
+    c[k] = ci < 0 ? 0 : (ci > maxc ? maxc : ci);
+  }
+}
+
 }  // namespace
 }  // namespace hpz

@@ -1003,7 +1003,7 @@ static int qgz_quantize(hpz_ctx* c, int layer, cudaStream_t s) {
     q.war.target = epoch(c->slot_use[slot]);
   }
   q.sync = c->sync();
-  cudaError_t e = launch_qgz_quantize(q, grid_for(c, (L.numel_pad / kQgzBlock + 63) / 64, 8), s);
+  cudaError_t e = launch_qgz_quantize(q, grid_for(c, (L.numel_pad / kQgzBlock + 63) / 64, 4), s);   // 4 resident CTAs/SM: one wave
   if (e != cudaSuccess) return fail(c, HPZ_ECUDA, "qgZ quantize launch: %s", cudaGetErrorString(e));
   c->launches += 1;
   return HPZ_OK;

@@ -577,7 +577,7 @@ cudaError_t launch_rs_tma_t(const RSParams& r, const AdamParams& a, int grid, cu
 // anywhere in a block makes its (min, scale) NaN so it surfaces after dequantization.
 // fp32, one IEEE op per operator, round-half-even codes — the oracle's
 // quantize_blockwise decisions, bit for bit.
-__global__ void __launch_bounds__(256) qgz_quantize_kernel(const __grid_constant__ QuantParams q) {
+__global__ void __launch_bounds__(256, 4) qgz_quantize_kernel(const __grid_constant__ QuantParams q) {
   if (threadIdx.x == 0 && q.war.n) wait_all(q.war, q.sync);   // E6: peers done with the old codes
   __syncthreads();
   const int64_t n_blocks = q.n / kQgzBlock;
@@ -611,17 +611,19 @@ __global__ void __launch_bounds__(256) qgz_quantize_kernel(const __grid_constant
     }
     const bool pos = scale > 0.0f;
     const float rcp = pos ? __frcp_rn(scale) : 0.0f;
+    const float e[16] = {v[0].x, v[0].y, v[0].z, v[0].w, v[1].x, v[1].y, v[1].z, v[1].w,
+                         v[2].x, v[2].y, v[2].z, v[2].w, v[3].x, v[3].y, v[3].z, v[3].w};
+    int c[16];
+    if (pos) {
+      quant_codes<16>(e, mn, scale, rcp, 15, 0x1p-17f, c);
+    } else {
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const float e[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
-      uint32_t packed = 0;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int c = pos ? quant_code(e[k], mn, scale, rcp, 15, 0x1p-17f) : 0;
-        packed |= (uint32_t)c << (4 * k);
-      }
-      c16[b * 16 + sub + 4 * u] = (uint16_t)packed;
+      for (int k = 0; k < 16; ++k) c[k] = 0;
     }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      c16[b * 16 + sub + 4 * u] =
+          (uint16_t)(c[4 * u] | (c[4 * u + 1] << 4) | (c[4 * u + 2] << 8) | (c[4 * u + 3] << 12));
     if (sub == 0) q.params[b] = make_float2(mn, scale);
   }
 }
@@ -779,11 +781,11 @@ __global__ void __launch_bounds__(256) qwz_quantize_kernel(const __grid_constant
     uint32_t lo = 0, hi = 0;
     const bool pos = scale > 0.0f;
     const float rcp = pos ? __frcp_rn(scale) : 0.0f;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const int c = pos ? quant_code(v[k], mn, scale, rcp, 255, 0x1p-13f) : 0;
-      if (k < 4) lo |= (uint32_t)c << (8 * k);
-      else hi |= (uint32_t)c << (8 * (k - 4));
+    if (pos) {
+      int c[8];
+      quant_codes<8>(v, mn, scale, rcp, 255, 0x1p-13f, c);
+      lo = (uint32_t)c[0] | ((uint32_t)c[1] << 8) | ((uint32_t)c[2] << 16) | ((uint32_t)c[3] << 24);
+      hi = (uint32_t)c[4] | ((uint32_t)c[5] << 8) | ((uint32_t)c[6] << 16) | ((uint32_t)c[7] << 24);
     }
     reinterpret_cast<uint2*>(q.codes)[b * 32 + lane] = make_uint2(lo, hi);
     if (lane == 0) q.params[b] = make_float2(mn, scale);
