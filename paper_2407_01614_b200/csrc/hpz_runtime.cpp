@@ -216,7 +216,7 @@ int qwz_quantize(hpz_ctx* c, int layer, uint32_t value, cudaStream_t s) {
   for (int j = 0; j < c->world; ++j) q.rel.ptr[q.rel.n++] = c->flag(j, F_PRIM_READY, layer, c->rank);
   q.rel.value = value;
   q.sync = c->sync();
-  cudaError_t e = launch_qwz_quantize(q, grid_for(c, (L.shard / kQwzBlock + 7) / 8, 8), s);
+  cudaError_t e = launch_qwz_quantize(q, grid_for(c, (L.shard / kQwzBlock + 31) / 32, 4), s);   // one wave of 4 CTAs/SM, 8 warps x 4 blocks per CTA step
   if (e != cudaSuccess) return fail(c, HPZ_ECUDA, "qwZ quantize launch: %s", cudaGetErrorString(e));
   c->launches += 1;
   return HPZ_OK;

@@ -341,6 +341,7 @@ __global__ void __launch_bounds__(RsCfg<P, ADAM, MODE, PUSH>::kLead + RsCfg<P, A
     // other keeps issuing.
     if (lane == 0 && r.push_on) {
       constexpr int PW = C::kPushWarps;
+      constexpr int PM1 = P > 1 ? P - 1 : 1;   // push instantiations have P >= 2
       constexpr int SP = C::kPushStages / PW;   // stages per push warp
       constexpr int LAG = C::kPushLag / PW, BATCH = C::kPushBatch / PW;
       const int pw = warp - 1;
@@ -349,13 +350,13 @@ __global__ void __launch_bounds__(RsCfg<P, ADAM, MODE, PUSH>::kLead + RsCfg<P, A
       fence_proxy_async();
       char* ring = smem + (size_t)C::kStages * C::kStageBytes + (size_t)pw * SP * C::kPushUnit;
       uint64_t* bar = push_bar + pw * SP;
-      const int64_t nu_all = nk * (P - 1);
+      const int64_t nu_all = nk * PM1;
       const int64_t nu = nu_all > pw ? (nu_all - pw + PW - 1) / PW : 0;   // my units i -> x = i*PW + pw
       auto unit = [&](int64_t i, int& q, int64_t& w, uint32_t& bytes) {
         const int64_t x = i * PW + pw;
-        const int64_t k = x / (P - 1);
-        const int d = (int)(x % (P - 1));
-        q = (r.self + 1 + (d + (int)(blockIdx.x % (P - 1))) % (P - 1)) % P;   // never self; rotated per CTA
+        const int64_t k = x / PM1;
+        const int d = (int)(x % PM1);
+        q = (r.self + 1 + (d + (int)(blockIdx.x % PM1)) % PM1) % P;   // never self; rotated per CTA
         w = blockIdx.x + k * gridDim.x;                                       // global chunk index
         const int64_t rem = n - w * C::kChunk;
         bytes = (uint32_t)((rem < C::kChunk ? rem : C::kChunk) * C::kGradBytes);
@@ -739,56 +740,68 @@ __global__ void __launch_bounds__(32 * (1 + kFpWarps), 1) push_gather_kernel(con
 // elements to fp32, the warp reduces min/max/NaN, and the block's codes are
 // round-half-even((v - min) / scale) with scale = (max - min) / 255 — the oracle's
 // quantize_blockwise(bits=8, block=256), bit for bit.  The last CTA releases E1.
-__global__ void __launch_bounds__(256) qwz_quantize_kernel(const __grid_constant__ QwzQuantParams q) {
+__global__ void __launch_bounds__(256, 4) qwz_quantize_kernel(const __grid_constant__ QwzQuantParams q) {
+  constexpr int U = 4;   // blocks per warp step: their loads are all in flight before any is used
   const int lane = threadIdx.x & 31;
   const int64_t n_blocks = q.n / kQwzBlock;
   const int64_t warp_id = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
   const int64_t n_warps = (int64_t)gridDim.x * (blockDim.x / 32);
-  for (int64_t b = warp_id; b < n_blocks; b += n_warps) {
-    float v[8];
-    if (q.prim_bf16) {
-      const uint4 w = reinterpret_cast<const uint4*>(q.prim)[b * 32 + lane];
-      const uint32_t u[4] = {w.x, w.y, w.z, w.w};
+  for (int64_t b0 = warp_id * U; b0 < n_blocks; b0 += n_warps * U) {
+    float v[U][8];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        v[2 * k] = __uint_as_float(u[k] << 16);
-        v[2 * k + 1] = __uint_as_float(u[k] & 0xFFFF0000u);
+    for (int u = 0; u < U; ++u) {
+      const int64_t b = b0 + u;
+      if (b >= n_blocks) break;
+      if (q.prim_bf16) {
+        const uint4 w = reinterpret_cast<const uint4*>(q.prim)[b * 32 + lane];
+        const uint32_t x[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          v[u][2 * k] = __uint_as_float(x[k] << 16);
+          v[u][2 * k + 1] = __uint_as_float(x[k] & 0xFFFF0000u);
+        }
+      } else {
+        const float4 a = reinterpret_cast<const float4*>(q.prim)[(b * 32 + lane) * 2];
+        const float4 c = reinterpret_cast<const float4*>(q.prim)[(b * 32 + lane) * 2 + 1];
+        v[u][0] = a.x; v[u][1] = a.y; v[u][2] = a.z; v[u][3] = a.w;
+        v[u][4] = c.x; v[u][5] = c.y; v[u][6] = c.z; v[u][7] = c.w;
       }
-    } else {
-      const float4 a = reinterpret_cast<const float4*>(q.prim)[(b * 32 + lane) * 2];
-      const float4 c = reinterpret_cast<const float4*>(q.prim)[(b * 32 + lane) * 2 + 1];
-      v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = c.x; v[5] = c.y; v[6] = c.z; v[7] = c.w;
-    }
-    int nan = 0;
-    float mn = v[0], mx = v[0];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      nan |= isnan(v[k]);
-      mn = fminf(mn, v[k]);
-      mx = fmaxf(mx, v[k]);
     }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-      nan |= __shfl_xor_sync(0xffffffffu, nan, o);
+    for (int u = 0; u < U; ++u) {
+      const int64_t b = b0 + u;
+      if (b >= n_blocks) break;
+      int nan = 0;
+      float mn = v[u][0], mx = v[u][0];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        nan |= isnan(v[u][k]);
+        mn = fminf(mn, v[u][k]);
+        mx = fmaxf(mx, v[u][k]);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        nan |= __shfl_xor_sync(0xffffffffu, nan, o);
+      }
+      float scale = __fdiv_rn(__fsub_rn(mx, mn), 255.0f);
+      if (nan) {
+        mn = __int_as_float(0x7fc00000);
+        scale = mn;
+      }
+      uint32_t lo = 0, hi = 0;
+      const bool pos = scale > 0.0f;
+      const float rcp = pos ? __frcp_rn(scale) : 0.0f;
+      if (pos) {
+        int c[8];
+        quant_codes<8>(v[u], mn, scale, rcp, 255, 0x1p-13f, c);
+        lo = (uint32_t)c[0] | ((uint32_t)c[1] << 8) | ((uint32_t)c[2] << 16) | ((uint32_t)c[3] << 24);
+        hi = (uint32_t)c[4] | ((uint32_t)c[5] << 8) | ((uint32_t)c[6] << 16) | ((uint32_t)c[7] << 24);
+      }
+      reinterpret_cast<uint2*>(q.codes)[b * 32 + lane] = make_uint2(lo, hi);
+      if (lane == 0) q.params[b] = make_float2(mn, scale);
     }
-    float scale = __fdiv_rn(__fsub_rn(mx, mn), 255.0f);
-    if (nan) {
-      mn = __int_as_float(0x7fc00000);
-      scale = mn;
-    }
-    uint32_t lo = 0, hi = 0;
-    const bool pos = scale > 0.0f;
-    const float rcp = pos ? __frcp_rn(scale) : 0.0f;
-    if (pos) {
-      int c[8];
-      quant_codes<8>(v, mn, scale, rcp, 255, 0x1p-13f, c);
-      lo = (uint32_t)c[0] | ((uint32_t)c[1] << 8) | ((uint32_t)c[2] << 16) | ((uint32_t)c[3] << 24);
-      hi = (uint32_t)c[4] | ((uint32_t)c[5] << 8) | ((uint32_t)c[6] << 16) | ((uint32_t)c[7] << 24);
-    }
-    reinterpret_cast<uint2*>(q.codes)[b * 32 + lane] = make_uint2(lo, hi);
-    if (lane == 0) q.params[b] = make_float2(mn, scale);
   }
   if (last_cta(q.done_ctr)) release_all(q.rel);   // E1: codes of step t+1 are ready
 }
@@ -797,9 +810,18 @@ __global__ void __launch_bounds__(256) qwz_quantize_kernel(const __grid_constant
 // and (min, scale) pairs (256 B); 8 consumer warps dequantize 8 elements per thread-step
 // (fp32 min + code*scale, then the parameter dtype), store 16-byte words to the full
 // buffer and — fused secondary store — to the secondary, and fingerprint them.
-constexpr int kQwChunk = 8192;
-constexpr int kQwStages = 4;
-constexpr int kQwConsumers = 256;
+#ifndef HPZ_QW_CHUNK
+#define HPZ_QW_CHUNK 16384   // 16 KiB of codes x 4 stages, 16 consumer warps: fwd qwZ gather
+#endif                       // 7.2 vs 7.6 ms/step (N=2) for 8 KiB / 8 warps
+#ifndef HPZ_QW_STAGES
+#define HPZ_QW_STAGES 4
+#endif
+#ifndef HPZ_QW_CONSUMERS
+#define HPZ_QW_CONSUMERS 512
+#endif
+constexpr int kQwChunk = HPZ_QW_CHUNK;
+constexpr int kQwStages = HPZ_QW_STAGES;
+constexpr int kQwConsumers = HPZ_QW_CONSUMERS;
 __global__ void __launch_bounds__(32 + kQwConsumers, 1) gather_qwz_kernel(const __grid_constant__ GatherParams p) {
   extern __shared__ __align__(1024) char smem[];
   __shared__ __align__(8) uint64_t full_bar[kQwStages];

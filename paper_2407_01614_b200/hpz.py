@@ -10,7 +10,8 @@ import os
 from ctypes import POINTER, byref, c_char_p, c_double, c_float, c_int, c_int64, c_uint64, c_void_p
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libhpz.so")
+# HPZ_LIB: another in-tree build of the same sources (A/B experiments, abtest_*/libhpz.so)
+LIB_PATH = os.environ.get("HPZ_LIB") or os.path.join(_HERE, "libhpz.so")
 
 HPZ_OK, HPZ_EINVAL, HPZ_ESTATE, HPZ_ECUDA, HPZ_ETIMEOUT, HPZ_ENOMEM = 0, -1, -2, -3, -4, -5
 HPZ_F32, HPZ_BF16 = 0, 1
