@@ -293,7 +293,8 @@ typedef enum {
                                     every rank's codes of its shard (0.625 B/elem instead of
                                     4), dequantizes (min + code*scale) and reduces in the R7
                                     order.  Set BEFORE hpz_register_flat_params (it sizes the
-                                    arena).  With qgZ, hpz_grads_ready also quantizes. */
+                                    arena); needs align_elems % 256 == 0.  With qgZ,
+                                    hpz_grads_ready also quantizes. */
   HPZ_OPT_GRAD_DTYPE = 4,        /* HPZ_F32 (default) or HPZ_BF16: gradient slots hold
                                     bf16; the reduce-scatter converts (exactly) to fp32 and
                                     reduces in fp32 in the R7 order — half the NVLink bytes.

@@ -320,6 +320,8 @@ int hpz_register_flat_params(hpz_ctx* c, int n_layers, const int64_t* numel, int
   if (n_grad_slots < 1 || n_grad_slots > n_layers) return fail(c, HPZ_EINVAL, "n_grad_slots must be in [1, n_layers]");
   if (c->qwz_bits && align_elems % kQwzBlock)
     return fail(c, HPZ_EINVAL, "qwZ needs align_elems to be a multiple of 256 (whole quantization blocks per shard)");
+  if (c->qgz_bits && align_elems % 256)   // whole 64-blocks per shard, 16-byte bulk copies of their params
+    return fail(c, HPZ_EINVAL, "qgZ needs align_elems to be a multiple of 256");
   c->dtype = param_dtype;
   c->elem = elem;
   c->align = align_elems;

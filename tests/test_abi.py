@@ -188,3 +188,16 @@ def test_rs_push_option_sizes_arena(H):
     # bf16 gradient slots: the landing slots hold bf16 too
     assert sizes[(8, 1, "bf16")] < sizes[(8, 1, "f32")]
     assert sizes[(1, 1, "f32")] == sizes[(1, 0, "f32")]
+
+
+def test_quantized_options_need_block_aligned_shards(H):
+    for opt, val in (("qgz", 4), ("qwz", 8)):
+        ctx = H.hpz_init(4, 2, 0, -1)
+        try:
+            H.hpz_set_option(ctx, opt, val)
+            with pytest.raises(H.HpzError) as e:
+                H.hpz_register_flat_params(ctx, [100_000], 1, 64)
+            assert e.value.code == H.HPZ_EINVAL
+            H.hpz_register_flat_params(ctx, [100_000], 1, 256)
+        finally:
+            H.hpz_finalize(ctx)
