@@ -83,3 +83,38 @@ def test_multiproc_parity_rs_push(n, node, extra):
     if n > NGPU:
         pytest.skip(f"needs {n} GPUs")
     _run(n, node, extra=("--rs-push", "1", *extra), port=30411 + n * 10 + node + 3 * len(extra))
+
+
+def _mp_draw(seed):
+    import numpy as np
+    rng = np.random.default_rng(2000 + seed)
+    n = int(rng.choice([2, 4]))
+    node = int(rng.choice([d for d in (1, 2, 4) if d <= n and n % d == 0]))
+    quant = str(rng.choice(["none", "qgz", "qwz", "both"]))
+    qgz, qwz = quant in ("qgz", "both"), quant in ("qwz", "both")
+    order = "fixed" if qwz else str(rng.choice(["fixed", "paper", "off"]))
+    engine = str(rng.choice(["tma", "ldg"]))
+    verify = "exact" if engine == "ldg" and not qwz and rng.random() < 0.5 else "fingerprint"
+    numels = [int(x) for x in rng.integers(1, 400_000, 3)]
+    extra = ["--engine", engine, "--verify", verify, "--fused", str(int(rng.random() < 0.6)),
+             "--numels", ",".join(map(str, numels)), "--grad-slots", str(int(rng.integers(1, 4)))]
+    if qgz:
+        extra += ["--qgz", "1"]
+    elif rng.random() < 0.3:
+        extra += ["--grad-dtype", "bf16"]
+    if qwz:
+        extra += ["--qwz", "1"]
+    if order == "fixed" and not qwz and rng.random() < 0.3:
+        extra += ["--push", "1"]
+    if not qgz and rng.random() < 0.4:
+        extra += ["--rs-push", "1"]
+    return n, node, order, extra
+
+
+@pytest.mark.parametrize("case", range(8))
+def test_multiproc_fuzz_option_combinations(case):
+    """Seeded random option combinations over real NVLink P2P (one process per GPU)."""
+    n, node, order, extra = _mp_draw(case)
+    if n > NGPU:
+        pytest.skip(f"needs {n} GPUs")
+    _run(n, node, order=order, extra=tuple(extra), port=30611 + case)
