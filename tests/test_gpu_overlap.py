@@ -61,3 +61,41 @@ def test_prefetch_depth_does_not_change_results():
 def test_stock_ordering_diverges():
     ls, _, c = _train("stock", steps=4)
     assert any(not math.isfinite(v) for v in ls)
+
+
+def _train_tf(order, steps=5, h=256, L=3, B=2, S=128, f=512, heads=4):
+    from paper_2407_01614_b200 import hpz as H
+    from paper_2407_01614_b200.overlap import PrefetchTrainer, block_numel
+    from paper_2407_01614_b200.world import EmulatedWorld
+    from synth import inputs as S_
+    w = EmulatedWorld([block_numel(h, f)] * L, 1, 1, grad_dtype="bf16", timeout_s=10.0)
+    try:
+        rc = w.ranks[0]
+        H.hpz_set_order(rc.ctx, order, stock_delay_us=5000 if order == "stock" else 0,
+                        stock_poison=order == "stock")
+        H.hpz_set_option(rc.ctx, "max_ctas", 16)
+        s = torch.cuda.current_stream()
+        for i in range(L):
+            H.hpz_synth_master(rc.ctx, i, S_.stream_key(S_.SEED_PARAMS, i, 0, 0), 2.0 ** -5, s)
+        g = torch.Generator(device="cuda").manual_seed(7)
+        x = (torch.randn(B, S, h, device="cuda", generator=g) * 0.5).to(torch.bfloat16)
+        y = (x.float() * 0.05).to(torch.bfloat16)
+        tr = PrefetchTrainer(rc, h, L, B * S, depth=1, model="transformer", ffn=f, n_heads=heads, lr=1e-4)
+        losses = [float(tr.step(x, y)) for _ in range(steps)]
+        torch.cuda.synchronize()
+        return losses, H.hpz_counters(rc.ctx)
+    finally:
+        w.close()
+
+
+def test_transformer_blocks_train_and_stock_diverges():
+    """f3 with pre-norm transformer blocks (SDPA attention + GELU MLP, activation
+    checkpointing): fixed and off agree (to attention-kernel rounding), the loss falls,
+    the stock ordering with a poisoned delayed secondary goes NaN."""
+    lf, cf = _train_tf("fixed")
+    lo, _ = _train_tf("off")
+    assert all(math.isfinite(v) for v in lf) and lf[-1] < lf[0], lf
+    assert all(abs(a - b) <= 1e-3 * abs(b) for a, b in zip(lf, lo)), (lf, lo)
+    assert cf["timeouts"] == 0 and cf["fp_mismatches"] == 0
+    ls, _ = _train_tf("stock", steps=3)
+    assert any(not math.isfinite(v) for v in ls), ls

@@ -27,7 +27,9 @@ def run(order, depth, args, world, rank, local, node_size):
     from paper_2407_01614_b200.overlap import PrefetchTrainer
     from paper_2407_01614_b200.world import DistWorld, EmulatedWorld, max_over_ranks
     from synth import inputs as S
-    numels = [args.h * args.h] * args.layers
+    from paper_2407_01614_b200.overlap import block_numel
+    per_layer = args.h * args.h if args.model == "mlp" else block_numel(args.h, args.ffn)
+    numels = [per_layer] * args.layers
     kw = dict(n_grad_slots=len(numels), timeout_s=60.0, grad_dtype="bf16")
     W = DistWorld(numels, node_size, device=local, **kw) if world > 1 else EmulatedWorld(numels, 1, 1, device=local, **kw)
     rc = W.ranks[0]
@@ -40,9 +42,11 @@ def run(order, depth, args, world, rank, local, node_size):
     for i in range(args.layers):
         H.hpz_synth_master(rc.ctx, i, S.stream_key(S.SEED_PARAMS, i, 0, 0), args.init_scale, s)
     g = torch.Generator(device="cuda").manual_seed(1234 + rank)
-    x = (torch.randn(args.tokens, args.h, device="cuda", generator=g) * 0.5).to(torch.bfloat16)
+    shape = (args.tokens, args.h) if args.model == "mlp" else (args.tokens // args.seq, args.seq, args.h)
+    x = (torch.randn(*shape, device="cuda", generator=g) * 0.5).to(torch.bfloat16)
     y = (x.float() * 0.05).to(torch.bfloat16)     # learnable target: a scaled copy of the input
-    tr = PrefetchTrainer(rc, args.h, args.layers, args.tokens, depth=depth, lr=args.lr)
+    tr = PrefetchTrainer(rc, args.h, args.layers, args.tokens, depth=depth, lr=args.lr, model=args.model,
+                         ffn=args.ffn, n_heads=args.heads)
     torch.cuda.synchronize()
     losses = []
     for _ in range(args.warmup):
@@ -72,6 +76,10 @@ def run(order, depth, args, world, rank, local, node_size):
 
 def main():
     ap = argparse.ArgumentParser()
+    ap.add_argument("--model", default="mlp", choices=["mlp", "transformer"])
+    ap.add_argument("--ffn", type=int, default=5632, help="transformer MLP width")
+    ap.add_argument("--heads", type=int, default=16)
+    ap.add_argument("--seq", type=int, default=1024, help="transformer sequence length (tokens = batch x seq)")
     ap.add_argument("--h", type=int, default=4096)
     ap.add_argument("--layers", type=int, default=8)
     ap.add_argument("--tokens", type=int, default=2048)
@@ -98,8 +106,11 @@ def main():
         res.append(run(order, int(depth), args, world, rank, local, node_size))
     if rank == 0:
         by = {f"{r['order']}:{r['prefetch_depth']}": r for r in res}
-        out = {"experiment": "f3 Table 1/2 analog: toy ReLU net, bf16 GEMMs + hpZ collectives on a comm stream",
-               "world": world, "node_size": node_size, "h": args.h, "layers": args.layers,
+        what = ("toy ReLU net" if args.model == "mlp" else
+                f"pre-norm transformer blocks (h {args.h}, {args.heads} heads, GELU MLP {args.ffn}, seq {args.seq}, "
+                f"activation checkpointing)")
+        out = {"experiment": f"f3 Table 1/2 analog: {what}, bf16 compute + hpZ collectives on a comm stream",
+               "model": args.model, "world": world, "node_size": node_size, "h": args.h, "layers": args.layers,
                "tokens_per_rank": args.tokens, "max_ctas": args.max_ctas, "runs": res}
         if "fixed:1" in by and "off:1" in by:
             out["fixed_vs_off_loss_identical"] = by["fixed:1"]["loss_last"] == by["off:1"]["loss_last"]
