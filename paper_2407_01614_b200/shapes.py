@@ -44,6 +44,7 @@ MODELS = {
     "llama2_13b": _llama(5120, 13824, 40),                    # 13,015,864,320 (C3)
     "falcon40b": _falcon40b(),                                # 41,303,293,952 (C4)
     "falcon40b_block": [_falcon40b()[1]],                     # one decoder block, per-layer timing (C4)
+    "falcon7b_block": [_falcon7b()[1]],                       # one C2 decoder block (ncu captures of the bench's launches)
     "llama2_70b_layers": [_llama(8192, 28672, 1, kv_heads=8, heads=64)[1]] * 4,   # 4 x 855,654,400 (C5)
 }
 
