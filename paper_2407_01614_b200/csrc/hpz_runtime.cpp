@@ -867,6 +867,10 @@ int hpz_fwd_gather(hpz_ctx* c, int layer, void* full_out, void* stream) {
       if (e != cudaSuccess) return fail(c, HPZ_ECUDA, "release launch: %s", cudaGetErrorString(e));
       c->launches += 1;
       HPZ_CUDA(c, cudaEventRecord(c->copy_ev[layer], c->side));
+      // the copy reads the caller's full buffer: later work on the caller's stream (e.g. the
+      // next gather into the same buffer) must not overwrite it first — the stream-side
+      // equivalent of the caching allocator's record_stream on L_i
+      HPZ_CUDA(c, cudaStreamWaitEvent(s, c->copy_ev[layer], 0));
     }
   }
   L.fwd_t = c->t;

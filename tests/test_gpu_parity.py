@@ -476,3 +476,57 @@ def test_order_switch_between_steps():
         assert run.counters()["timeouts"] == 0
     finally:
         run.close()
+
+
+def test_paper_order_with_one_reused_full_buffer():
+    """ORDER_PAPER's MemcpyD2D reads the caller's full buffer on a side
+    stream.  A caller that reuses one full buffer for every layer (the bench; a prefetch
+    ring) must never let the next layer's gather overwrite it before the copy has read it
+    (regression: the secondary received the next layer's parameters and the backward
+    gather read them).  A 3 ms delay before each copy widens the window; EXACT verification
+    compares every backward-gathered element with the owners' primaries."""
+    from paper_2407_01614_b200 import hpz as H
+    from paper_2407_01614_b200.world import EmulatedWorld, buffer_view, run_step
+    numels = [300_007, 250_000, 65_536]
+    P, Pp = 4, 2
+    w = EmulatedWorld(numels, P, Pp, timeout_s=10.0)
+    o = O.HpzOracle(numels, P, Pp, align=256, order="fixed")
+    try:
+        s = torch.cuda.current_stream()
+        for rc in w.ranks:
+            H.hpz_set_order(rc.ctx, "paper", stock_delay_us=3000)
+            H.hpz_set_verify(rc.ctx, "exact")
+        for i, n in enumerate(numels):
+            w0 = torch.from_numpy(S.layer_params(i, n)).cuda()
+            for rc in w.ranks:
+                H.hpz_load_master(rc.ctx, i, w0.data_ptr(), s)
+        nmax = max(x.numel_pad for x in w.ranks[0].infos)
+        fwd = [torch.empty(nmax, dtype=torch.bfloat16, device="cuda") for _ in range(P)]   # one per rank, all layers
+        bwd = [torch.empty(nmax, dtype=torch.bfloat16, device="cuda") for _ in range(P)]
+        keep = []
+        t_box = [0]
+
+        def grad_fn(rc, i):
+            g = torch.from_numpy(S.layer_grads(i, t_box[0], rc.rank, numels[i])).cuda()
+            keep.append(g)
+            H.hpz_grad_upload(rc.ctx, i, g.data_ptr(), numels[i], s)
+
+        adam = H.make_adam()
+        for t in range(3):
+            t_box[0] = t
+            run_step(w.ranks, [lambda i, r=r: fwd[r].data_ptr() for r in range(P)],
+                     [lambda i, r=r: bwd[r].data_ptr() for r in range(P)], adam, stream=s, grad_fn=grad_fn,
+                     emulated=True, fused=True)
+            torch.cuda.synchronize()
+            o.step()
+        tot = {}
+        for rc in w.ranks:
+            for k, v in H.hpz_counters(rc.ctx).items():
+                tot[k] = tot.get(k, 0) + v
+        assert tot["mismatches"] == 0 and tot["nan_reads"] == 0 and tot["timeouts"] == 0, tot
+        for i in range(len(numels)):
+            for rc in w.ranks:
+                got = buffer_view(rc, i, "master", "f32").cpu().numpy()
+                assert np.array_equal(got.view(np.uint32), o.state[i][rc.rank].master.view(np.uint32)), (i, rc.rank)
+    finally:
+        w.close()
