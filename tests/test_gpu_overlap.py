@@ -26,6 +26,7 @@ def _train(order, steps=6, depth=1, h=512, L=4, T=256):
         H.hpz_set_order(rc.ctx, order, stock_delay_us=5000 if order == "stock" else 0,
                         stock_poison=order == "stock")
         H.hpz_set_option(rc.ctx, "max_ctas", 16)
+        H.hpz_set_verify(rc.ctx, "fingerprint")
         s = torch.cuda.current_stream()
         for i in range(L):
             H.hpz_synth_master(rc.ctx, i, S.stream_key(S.SEED_PARAMS, i, 0, 0), 2.0 ** -5, s)
@@ -48,7 +49,7 @@ def test_fixed_equals_off_and_trains():
     assert lf == lo
     assert all(torch.equal(a.view(torch.int32), b.view(torch.int32)) for a, b in zip(mf, mo))
     assert lf[-1] < lf[0] and all(math.isfinite(v) for v in lf)
-    assert cf["timeouts"] == 0
+    assert cf["timeouts"] == 0 and cf["fp_mismatches"] == 0
 
 
 def test_prefetch_depth_does_not_change_results():
@@ -59,8 +60,10 @@ def test_prefetch_depth_does_not_change_results():
 
 
 def test_stock_ordering_diverges():
+    """Which stale secondary the backward reads is a hardware race: the poisoned one (NaN
+    loss) or the previous step's (finite but wrong, caught by the fingerprints)."""
     ls, _, c = _train("stock", steps=4)
-    assert any(not math.isfinite(v) for v in ls)
+    assert any(not math.isfinite(v) for v in ls) or c["fp_mismatches"] > 0, (ls, c)
 
 
 def _train_tf(order, steps=5, h=256, L=3, B=2, S=128, f=512, heads=4):
@@ -74,6 +77,7 @@ def _train_tf(order, steps=5, h=256, L=3, B=2, S=128, f=512, heads=4):
         H.hpz_set_order(rc.ctx, order, stock_delay_us=5000 if order == "stock" else 0,
                         stock_poison=order == "stock")
         H.hpz_set_option(rc.ctx, "max_ctas", 16)
+        H.hpz_set_verify(rc.ctx, "fingerprint")
         s = torch.cuda.current_stream()
         for i in range(L):
             H.hpz_synth_master(rc.ctx, i, S_.stream_key(S_.SEED_PARAMS, i, 0, 0), 2.0 ** -5, s)
@@ -97,5 +101,5 @@ def test_transformer_blocks_train_and_stock_diverges():
     assert all(math.isfinite(v) for v in lf) and lf[-1] < lf[0], lf
     assert all(abs(a - b) <= 1e-3 * abs(b) for a, b in zip(lf, lo)), (lf, lo)
     assert cf["timeouts"] == 0 and cf["fp_mismatches"] == 0
-    ls, _ = _train_tf("stock", steps=3)
-    assert any(not math.isfinite(v) for v in ls), ls
+    ls, cs = _train_tf("stock", steps=3)
+    assert any(not math.isfinite(v) for v in ls) or cs["fp_mismatches"] > 0, (ls, cs)
