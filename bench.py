@@ -402,6 +402,27 @@ def main():
                 "alg_bytes_per_step": alg, "launches_per_step": L, "ms_per_step": round(share[dom], 4),
                 "share_of_step": round(share[dom] / max(fwd_ms + bwd_ms + rs_ms + adam_ms + q_ms + g_ms, 1e-9), 4)}
 
+    # per-kernel table (north_star: per-step gather / reduce-scatter time, NVLink GB/s
+    # against 900 per direction, HBM GB/s against the measured copy peak); algorithmic bytes
+    # per rank and step: NVLink ingress as above; HBM = every byte each kernel must read or
+    # write in this GPU's memory (incl. the shards it serves to peers)
+    shard_sum = sum(x.shard for x in infos)
+    hbm_k = {"fwd_gather": ag_bytes + ag_bytes + ag_bytes / Pp,       # serve primary; write out + secondary
+             "bwd_gather": ag_bytes + ag_bytes,                       # serve secondary; write out
+             rs_name: rs_bytes + (shard_sum * (28 + e) if fused else shard_sum * 4)}
+    nv_k = {"fwd_gather": fwd_wire * (P - 1) / P, "bwd_gather": ag_bytes * (Pp - 1) / Pp,
+            rs_name: rs_wire * (P - 1) / P}
+    kernels = {}
+    for k, ms in (("fwd_gather", fwd_ms), ("bwd_gather", bwd_ms), (rs_name, rs_ms)):
+        if ms <= 0:
+            continue
+        nv = nv_k[k] / (ms * 1e-3) / 1e9
+        hb = hbm_k[k] / (ms * 1e-3) / 1e9
+        kernels[k] = {"ms_per_step": round(ms, 3), "nvlink_GB": round(nv_k[k] / 1e9, 3), "nvlink_GBps": round(nv, 1),
+                      "nvlink_frac_of_770": round(nv / 770.0, 4), "nvlink_frac_of_900": round(nv / 900.0, 4),
+                      "hbm_GB": round(hbm_k[k] / 1e9, 3), "hbm_GBps": round(hb, 1),
+                      "hbm_frac_of_measured": round(hb / hbm_peak, 4)}
+
     # ------------------------------------------------ end-to-end arm (host buffers)
     e2e = None
     if not args.no_e2e and args.e2e_steps > 0:
@@ -486,7 +507,7 @@ def main():
             "nvlink_ingress_GBps_per_gpu": round(ingress / (step_ms * 1e-3) / 1e9, 2) if world > 1 else None,
             "nvlink_frac_of_900": round(ingress / (step_ms * 1e-3) / 1e9 / 900, 4) if world > 1 else None,
             "collectives_only_GBps": round(world * coll_bytes / (coll_ms * 1e-3) / 1e9, 2),
-            "roofline": roofline,
+            "roofline": roofline, "kernels": kernels,
             "cpu_baseline": cpu,
             "nccl_baseline": nccl,
             "e2e": e2e,
