@@ -409,7 +409,9 @@ def main():
     shard_sum = sum(x.shard for x in infos)
     hbm_k = {"fwd_gather": ag_bytes + ag_bytes + ag_bytes / Pp,       # serve primary; write out + secondary
              "bwd_gather": ag_bytes + ag_bytes,                       # serve secondary; write out
-             rs_name: rs_bytes + (shard_sum * (28 + e) if fused else shard_sum * 4)}
+             # RS: my slot is read once in total (by its owners); fused Adam: w, m, v read +
+             # written (24 B) and the primary refreshed (e); unfused: the fp32 shard written
+             rs_name: rs_bytes + (shard_sum * (24 + e) if fused else shard_sum * 4)}
     nv_k = {"fwd_gather": fwd_wire * (P - 1) / P, "bwd_gather": ag_bytes * (Pp - 1) / Pp,
             rs_name: rs_wire * (P - 1) / P}
     kernels = {}
