@@ -7,9 +7,15 @@
 //   * gather_tma_kernel: producer bulk-loads a 32 KiB chunk of source j, then bulk-stores
 //     the same smem stage to the full buffer and (fused secondary store, a2) to the
 //     secondary; optional fingerprint consumer warps read the stage (a7).
-//   * rs_tma_kernel<P, ADAM>: producer bulk-loads the P peers' gradient slices of a
-//     chunk (+ the master/m/v chunk when ADAM); 256 consumer threads sum in the fixed
-//     pairwise-by-rank order (R7) and apply Adam (R8) from smem, storing with STG.128.
+//   * rs_tma_kernel<P, ADAM, MODE, PUSH>: producer bulk-loads the P peers' gradient
+//     slices of a chunk (fp32 / bf16 / qgZ codes; + the master/m/v chunk when ADAM); up to
+//     512 consumer threads sum in the fixed pairwise-by-rank order (R7) and apply Adam (R8)
+//     from smem, storing with STG.128.  PUSH: a push warp bulk-stores this rank's slices
+//     into the owners' landing slots and the producer reduces from the local landing slot
+//     as per-chunk arrival counters complete (HPZ_OPT_RS_PUSH).
+//   * qgz_quantize_kernel / qwz_quantize_kernel / gather_qwz_kernel: the ZeRO++ qgZ / qwZ
+//     blockwise quantizers and the dequantizing forward gather (f1, f2).
+//   * push_gather_kernel: owner-driven forward gather into landing buffers.
 // Flags are acquired by the producer before the first bulk read of a source; a
 // fence.proxy.async orders the generic-proxy acquire before the async-proxy reads, and
 // the bulk stores are drained (wait_group 0) and proxy-fenced before the grid-wide
