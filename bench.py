@@ -389,7 +389,10 @@ def main():
         else:
             bound, peak, unit = "nvlink", 770.0, "GB/s"
     achieved = alg / (share[dom] * 1e-3) / 1e9          # per-launch bytes / per-launch time, summed over L launches
-    traffic = traffic_alg = traffic_src = None
+    traffic = traffic_alg = None
+    traffic_src = None if world == 1 else (
+        "not captured: ncu replays a kernel ~40 times, which a kernel waiting on peer GPUs' flags cannot "
+        "survive (single-GPU captures only); see the N=1 capture and profiles/README.md")
     tr = ncu_traffic().get(f"P{world}_{dom}")
     if tr and not (args.qgz or args.qwz or args.grad_dtype != "f32"):
         # DRAM bytes of ONE captured launch (ncu --set full) next to that launch's algorithmic bytes
