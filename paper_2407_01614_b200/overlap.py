@@ -82,7 +82,7 @@ class PrefetchTrainer:
 
     def __init__(self, rc, h: int, L: int, tokens: int, depth: int = 1, n_bufs: int = 3,
                  comm_stream=None, compute_stream=None, lr: float = 1e-3, model: str = "mlp",
-                 ffn: int | None = None, n_heads: int = 16):
+                 ffn: int | None = None, n_heads: int = 16, grad_dtype: str = "bf16"):
         self.rc, self.ctx, self.h, self.L, self.T = rc, rc.ctx, h, L, tokens
         self.depth = depth
         self.model, self.f, self.n_heads = model, ffn or 4 * h, n_heads
@@ -95,11 +95,13 @@ class PrefetchTrainer:
         npad = max(x.numel_pad for x in rc.infos)
         self.ring = GatherRing(max(n_bufs, depth + 2), npad, torch.bfloat16, dev)
         self.adam = H.make_adam(lr=lr)
-        # gradient slots: bf16 (f4), zero once (padding must stay zero)
+        # gradient slots: bf16 (f4) or fp32 (qgZ quantizes fp32 gradients), zeroed once
+        # (padding must stay zero)
+        self.grad_dtype = grad_dtype
         self.gslots = []
         for i in range(L):
             ptr, n = H.hpz_buffer(self.ctx, i, "grad_slot")
-            v = device_view(ptr, n, "bf16")
+            v = device_view(ptr, n, grad_dtype)
             v.zero_()
             self.gslots.append(v)
         self.k = 0          # gather sequence number (ring position)
@@ -165,7 +167,10 @@ class PrefetchTrainer:
                 dz = dh if i == L - 1 else dh * (pre[i] > 0).to(dh.dtype)
                 slot = H.hpz_grad_buffer(self.ctx, i, self.comp)               # E6 on the compute stream
                 dW = self.gslots[i][: self.h * self.h].view(self.h, self.h)
-                torch.matmul(dz.t(), acts[i], out=dW)                           # L_i.backward() -> grad slot
+                if self.grad_dtype == "bf16":
+                    torch.matmul(dz.t(), acts[i], out=dW)                       # L_i.backward() -> grad slot
+                else:
+                    dW.copy_(dz.t() @ acts[i])
                 dh = dz @ W                                                      # uses the bwd-gathered W_i
                 self._release(b)
                 assert slot == self.gslots[i].data_ptr()

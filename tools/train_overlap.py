@@ -30,7 +30,8 @@ def run(order, depth, args, world, rank, local, node_size):
     from paper_2407_01614_b200.overlap import block_numel
     per_layer = args.h * args.h if args.model == "mlp" else block_numel(args.h, args.ffn)
     numels = [per_layer] * args.layers
-    kw = dict(n_grad_slots=len(numels), timeout_s=60.0, grad_dtype="bf16")
+    # qgZ (the paper's Table 2 runs every hpZ variant with qgZ) quantizes fp32 gradients
+    kw = dict(n_grad_slots=len(numels), timeout_s=60.0, grad_dtype="f32" if args.qgz else "bf16", qgz=args.qgz)
     W = DistWorld(numels, node_size, device=local, **kw) if world > 1 else EmulatedWorld(numels, 1, 1, device=local, **kw)
     rc = W.ranks[0]
     H.hpz_set_order(rc.ctx, order, stock_delay_us=args.stock_delay_us if order == "stock" else 0,
@@ -46,7 +47,7 @@ def run(order, depth, args, world, rank, local, node_size):
     x = (torch.randn(*shape, device="cuda", generator=g) * 0.5).to(torch.bfloat16)
     y = (x.float() * 0.05).to(torch.bfloat16)     # learnable target: a scaled copy of the input
     tr = PrefetchTrainer(rc, args.h, args.layers, args.tokens, depth=depth, lr=args.lr, model=args.model,
-                         ffn=args.ffn, n_heads=args.heads)
+                         ffn=args.ffn, n_heads=args.heads, grad_dtype="f32" if args.qgz else "bf16")
     torch.cuda.synchronize()
     losses = []
     for _ in range(args.warmup):
@@ -77,6 +78,7 @@ def run(order, depth, args, world, rank, local, node_size):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--model", default="mlp", choices=["mlp", "transformer"])
+    ap.add_argument("--qgz", action="store_true", help="INT4 gradient all-to-all (fp32 gradient slots)")
     ap.add_argument("--ffn", type=int, default=5632, help="transformer MLP width")
     ap.add_argument("--heads", type=int, default=16)
     ap.add_argument("--seq", type=int, default=1024, help="transformer sequence length (tokens = batch x seq)")
@@ -110,7 +112,8 @@ def main():
                 f"pre-norm transformer blocks (h {args.h}, {args.heads} heads, GELU MLP {args.ffn}, seq {args.seq}, "
                 f"activation checkpointing)")
         out = {"experiment": f"f3 Table 1/2 analog: {what}, bf16 compute + hpZ collectives on a comm stream",
-               "model": args.model, "world": world, "node_size": node_size, "h": args.h, "layers": args.layers,
+               "model": args.model, "qgz": args.qgz, "world": world, "node_size": node_size, "h": args.h,
+               "layers": args.layers,
                "tokens_per_rank": args.tokens, "max_ctas": args.max_ctas, "runs": res}
         if "fixed:1" in by and "off:1" in by:
             out["fixed_vs_off_loss_identical"] = by["fixed:1"]["loss_last"] == by["off:1"]["loss_last"]
