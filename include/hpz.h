@@ -193,10 +193,12 @@ HPZ_API int hpz_version(void);
 
 /* ---- configuration ------------------------------------------------------------------ */
 
-/* Ordering scheme (see hpz_order); stock_delay_us delays the stock secondary copy on
- * its side stream, stock_poison != 0 fills the secondary with quiet NaNs first
+/* Ordering scheme (see hpz_order); stock_delay_us delays the stock / paper secondary
+ * copy on its side stream, stock_poison != 0 fills the secondary with quiet NaNs first
  * (bf16 0x7FC0 / f32 0x7FC00000, reading R16).  Must be identical on all ranks and
- * changed only between steps. */
+ * changed only between steps (FIXED, PAPER and OFF may follow each other directly; after
+ * STOCK, whose side-stream copy is ordered with nothing by design, synchronize the device
+ * before the next step). */
 HPZ_API int hpz_set_order(hpz_ctx* ctx, int order, int stock_delay_us, int stock_poison);
 HPZ_API int hpz_set_verify(hpz_ctx* ctx, int mode);
 /* Device-side flag wait timeout in seconds (default 20). */
