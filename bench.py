@@ -63,6 +63,8 @@ def parse():
                     help="gradient slots (0 = one per layer, resident).  Fewer slots (large models) "
                          "regenerate each layer's gradient on the device inside the step (timed, "
                          "reported as grad_synth)")
+    ap.add_argument("--trace", default=None, help="write a JSONL op trace (one line per hpz_* call) of the "
+                    "instrumented breakdown steps to this file (per rank: FILE.rankR)")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -253,11 +255,13 @@ def main():
         uploaded into every layer's gradient slot (end-to-end arm): the uploads run on a
         copy stream from the start of the step, in backward order, each reduce-scatter
         waiting only for its own layer's upload."""
-        def rec(k, st=None):
+        def rec(k, st=None, layer=None):
             if ev is not None:
                 x = torch.cuda.Event(enable_timing=True)
                 x.record(stream if st is None else st)
                 ev[k].append(x)
+                if k.endswith("0"):
+                    ev["_layer_" + k[:-1]].append(layer)
         up = {}
         if grads_from is not None:
             copy_stream.wait_stream(stream)
@@ -266,7 +270,7 @@ def main():
                 up[i] = torch.cuda.Event()
                 up[i].record(copy_stream)
         for i in range(L):
-            rec("fwd0")
+            rec("fwd0", layer=i)
             H.hpz_fwd_gather(ctx, i, fwd_buf.data_ptr(), stream)
             rec("fwd1")
         if gstream is not stream:
@@ -276,7 +280,7 @@ def main():
             if gstream is not stream and i + len(bwd_bufs) in rs_done:
                 # buffer reuse: layer i+2's backward (here: its reduce-scatter) is done with it
                 gstream.wait_event(rs_done[i + len(bwd_bufs)])
-            rec("bwd0", gstream)
+            rec("bwd0", gstream, layer=i)
             H.hpz_bwd_gather(ctx, i, bwd_bufs[i % len(bwd_bufs)].data_ptr(), gstream)
             rec("bwd1", gstream)
             if gstream is not stream:      # the layer's gradient exists only after its bwd gather
@@ -286,14 +290,14 @@ def main():
             if grads_from is not None:
                 stream.wait_event(up[i])
             elif n_slots < L:    # shared slots: this layer's gradient is produced in the step
-                rec("g0")
+                rec("g0", layer=i)
                 H.hpz_synth_grads(ctx, i, S.stream_key(S.SEED_GRADS, i, 0, rank), S.GRAD_SCALE, 0, stream)
                 rec("g1")
             if args.qgz:
-                rec("q0")
+                rec("q0", layer=i)
                 H.hpz_grads_ready(ctx, i, stream)      # qgZ: INT4-quantize my slot, publish E5
                 rec("q1")
-            rec("rs0")
+            rec("rs0", layer=i)
             if fused:
                 H.hpz_reduce_scatter_adam(ctx, i, adam, stream)   # RS + this layer's Adam
             else:
@@ -306,7 +310,7 @@ def main():
             stream.wait_stream(gstream)
         if not fused:
             for i in range(L):
-                rec("adam0")
+                rec("adam0", layer=i)
                 H.hpz_step(ctx, i, adam, stream)
                 rec("adam1")
 
@@ -337,9 +341,26 @@ def main():
     # timed region; used for the breakdown and the roofline's per-kernel durations
     KB = max(1, min(K, 5))
     evs = {k: [] for k in ("fwd0", "fwd1", "bwd0", "bwd1", "rs0", "rs1", "adam0", "adam1", "q0", "q1", "g0", "g1")}
+    evs.update({"_layer_" + k: [] for k in ("fwd", "bwd", "rs", "adam", "q", "g")})
+    t_ref = torch.cuda.Event(enable_timing=True)
+    t_ref.record(stream)
     for _ in range(KB):
         one_step(evs)
     barrier()
+    if args.trace:
+        # JSONL op trace of the instrumented steps (one line per call; SURVEY §5 tracing)
+        names = {"fwd": "hpz_fwd_gather", "bwd": "hpz_bwd_gather", "rs": "hpz_reduce_scatter" + ("_adam" if fused else ""),
+                 "adam": "hpz_step", "q": "hpz_grads_ready(qgZ quantize)", "g": "hpz_synth_grads"}
+        recs = []
+        for k, nm in names.items():
+            per_step = len(evs[k + "0"]) // KB if evs[k + "0"] else 0
+            for idx, (a, b) in enumerate(zip(evs[k + "0"], evs[k + "1"])):
+                recs.append({"rank": rank, "step": idx // max(per_step, 1), "op": nm, "layer": evs["_layer_" + k][idx],
+                             "start_ms": round(t_ref.elapsed_time(a), 4), "dur_ms": round(a.elapsed_time(b), 4)})
+        recs.sort(key=lambda r: r["start_ms"])
+        with open(args.trace if world == 1 else f"{args.trace}.rank{rank}", "w") as f:
+            for r in recs:
+                f.write(json.dumps(r) + "\n")
     tot = {k: sum(a.elapsed_time(b) for a, b in zip(evs[k + "0"], evs[k + "1"])) / KB
            for k in ("fwd", "bwd", "rs", "adam", "q", "g")}
     # bytes per rank per step (algbw: AG output bytes, RS input bytes)
