@@ -335,10 +335,17 @@ typedef enum {
                                     landing slots of P x max-shard gradient elements are added
                                     to the arena.  Set before hpz_register_flat_params. */
   HPZ_OPT_BWD_CTAS = 10,         /* CTA cap of the backward gathers (0 = none) and ... */
-  HPZ_OPT_RS_CTAS = 11           /* ... of the reduce-scatters: with caps summing to at most the
+  HPZ_OPT_RS_CTAS = 11,          /* ... of the reduce-scatters: with caps summing to at most the
                                     SM count, a backward gather on one stream and a
                                     reduce-scatter on another run side by side (no kernel of
                                     either waits on the other, so they may share the GPU) */
+  HPZ_OPT_XNODE_MBPS = 12        /* 0 (default) or MB/s: emulate the paper's constrained
+                                    inter-node network (PAPER.md title, 147-151) on one NVSwitch
+                                    box — the TMA pull kernels pace their reads from ranks of
+                                    OTHER virtual nodes to this rate per GPU (forward gathers,
+                                    pull reduce-scatters, ORDER_OFF backward gathers; hpZ's
+                                    backward gathers stay inside the node).  Experiment knob
+                                    for the f3 / Table 2 analog; may change between steps. */
 } hpz_option;
 /* Copy engine of the gathers and the reduce-scatter: TMA 1-D bulk copies through a
  * shared-memory stage ring (cp.async.bulk, one persistent CTA per SM), or 16-byte

@@ -16,6 +16,10 @@ struct SyncCommon {
   uint32_t* abort_flag;                // local arena: set after the first timeout -> later waits skip
   unsigned long long* timeouts;        // local arena counter
   volatile uint32_t* host_err;         // host-mapped pinned word polled by the runtime
+  // emulated inter-node link (HPZ_OPT_XNODE_MBPS): reads from the sources set in
+  // xnode_mask (source index of the kernel) are paced to xnode_gbps per GPU (0: off)
+  float xnode_gbps;
+  uint32_t xnode_mask;
 };
 
 // A list of flags to release (st.release.sys of `value`), possibly in peer arenas.

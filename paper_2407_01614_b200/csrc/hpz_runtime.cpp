@@ -72,6 +72,7 @@ struct hpz_ctx {
   int qwz_bits = 0;                       // f2: 8 = INT8 blockwise weights in the forward gather
   int max_ctas = 0;                       // cap on every grid (0 = all SMs)
   int bwd_ctas = 0, rs_ctas = 0;          // caps of the backward gathers / reduce-scatters (overlap)
+  float xnode_gbps = 0.0f;                // emulated inter-node link per GPU (0: NVLink speed)
   int n_land = 0;                         // library-owned landing buffers (push forward gather)
   bool split_phases = false;              // push gather: caller issues post / finish itself
   std::vector<uint64_t> off_land, land_use;
@@ -128,7 +129,17 @@ struct hpz_ctx {
     s.abort_flag = reinterpret_cast<uint32_t*>(stat(5));
     s.timeouts = stat(4);
     s.host_err = host_err_dev;
+    s.xnode_gbps = xnode_gbps;
+    s.xnode_mask = 0;
     return s;
+  }
+  // emulated inter-node link: bit j set for every rank j on another virtual node
+  uint32_t xnode_mask() const {
+    if (xnode_gbps <= 0.0f) return 0;
+    uint32_t m = 0;
+    for (int j = 0; j < world; ++j)
+      if (j / node_size != rank / node_size) m |= 1u << j;
+    return m;
   }
   int node_first() const { return (rank / node_size) * node_size; }
   int local() const { return rank % node_size; }
@@ -813,6 +824,7 @@ int hpz_fwd_gather(hpz_ctx* c, int layer, void* full_out, void* stream) {
   for (int j = 0; j < c->world; ++j) p.rel.ptr[p.rel.n++] = c->flag(j, F_FWD_DONE, layer, c->rank);            // E2
   p.rel.value = t1;
   p.sync = c->sync();
+  p.sync.xnode_mask = c->xnode_mask();   // sources are the ranks
   cudaError_t e;
   if (c->qwz_bits) {
     // qwZ: pull every owner's INT8 codes + (min, scale) and dequantize (f2, R28)
@@ -939,6 +951,7 @@ int hpz_bwd_gather(hpz_ctx* c, int layer, void* full_out, void* stream) {
     for (int j = 0; j < c->world; ++j) p.rel.ptr[p.rel.n++] = c->flag(j, F_BWDP_DONE, layer, c->rank);
   p.rel.value = t1;
   p.sync = c->sync();
+  if (c->order == HPZ_ORDER_OFF) p.sync.xnode_mask = c->xnode_mask();   // ZeRO-3: every rank
   if (reads_prim) {
     // the primaries read here must still be W_t: they are, because Adam(t) waits for BWDP_DONE
     // and the sources' PRIMARY_READY >= t+1 is acquired per source (OFF) or below (EXACT)
@@ -1121,6 +1134,7 @@ static void build_rs(hpz_ctx* c, int layer, RSParams& p) {
   for (int j = 0; j < c->world; ++j) p.rel.ptr[p.rel.n++] = c->slot_flag(j, S_RS_DONE, slot, c->rank);   // E6
   p.rel.value = u1;
   p.sync = c->sync();
+  p.sync.xnode_mask = c->xnode_mask();   // src[j] = rank j
   if (c->qgz_bits) {
     for (int j = 0; j < c->world; ++j) {
       p.qcodes[j] = reinterpret_cast<const uint8_t*>(c->arena[j] + c->off_qcodes[slot]) + (int64_t)c->rank * L.shard / 2;
@@ -1303,6 +1317,10 @@ int hpz_set_option(hpz_ctx* c, int option, int64_t value) {
     case HPZ_OPT_RS_CTAS:
       if (value < 0 || value > 1 << 20) return fail(c, HPZ_EINVAL, "CTA caps must be >= 0");
       (option == HPZ_OPT_BWD_CTAS ? c->bwd_ctas : c->rs_ctas) = (int)value;
+      return HPZ_OK;
+    case HPZ_OPT_XNODE_MBPS:
+      if (value < 0 || value > 100000000) return fail(c, HPZ_EINVAL, "xnode_mbps must be in [0, 1e8]");
+      c->xnode_gbps = (float)value / 1000.0f;
       return HPZ_OK;
     case HPZ_OPT_RS_PUSH:
       if (c->registered) return fail(c, HPZ_ESTATE, "the push reduce-scatter must be chosen before hpz_register_flat_params");

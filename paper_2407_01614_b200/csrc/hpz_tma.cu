@@ -167,6 +167,21 @@ __global__ void __launch_bounds__(32 * (1 + kFpWarps), 1)
     if (lane == 0) {
       uint32_t waited = 0;
       bool war_done = false;
+      const uint64_t xt0 = p.sync.xnode_mask ? globaltimer() : 0;
+      uint64_t xbytes = 0;
+      float xns = 0.0f;   // ns per cross-node byte for this CTA (its share of the link)
+      if (p.sync.xnode_mask) {
+        uint64_t mine = 0;
+        for (int64_t k = 0; k < nk; ++k) {
+          int j;
+          int64_t off;
+          uint32_t bytes;
+          chunk_of(k, j, off, bytes);
+          if ((p.sync.xnode_mask >> j) & 1u) mine += bytes;
+        }
+        const float all = (float)p.src_bytes * (float)__popc(p.sync.xnode_mask & ((1u << n_src) - 1u));
+        xns = mine ? all / ((float)mine * p.sync.xnode_gbps) : 0.0f;
+      }
       auto issue_load = [&](int64_t k) {
         int j;
         int64_t off;
@@ -177,6 +192,7 @@ __global__ void __launch_bounds__(32 * (1 + kFpWarps), 1)
           fence_proxy_async();
           waited |= 1u << j;
         }
+        if ((p.sync.xnode_mask >> j) & 1u) xnode_pace(xt0, xbytes += bytes, xns);
         const int s = (int)(k % kGatherStages);
         mbar_expect_tx(&full_bar[s], bytes);
         tma_load(smem + (size_t)s * kGatherChunk, p.src[j] + off, bytes, &full_bar[s]);
@@ -422,6 +438,8 @@ __global__ void __launch_bounds__(RsCfg<P, ADAM, MODE, PUSH>::kLead + RsCfg<P, A
         if (ADAM) wait_all(a.wait, a.sync);   // E2 (+E7)
         fence_proxy_async();
       }
+      const uint64_t xt0 = r.sync.xnode_mask ? globaltimer() : 0;
+      uint64_t xbytes = 0;
       for (int64_t k = 0; k < nk; ++k) {
         const int s = (int)(k % C::kStages);
         if (k >= C::kStages) mbar_wait_bounded(&empty_bar[s], (uint32_t)(((k / C::kStages) - 1) & 1), r.sync);
@@ -438,6 +456,11 @@ __global__ void __launch_bounds__(RsCfg<P, ADAM, MODE, PUSH>::kLead + RsCfg<P, A
         const uint32_t bytes = cnt * 4;
         char* st = smem + (size_t)s * C::kStageBytes;
         const uint32_t src_bytes = QGZ ? cnt / 2 + cnt / kQgzBlock * 8 : (BF16 ? cnt * 2 : bytes);
+        if (r.sync.xnode_mask) {   // emulated inter-node link: pace the cross-node slices
+          xbytes += (uint64_t)src_bytes * __popc(r.sync.xnode_mask);
+          // chunks are dealt round-robin: every CTA carries ~1/gridDim.x of the bytes
+          xnode_pace(xt0, xbytes, (float)gridDim.x / r.sync.xnode_gbps);
+        }
         mbar_expect_tx(&full_bar[s], src_bytes * P + (ADAM ? 3 * bytes : 0));
 #pragma unroll
         for (int j = 0; j < P; ++j) {
@@ -859,6 +882,21 @@ __global__ void __launch_bounds__(32 + kQwConsumers, 1) gather_qwz_kernel(const 
   if (warp == 0) {
     if (lane == 0) {
       uint32_t waited = 0;
+      const uint64_t xt0 = p.sync.xnode_mask ? globaltimer() : 0;
+      uint64_t xbytes = 0;
+      float xns = 0.0f;   // ns per cross-node byte for this CTA (its share of the link)
+      if (p.sync.xnode_mask) {
+        uint64_t mine = 0;
+        for (int64_t k = 0; k < nk; ++k) {
+          int j;
+          int64_t off;
+          uint32_t cnt;
+          chunk_of(k, j, off, cnt);
+          if ((p.sync.xnode_mask >> j) & 1u) mine += cnt + cnt / kQwzBlock * 8;
+        }
+        const float all = (float)(n_el + n_el / kQwzBlock * 8) * (float)__popc(p.sync.xnode_mask & ((1u << n_src) - 1u));
+        xns = mine ? all / ((float)mine * p.sync.xnode_gbps) : 0.0f;
+      }
       for (int64_t k = 0; k < nk; ++k) {
         const int s = (int)(k % kQwStages);
         if (k >= kQwStages) mbar_wait_bounded(&empty_bar[s], (uint32_t)(((k / kQwStages) - 1) & 1), p.sync);
@@ -866,6 +904,7 @@ __global__ void __launch_bounds__(32 + kQwConsumers, 1) gather_qwz_kernel(const 
         int64_t off;
         uint32_t cnt;
         chunk_of(k, j, off, cnt);
+        if ((p.sync.xnode_mask >> j) & 1u) xnode_pace(xt0, xbytes += cnt + cnt / kQwzBlock * 8, xns);
         if (!((waited >> j) & 1u)) {
           if (p.src_flag[j] != nullptr) wait_geq(p.src_flag[j], p.src_target, p.sync);   // E1
           fence_proxy_async();

@@ -32,7 +32,7 @@ EXPORTED = [
     "hpz_landing_buffer", "hpz_fwd_gather_post", "hpz_fwd_gather_finish", "hpz_load_state",
 ]
 OPT = {"store_grad_shard": 0, "ctas_per_sm": 1, "copy_engine": 2, "qgz": 3, "grad_dtype": 4, "qwz": 5, "max_ctas": 6, "landing_bufs": 7, "split_phases": 8, "rs_push": 9,
-       "bwd_ctas": 10, "rs_ctas": 11}
+       "bwd_ctas": 10, "rs_ctas": 11, "xnode_mbps": 12}
 COPY = {"ldg": 0, "tma": 1}
 
 
