@@ -201,3 +201,21 @@ def test_quantized_options_need_block_aligned_shards(H):
             H.hpz_register_flat_params(ctx, [100_000], 1, 256)
         finally:
             H.hpz_finalize(ctx)
+
+
+def test_experiment_options_validation(H):
+    """Grid caps and the emulated inter-node link: accepted ranges, rejected values, and
+    they may change after registration (they size nothing)."""
+    ctx = H.hpz_init(4, 2, 1, -1)
+    try:
+        H.hpz_register_flat_params(ctx, [100_000], 1, 256)
+        for opt, good, bad in (("bwd_ctas", 48, -1), ("rs_ctas", 100, -5), ("xnode_mbps", 25_000, -1)):
+            H.hpz_set_option(ctx, opt, good)
+            H.hpz_set_option(ctx, opt, 0)
+            with pytest.raises(H.HpzError) as e:
+                H.hpz_set_option(ctx, opt, bad)
+            assert e.value.code == H.HPZ_EINVAL
+        with pytest.raises(H.HpzError):
+            H.hpz_set_option(ctx, "xnode_mbps", 10 ** 9)
+    finally:
+        H.hpz_finalize(ctx)
