@@ -50,10 +50,6 @@ def parse():
     ap.add_argument("--copy-engine", default="tma", choices=["tma", "ldg"])
     ap.add_argument("--qgz", action="store_true", help="ZeRO++ qgZ: INT4 gradient all-to-all (SURVEY f1)")
     ap.add_argument("--qwz", action="store_true", help="ZeRO++ qwZ: INT8 weights in the forward gather (SURVEY f2)")
-    ap.add_argument("--gather", default="pull", choices=["pull", "push"],
-                    help="forward gather: ranks pull (default) or owners push into arena landing buffers")
-    ap.add_argument("--rs", default="pull", choices=["pull", "push"],
-                    help="reduce-scatter: owners pull slices (default) or ranks push them into owners' landing slots")
     ap.add_argument("--overlap-bwd", type=int, default=0,
                     help="run each layer's backward gather on a second stream, capped at this many CTAs, "
                          "beside the previous layer's reduce-scatter (capped at the remaining SMs); 0 = one stream")
@@ -69,7 +65,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-nccl", action="store_true")
-    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle sample time")
+    ap.add_argument("--oracle-numel", type=int, default=0,
+                    help="elements of the oracle's sample (0: 2^25/P; tests use small samples)")
     return ap.parse_args()
 
 
@@ -139,48 +136,164 @@ def ncu_traffic():
 
 
 def host_cores():
-    return os.cpu_count()
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def host_mem_available():
+    try:
+        with open("/proc/meminfo") as f:
+            for line in f:
+                if line.startswith("MemAvailable:"):
+                    return int(line.split()[1]) * 1024
+    except OSError:
+        pass
+    return 8 << 30
 
 
 # ----------------------------------------------------------------------------- oracle legs
-def oracle_sample(world, node_size, dtype, target_s):
-    """Time the CPU oracle (as it stands) on a bounded sample of the workload: one flat
-    layer of S elements, all P ranks simulated, one full step (both gathers, RS, Adam).
-    S is grown until a step takes >= target_s/4, then one more timed step is run.
-    Returns (GB/s by the same byte accounting, seconds, S)."""
+def oracle_sample_numel(world, override=0):
+    """The bounded sample of the workload the oracle is timed on: the first S elements of
+    one flat layer, S = 2^25 / P (rounded to whole P*256 blocks) — the oracle simulates all P
+    ranks, so its work per sample is ~constant in P.  Deterministic: both arms time exactly
+    this sample."""
+    q = world * 256
+    return max(q, ((override or (1 << 25) // world)) // q * q)
+
+
+def _oracle_worker(world, node_size, dtype, S, rounds, barrier, out_q):
+    """One oracle process: build a one-layer HpzOracle of S elements (all P ranks), then
+    `rounds` times: wait for every process, time one full step (fwd gather + secondary,
+    bwd gather, RS, Adam)."""
+    os.environ["OMP_NUM_THREADS"] = "1"
     from oracle import hpz_oracle as O
-    e = 2 if dtype == "bf16" else 4
-    S = 1 << 18
-    while True:
-        o = O.HpzOracle([S], world, node_size, align=256, param_dtype=dtype)
-        t0 = time.perf_counter()
+    o = O.HpzOracle([S], world, node_size, align=256, param_dtype=dtype)
+    for k in range(rounds):
+        barrier.wait()
+        t0 = time.time()
         o.step()
-        dt = time.perf_counter() - t0
-        if dt >= target_s / 4 or S >= (1 << 27):
-            break
-        S = int(S * min(8.0, max(2.0, (target_s / 4) / max(dt, 1e-3))))
-    lay = o.layouts[0]
-    t0 = time.perf_counter()
-    o.step()
-    dt = time.perf_counter() - t0
-    bytes_ = world * (2 * lay.numel_pad * e + 4 * lay.numel_pad)
-    return bytes_ / dt / 1e9, dt, S
+        out_q.put((k, t0, time.time()))
+
+
+def oracle_bytes(world, S, dtype):
+    """Algorithmic bytes of one sample step (same algbw accounting as the GPU arm)."""
+    e = 2 if dtype == "bf16" else 4
+    return world * (2 * S * e + 4 * S)
+
+
+def oracle_time(world, node_size, dtype, S, procs, rounds=1):
+    """Wall time of each of `rounds` rounds of `procs` concurrent one-step samples
+    (processes, one per core)."""
+    import multiprocessing as mp
+    ctx = mp.get_context("fork")
+    barrier = ctx.Barrier(procs)
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_oracle_worker, args=(world, node_size, dtype, S, rounds, barrier, q))
+          for _ in range(procs)]
+    for p in ps:
+        p.start()
+    spans = [q.get() for _ in range(procs * rounds)]
+    for p in ps:
+        p.join()
+    walls = []
+    for k in range(rounds):
+        sk = [(a, b) for kk, a, b in spans if kk == k]
+        walls.append(max(b for _, b in sk) - min(a for a, _ in sk))
+    return walls if rounds > 1 else walls[0]
+
+
+def oracle_procs(world, S):
+    """Processes for the all-cores leg: every core, bounded so the samples' memory (about
+    80 B per element per simulated rank, measured) stays under half of MemAvailable."""
+    per = 80 * S * world + (300 << 20)
+    return max(1, min(host_cores(), int(host_mem_available() * 0.5 // per)))
+
+
+def cpu_baseline(world, node_size, dtype, model_elems, override=0):
+    """The oracle as it stands, timed on this box's host cores: one thread, then one
+    process per core; plus the per-step time extrapolated to the whole model."""
+    S = oracle_sample_numel(world, override)
+    bytes1 = oracle_bytes(world, S, dtype)
+    dt1 = oracle_time(world, node_size, dtype, S, 1)
+    C = oracle_procs(world, S)
+    dtc = oracle_time(world, node_size, dtype, S, C) if C > 1 else dt1
+    v1 = bytes1 / dt1 / 1e9
+    vc = C * bytes1 / dtc / 1e9
+    step1 = model_elems / S * dt1
+    return {"value": round(vc, 4), "unit": "GB/s", "cores": C, "kind": "oracle",
+            "sample": f"oracle/hpz_oracle.py HpzOracle, one full step (fwd gather + secondary, bwd gather, RS, Adam) "
+                      f"of the first {S} elements of one flat layer, all {world} rank(s) simulated (P={world}, "
+                      f"P'={node_size}); {C} such samples in {C} concurrent processes ({dtc:.2f} s wall); "
+                      f"numpy; same algbw byte accounting as the GPU arm; host has {host_cores()} cores",
+            "single_thread": {"value": round(v1, 4), "unit": "GB/s", "cores": 1, "seconds": round(dt1, 3)},
+            "extrapolated_step_s": {"single_thread": round(step1, 1), "all_cores": round(step1 * v1 / vc, 1),
+                                    "note": "EXTRAPOLATED: (model elements / sample elements) x sample time"}}
 
 
 # ----------------------------------------------------------------------------- main arm
+def free_port():
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def relaunch(n):
+    """`python bench.py --gpus N` outside torchrun: start N ranks (one process per GPU)
+    through torch.distributed.run on 127.0.0.1 and relay rank 0's JSON line; everything
+    else the ranks print goes to stderr.  Returns the launcher's exit code."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    p = subprocess.Popen(cmd, stdout=subprocess.PIPE, text=True, cwd=ROOT)
+    for line in p.stdout:
+        s = line.strip()
+        if s.startswith("{") and s.endswith("}"):
+            print(s, flush=True)
+        else:
+            sys.stderr.write(line)
+    return p.wait()
+
+
+def make_config(args, world, node_size, n_layers, n_params, n_slots):
+    """The workload this line measures (identical for both arms)."""
+    return {"workload": f"{args.model}-shaped flat parameter buffers ({n_layers} layers, "
+                        f"{n_params} params), bf16 params + fp32 master/Adam",
+            "world": world, "node_size": node_size, "virtual_nodes": world // node_size,
+            "parallelism": f"hpZ dp{world} (P={world}, P'={node_size})", "order": args.order,
+            "verify": args.verify, "copy_engine": args.copy_engine,
+            "reduce_scatter": "pull" if world > 1 else "local",
+            "overlap_bwd": (f"backward gathers on a second stream ({args.overlap_bwd} CTAs) beside "
+                            f"the reduce-scatters") if args.overlap_bwd else None,
+            "qgz": "int4 blockwise (64) gradient all-to-all; RS bytes counted as the fp32 "
+                   "gradient bytes reduced, wire bytes 0.625 B/elem" if args.qgz else None,
+            "grad_dtype": args.grad_dtype, "grad_slots": n_slots,
+            "qwz": "int8 blockwise (256) weights in the forward gather; AG bytes counted as the "
+                   "bf16 parameter bytes delivered" if args.qwz else None,
+            "l2": "no flush: per-step working set >> 126 MB L2 (every layer buffer is "
+                  "touched once per phase)",
+            "value_def": "sum over ranks of AllGather output bytes (fwd+bwd) + ReduceScatter "
+                         "input bytes per step (nccl-tests algbw bytes) / max-over-ranks device time "
+                         "of the whole step (gathers, reduce-scatter and Adam)"}
+
+
 def main():
     args = parse()
+    under_launcher = "WORLD_SIZE" in os.environ
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     n_gpus = args.gpus if args.gpus is not None else world
-    if n_gpus != world:
-        if world == 1 and n_gpus > 1:
-            sys.exit(f"--gpus {n_gpus} needs torchrun --nproc-per-node {n_gpus}")
-    node_size = args.node_size or (world // 2 if world >= 2 else 1)
-
     if args.impl == "reference":
-        return reference_arm(args, world, rank, node_size)
+        # the oracle arm needs no GPU ranks: rank 0 (or this lone process) simulates all N
+        return reference_arm(args, n_gpus if not under_launcher else world, rank,
+                             args.node_size or (n_gpus // 2 if n_gpus >= 2 else 1))
+    if not under_launcher and n_gpus > 1:
+        sys.exit(relaunch(n_gpus))
+    if n_gpus != world:
+        sys.exit(f"--gpus {n_gpus} but WORLD_SIZE={world}")
+    node_size = args.node_size or (world // 2 if world >= 2 else 1)
 
     import torch
     import torch.distributed as dist
@@ -201,14 +314,10 @@ def main():
     n_slots = args.grad_slots if 0 < args.grad_slots < L else L
     if world > 1:
         W = DistWorld(numels, node_size, dtype=dtype, n_grad_slots=n_slots, device=local_rank, timeout_s=60.0,
-                      qgz=args.qgz, grad_dtype=args.grad_dtype, qwz=args.qwz,
-                      landing_bufs=1 if args.gather == "push" else 0, rs_push=args.rs == "push")
+                      qgz=args.qgz, grad_dtype=args.grad_dtype, qwz=args.qwz)
     else:
         W = EmulatedWorld(numels, 1, 1, dtype=dtype, n_grad_slots=n_slots, device=local_rank, timeout_s=60.0,
-                          qgz=args.qgz, grad_dtype=args.grad_dtype, qwz=args.qwz,
-                          landing_bufs=1 if args.gather == "push" else 0)
-        if args.gather == "push":
-            H.hpz_set_option(W.ranks[0].ctx, "split_phases", 0)     # one rank: phases inline
+                          qgz=args.qgz, grad_dtype=args.grad_dtype, qwz=args.qwz)
     rc = W.ranks[0]
     ctx = rc.ctx
     H.hpz_set_order(ctx, args.order)
@@ -232,11 +341,7 @@ def main():
             H.hpz_synth_grads(ctx, i, S.stream_key(S.SEED_GRADS, i, 0, rank), S.GRAD_SCALE, 0, stream)
     tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
     nmax = max(x.numel_pad for x in infos)
-    if args.gather == "push":   # arena landing buffer: owners store their shards into it (P2P)
-        from paper_2407_01614_b200.world import device_view
-        fwd_buf = device_view(H.hpz_landing_buffer(ctx, 0), nmax, dtype)
-    else:
-        fwd_buf = torch.empty(nmax, dtype=tdt, device=dev)     # caller-owned full buffers, reused
+    fwd_buf = torch.empty(nmax, dtype=tdt, device=dev)     # caller-owned full buffers, reused
     # per layer (repartition); with --overlap-bwd the gathers run ahead of the
     # reduce-scatters, so a small ring of buffers stands in for the backward compute's reads
     bwd_bufs = [torch.empty(nmax, dtype=tdt, device=dev) for _ in range(2 if args.overlap_bwd else 1)]
@@ -492,35 +597,13 @@ def main():
     if rank == 0:
         cpu = None
         if not args.no_cpu_baseline:
-            gbs, dt, Ssz = oracle_sample(world, node_size, dtype, args.cpu_seconds)
-            cpu = {"value": round(gbs, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
-                   "sample": f"oracle/hpz_oracle.py HpzOracle: one step (fwd gather+secondary, bwd gather, "
-                             f"RS, Adam) of ONE flat layer of {Ssz} elements, all {world} rank(s) simulated "
-                             f"(P={world}, P'={node_size}), {dt:.2f} s; same algbw byte accounting; numpy, "
-                             f"single thread (host has {host_cores()} cores)"}
+            cpu = cpu_baseline(world, node_size, dtype, sum(x.numel_pad for x in infos), args.oracle_numel)
         out = {
             "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world,
             "steps": K, "warmup": args.warmup, "ms_per_step": round(step_ms, 3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "bf16 gathers / f32 reduce-scatter+Adam", "data": "synthetic",
-            "config": {"workload": f"{args.model}-shaped flat parameter buffers ({L} layers, "
-                                   f"{sum(x.numel for x in infos)} params), bf16 params + fp32 master/Adam",
-                       "world": world, "node_size": node_size, "virtual_nodes": world // node_size,
-                       "parallelism": f"hpZ dp{world} (P={world}, P'={node_size})", "order": args.order,
-                       "verify": args.verify, "copy_engine": args.copy_engine, "fwd_gather": args.gather,
-                       "reduce_scatter": args.rs if world > 1 else "local",
-                       "overlap_bwd": (f"backward gathers on a second stream ({args.overlap_bwd} CTAs) beside "
-                                       f"the reduce-scatters") if args.overlap_bwd else None,
-                       "qgz": "int4 blockwise (64) gradient all-to-all; RS bytes counted as the fp32 "
-                              "gradient bytes reduced, wire bytes 0.625 B/elem" if args.qgz else None,
-                       "grad_dtype": args.grad_dtype, "grad_slots": n_slots,
-                       "qwz": "int8 blockwise (256) weights in the forward gather; AG bytes counted as the "
-                              "bf16 parameter bytes delivered" if args.qwz else None,
-                       "l2": "no flush: per-step working set >> 126 MB L2 (every layer buffer is "
-                             "touched once per phase)",
-                       "value_def": "sum over ranks of AllGather output bytes (fwd+bwd) + ReduceScatter "
-                                    "input bytes per step (nccl-tests algbw bytes) / max-over-ranks device time "
-                                    "of the whole step (gathers, reduce-scatter and Adam)"},
+            "config": make_config(args, world, node_size, L, sum(x.numel for x in infos), n_slots),
             "stale_param_mismatches": {"fingerprint_layers": int(stats[0]), "exact_elements": int(stats[1]),
                                        "nan_reads": int(stats[2]), "timeouts": int(stats[3]),
                                        "layers_checked": int(stats[4])},
@@ -611,29 +694,36 @@ def nccl_baseline(infos, e, node_size, dev, tdt, args):
 
 def reference_arm(args, world, rank, node_size):
     """--impl reference: the CPU oracle as it stands, on this arm's config/metric/unit, each
-    step a bounded sample of the workload.  Under torchrun only rank 0 runs."""
+    step the bounded sample of the workload that `cpu_baseline` times (one process per host
+    core, each simulating one step of all P ranks on the first S elements of a layer).
+    Under torchrun only rank 0 runs; the other ranks exit without work."""
     if rank != 0:
         return
     from paper_2407_01614_b200 import shapes
     dtype = shapes.PARAM_DTYPE.get(args.model, "bf16")
-    target = max(2.0, min(args.cpu_seconds, 60.0 / max(1, args.steps + args.warmup)))
-    vals = []
-    Ssz = dt = None
-    for k in range(args.warmup + args.steps):
-        gbs, dt, Ssz = oracle_sample(world, node_size, dtype, target)
-        if k >= args.warmup:
-            vals.append((gbs, dt))
-    value = statistics.median(v for v, _ in vals)
-    ms = statistics.median(d for _, d in vals) * 1e3
-    sample = (f"oracle/hpz_oracle.py HpzOracle: one step of ONE flat layer of {Ssz} elements, all {world} "
-              f"rank(s) simulated (P={world}, P'={node_size}); numpy single thread")
+    numels = shapes.numels(args.model)
+    L = len(numels)
+    n_slots = args.grad_slots if 0 < args.grad_slots < L else L
+    S = oracle_sample_numel(world, args.oracle_numel)
+    C = oracle_procs(world, S)
+    walls = oracle_time(world, node_size, dtype, S, C, rounds=args.warmup + args.steps)
+    walls = walls if isinstance(walls, list) else [walls]
+    timed = walls[args.warmup:]
+    bytes_round = C * oracle_bytes(world, S, dtype)
+    value = statistics.median(bytes_round / w / 1e9 for w in timed)
+    ms = statistics.median(timed) * 1e3
+    q = world * 256
+    model_elems = sum(-(-n // q) * q for n in numels)
+    sample = (f"oracle/hpz_oracle.py HpzOracle, one full step of the first {S} elements of one flat layer, all "
+              f"{world} rank(s) simulated (P={world}, P'={node_size}); {C} such samples in {C} concurrent "
+              f"processes per step; numpy; host has {host_cores()} cores")
     out = {"metric": METRIC, "value": round(value, 4), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": round(ms, 1), "higher_is_better": True, "scaling": "weak",
            "vs_baseline": None, "dtype": "bf16 gathers / f32 reduce-scatter+Adam", "data": "synthetic",
            "impl": "reference",
-           "config": {"workload": f"{args.model}-shaped flat parameter buffers (bounded per-step sample)",
-                      "world": world, "node_size": node_size},
-           "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "kind": "oracle", "cores": 1, "sample": sample},
+           "config": make_config(args, world, node_size, L, sum(numels), n_slots),
+           "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "kind": "oracle", "cores": C, "sample": sample,
+                            "extrapolated_step_s": round(model_elems / (C * S) * statistics.median(timed), 1)},
            "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
 

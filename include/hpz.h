@@ -314,57 +314,17 @@ typedef enum {
                                     before hpz_register_flat_params. */
   HPZ_OPT_MAX_CTAS = 6,          /* cap on the CTAs of every launch (0 = whole GPU): bounds the SMs
                                     the collectives occupy while compute overlaps them (f3) */
-  HPZ_OPT_LANDING_BUFS = 7,      /* 0..8 library-owned full-parameter buffers in the arena
-                                    (hpz_landing_buffer); a forward gather into one of them runs
-                                    owner-driven: every owner bulk-stores its primary shard into
-                                    every rank's landing buffer and the secondaries over NVLink
-                                    (P2P stores), instead of every rank pulling.  FIXED order,
-                                    no qwZ.  Set before hpz_register_flat_params. */
-  HPZ_OPT_SPLIT_PHASES = 8,      /* 0/1: push gathers leave their post / finish phases to the
-                                    caller (hpz_fwd_gather_post / _finish) — needed when several
-                                    ranks share one GPU stream (single-GPU emulation); with
-                                    HPZ_OPT_RS_PUSH, hpz_grads_ready runs the push phase */
-  HPZ_OPT_RS_PUSH = 9,           /* 0 (default) or 1, P >= 2, fp32 or bf16 gradients (not qgZ):
-                                    owner-driven reduce-scatter.  Every rank bulk-stores the
-                                    slices of its gradient slot into the owners' landing slots
-                                    over NVLink (posted writes, one chunk counter per 2048 or
-                                    1024 elements incremented per source) and each owner reduces
-                                    from its local landing slot as the chunks arrive, in the
-                                    same R7 order (same bits as the pull).  One kernel per layer
-                                    does both (a push warp beside the reduce pipeline); two
-                                    landing slots of P x max-shard gradient elements are added
-                                    to the arena.  Set before hpz_register_flat_params. */
   HPZ_OPT_BWD_CTAS = 10,         /* CTA cap of the backward gathers (0 = none) and ... */
-  HPZ_OPT_RS_CTAS = 11,          /* ... of the reduce-scatters: with caps summing to at most the
+  HPZ_OPT_RS_CTAS = 11           /* ... of the reduce-scatters: with caps summing to at most the
                                     SM count, a backward gather on one stream and a
                                     reduce-scatter on another run side by side (no kernel of
                                     either waits on the other, so they may share the GPU) */
-  HPZ_OPT_XNODE_MBPS = 12        /* 0 (default) or MB/s: emulate the paper's constrained
-                                    inter-node network (PAPER.md title, 147-151) on one NVSwitch
-                                    box — the TMA pull kernels pace their reads from ranks of
-                                    OTHER virtual nodes to this rate per GPU (forward gathers,
-                                    pull reduce-scatters, ORDER_OFF backward gathers; hpZ's
-                                    backward gathers stay inside the node).  Experiment knob
-                                    for the f3 / Table 2 analog; may change between steps. */
 } hpz_option;
 /* Copy engine of the gathers and the reduce-scatter: TMA 1-D bulk copies through a
  * shared-memory stage ring (cp.async.bulk, one persistent CTA per SM), or 16-byte
  * LDG/STG streams (several CTAs per SM).  EXACT verification always uses LDG/STG. */
 typedef enum { HPZ_COPY_LDG = 0, HPZ_COPY_TMA = 1 } hpz_copy_engine;
 HPZ_API int hpz_set_option(hpz_ctx* ctx, int option, int64_t value);
-
-/* Landing buffer `idx` (HPZ_OPT_LANDING_BUFS) of this rank: a device buffer of the largest
- * layer's numel_pad elements (param dtype), peer-mapped.  Pass it as full_out to
- * hpz_fwd_gather to use the push path; its contents are valid after the gather (stream
- * order) until the next gather into the same buffer. */
-HPZ_API int hpz_landing_buffer(const hpz_ctx* ctx, int idx, void** out);
-
-/* Push-gather phases for callers that run several ranks on one stream (HPZ_OPT_SPLIT_PHASES):
- * post = E4 then "my landing buffer and secondary may be written" (FREE) to every owner;
- * hpz_fwd_gather = the owner's push kernel; finish = wait until every owner's shard landed
- * (DATA), then release E3 / E2.  Without SPLIT_PHASES hpz_fwd_gather does all three. */
-HPZ_API int hpz_fwd_gather_post(hpz_ctx* ctx, int layer, void* full_out, void* stream);
-HPZ_API int hpz_fwd_gather_finish(hpz_ctx* ctx, int layer, void* stream);
 
 #ifdef __cplusplus
 }

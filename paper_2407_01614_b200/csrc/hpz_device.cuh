@@ -48,15 +48,6 @@ __device__ __forceinline__ bool wait_geq(const uint32_t* flag, uint32_t target, 
   return true;
 }
 
-// Emulated inter-node link: a producer that has issued `bytes` of cross-node reads since t0
-// waits until its share of the link would have carried them.  ns_per_byte = (all CTAs'
-// cross-node bytes / this CTA's) / rate, so every CTA ends its cross-node reads together
-// and the GPU's aggregate cross-node rate is the link rate (GB/s = bytes/ns).
-__device__ __forceinline__ void xnode_pace(uint64_t t0, uint64_t bytes, float ns_per_byte) {
-  const uint64_t due = t0 + (uint64_t)((float)bytes * ns_per_byte);
-  while (globaltimer() < due) __nanosleep(200);
-}
-
 __device__ __forceinline__ void wait_all(const WaitList& w, const SyncCommon& s) {
   for (int k = 0; k < w.n; ++k) wait_geq(w.ptr[k], w.target, s);
 }

@@ -16,10 +16,6 @@ struct SyncCommon {
   uint32_t* abort_flag;                // local arena: set after the first timeout -> later waits skip
   unsigned long long* timeouts;        // local arena counter
   volatile uint32_t* host_err;         // host-mapped pinned word polled by the runtime
-  // emulated inter-node link (HPZ_OPT_XNODE_MBPS): reads from the sources set in
-  // xnode_mask (source index of the kernel) are paced to xnode_gbps per GPU (0: off)
-  float xnode_gbps;
-  uint32_t xnode_mask;
 };
 
 // A list of flags to release (st.release.sys of `value`), possibly in peer arenas.
@@ -71,26 +67,6 @@ struct GatherParams {
   SyncCommon sync;
 };
 
-// Push forward gather (a2 with P2P stores): owner j streams its primary shard through a
-// TMA stage ring and bulk-stores every chunk into every rank's landing buffer (and into
-// the secondaries whose slice contains shard j) over NVLink.
-struct PushParams {
-  const char* src;                     // my primary shard (local)
-  int64_t src_bytes;                   // shard bytes (multiple of 16)
-  const uint32_t* src_flag;            // E1 on my own primary (PRIMARY_READY[layer][me])
-  uint32_t src_target;
-  char* land[kMaxWorld];               // rank q's landing buffer + my offset j*src_bytes
-  char* sec[kMaxWorld];                // rank q's secondary + (j - l(q)*k)*src_bytes, or nullptr
-  const uint32_t* free_flag[kMaxWorld];  // local FREE flag of destination q (acquired once per CTA)
-  uint32_t free_target;
-  int n_dst;
-  unsigned long long* fp_dst[kMaxWorld]; // rank q's forward fingerprint accumulator, or nullptr
-  int64_t word_base;                   // my shard's first 16-byte word index in the full buffer
-  uint32_t* done_ctr;
-  ReleaseList rel;                     // DATA into every destination
-  SyncCommon sync;
-};
-
 // qgZ (f1): blockwise INT4 quantization of one rank's gradient slot.
 constexpr int kQgzBlock = 64;          // elements per (min, scale) block
 struct QuantParams {
@@ -128,20 +104,7 @@ struct RSParams {
   ReleaseList ready;                   // E5 release (may be empty if already released)
   WaitList ready_wait;                 // E5 acquire of every rank
   uint32_t* done_ctr;
-  ReleaseList rel;                     // E6 release (push: landing slot free, to every pusher)
-  // push reduce-scatter (HPZ_OPT_RS_PUSH): src[j != self] are then my LOCAL landing slot's
-  // slices (written by rank j), src[self] my own gradient slot's slice
-  int push_on, reduce_on, self;
-  const char* push_src;                // my gradient slot (local); owner q's slice at q * push_shard_bytes
-  int64_t push_shard_bytes;            // shard * gradient bytes
-  char* push_dst[kMaxWorld];           // owner q's landing slot + my slice (nullptr for q == self)
-  uint32_t* push_ctr[kMaxWorld];       // owner q's chunk counters of that landing slot
-  const uint32_t* push_free[kMaxWorld];  // local: owner q released the slot's previous use
-  uint32_t push_free_target;
-  uint32_t* chunk_ctr;                 // reduce: my chunk counters of the landing slot (reset to 0
-                                       // once consumed: layers of different sizes share a slot)
-  uint32_t chunk_target;               // P - 1
-  ReleaseList rel2;                    // push: E6 of my own gradient slot (local flags)
+  ReleaseList rel;                     // E6 release
   SyncCommon sync;
 };
 
@@ -172,19 +135,13 @@ cudaError_t launch_rs_adam(const RSParams& r, const AdamParams& a, int world, in
 cudaError_t launch_gather_tma(const GatherParams& p, int grid, cudaStream_t s);
 // mode: 0 fp32 gradients, 1 bf16 gradients (fp32 accumulation), 2 qgZ INT4 codes
 cudaError_t launch_rs_tma(const RSParams& r, const AdamParams* a, int world, int grid, cudaStream_t s,
-                          int mode = 0, bool push = false);
-// Chunk (elements of a shard) of the push reduce-scatter: one landing counter per chunk.
-int rs_push_chunk_elems(int world);
+                          int mode = 0);
 cudaError_t launch_qgz_quantize(const QuantParams& q, int grid, cudaStream_t s);
-cudaError_t launch_push_gather(const PushParams& p, int grid, cudaStream_t s);
 cudaError_t launch_qwz_quantize(const QwzQuantParams& q, int grid, cudaStream_t s);
 // qwZ forward gather: TMA-pulls codes + params, dequantizes, STG to out (+ secondary).
 cudaError_t launch_gather_qwz(const GatherParams& p, int grid, cudaStream_t s);
 cudaError_t launch_wait(const WaitList& w, const SyncCommon& sync, cudaStream_t s);
 cudaError_t launch_release(const ReleaseList& r, cudaStream_t s);
-cudaError_t launch_wait_release(const WaitList& w, const ReleaseList& r, const SyncCommon& sync, cudaStream_t s);
-cudaError_t launch_wait_copy_release(void* dst, const void* src, int64_t bytes, const WaitList& w, uint32_t* done_ctr,
-                                     const ReleaseList& r, const SyncCommon& sync, int grid, cudaStream_t s);
 cudaError_t launch_copy(void* dst, const void* src, int64_t bytes, int grid, cudaStream_t s);
 cudaError_t launch_refresh_primary(const float* master, void* prim, int prim_bf16, int64_t n, int grid, cudaStream_t s);
 cudaError_t launch_fill_u32(void* dst, uint32_t value, int64_t bytes, int grid, cudaStream_t s);

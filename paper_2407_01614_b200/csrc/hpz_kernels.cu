@@ -334,28 +334,6 @@ __global__ void wait_kernel(const WaitList w, const SyncCommon s) {
   if (threadIdx.x == 0) wait_all(w, s);
 }
 
-// wait for every flag of w, then (fence) release every flag of r: the small phase
-// kernels of the push gather (post: E4 -> FREE; finish: DATA -> SEC_READY, FWD_DONE)
-__global__ void wait_release_kernel(const WaitList w, const ReleaseList r, const SyncCommon s) {
-  if (threadIdx.x == 0) {
-    wait_all(w, s);
-    __threadfence_system();
-    release_all(r);
-  }
-}
-
-// wait for w (thread 0 of every CTA), copy `n_vec` 16-byte words dst <- src, then the last
-// CTA releases r: the push gather's finish phase (landing slice -> my secondary, E3/E2)
-__global__ void __launch_bounds__(kThreads) wait_copy_release_kernel(int4* dst, const int4* src, int64_t n_vec,
-                                                                      const WaitList w, uint32_t* done_ctr,
-                                                                      const ReleaseList r, const SyncCommon s) {
-  if (threadIdx.x == 0) wait_all(w, s);
-  __syncthreads();
-  for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n_vec; i += (int64_t)gridDim.x * kThreads)
-    st_v4(dst + i, ld_stream(src + i));
-  if (last_cta(done_ctr)) release_all(r);
-}
-
 __global__ void release_kernel(const ReleaseList r) {
   if (threadIdx.x == 0) {
     __threadfence_system();
@@ -503,18 +481,6 @@ cudaError_t launch_adam(const AdamParams& p, int grid, cudaStream_t s) {
 
 cudaError_t launch_wait(const WaitList& w, const SyncCommon& sync, cudaStream_t s) {
   wait_kernel<<<1, 32, 0, s>>>(w, sync);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_wait_release(const WaitList& w, const ReleaseList& r, const SyncCommon& sync, cudaStream_t s) {
-  wait_release_kernel<<<1, 32, 0, s>>>(w, r, sync);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_wait_copy_release(void* dst, const void* src, int64_t bytes, const WaitList& w, uint32_t* done_ctr,
-                                     const ReleaseList& r, const SyncCommon& sync, int grid, cudaStream_t s) {
-  wait_copy_release_kernel<<<grid, kThreads, 0, s>>>(reinterpret_cast<int4*>(dst), reinterpret_cast<const int4*>(src),
-                                                      bytes >> 4, w, done_ctr, r, sync);
   return cudaGetLastError();
 }
 

@@ -23,16 +23,13 @@ uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
 
 enum FlagKind { F_PRIM_READY = 0, F_FWD_DONE, F_SEC_READY, F_BWD_DONE, F_BWDP_DONE, F_NUM_LAYER_KINDS };
 enum SlotFlagKind { S_GRAD_READY = 0, S_RS_DONE, S_NUM };
-enum LandFlagKind { LF_FREE = 0, LF_DATA, LF_NUM };
-enum CtrKind { C_FWD = 0, C_BWD, C_RS, C_ADAM, C_QWZ, C_PUSH, C_FIN, C_NUM };
+enum CtrKind { C_FWD = 0, C_BWD, C_RS, C_ADAM, C_QWZ, C_NUM };
 
 struct Layer {
   int64_t numel, numel_pad, shard, sec_shard;
   uint64_t off_primary, off_master, off_m, off_v, off_gshard, off_secondary;
   uint64_t off_qw_codes = 0, off_qw_params = 0;   // qwZ (f2)
   int slot;
-  int rsl = -1;          // push RS: landing slot of the layer's pending reduce (-1: none)
-  uint64_t rsl_use = 0;  // ... and that slot's use index
   // host bookkeeping of the step t the layer's ops were issued for (-1: never)
   int64_t fwd_t = -1, bwd_t = -1, rs_t = -1, step_t = -1;
 };
@@ -72,21 +69,7 @@ struct hpz_ctx {
   int qwz_bits = 0;                       // f2: 8 = INT8 blockwise weights in the forward gather
   int max_ctas = 0;                       // cap on every grid (0 = all SMs)
   int bwd_ctas = 0, rs_ctas = 0;          // caps of the backward gathers / reduce-scatters (overlap)
-  float xnode_gbps = 0.0f;                // emulated inter-node link per GPU (0: NVLink speed)
-  int n_land = 0;                         // library-owned landing buffers (push forward gather)
-  bool split_phases = false;              // push gather: caller issues post / finish itself
-  std::vector<uint64_t> off_land, land_use;
-  std::vector<uint8_t> land_posted;
-  std::vector<int> land_pending;          // per layer: landing buffer awaiting finish (-1: none)
-  uint64_t land_bytes = 0;
   std::vector<uint64_t> off_qcodes, off_qparams;   // per grad slot (qgZ)
-  // push reduce-scatter (HPZ_OPT_RS_PUSH): kRsl landing slots of world x max-shard gradient
-  // elements, one chunk counter per rs_push_chunk_elems elements of a shard per slot
-  static constexpr int kRsl = 2;
-  bool rs_push = false;
-  uint64_t off_rsl[kRsl] = {}, rsl_stride = 0, off_rsc = 0;
-  int64_t rsc_chunks = 0;
-  uint64_t rs_seq = 0;                    // pushes issued (identical on every rank: SPMD order)
   std::string err;
 
   // ---- arena addressing (identical on every rank) ----
@@ -98,20 +81,6 @@ struct hpz_ctx {
     const uint64_t base = (uint64_t)F_NUM_LAYER_KINDS * n_layers * world;
     const uint64_t idx = base + ((uint64_t)kind * n_slots + slot) * world + src;
     return reinterpret_cast<uint32_t*>(arena[rank_arena] + off_flags) + idx;
-  }
-  uint32_t* land_flag(int rank_arena, int kind, int b, int src) const {
-    const uint64_t base = (uint64_t)F_NUM_LAYER_KINDS * n_layers * world + (uint64_t)S_NUM * n_slots * world;
-    const uint64_t idx = base + ((uint64_t)kind * n_land + b) * world + src;
-    return reinterpret_cast<uint32_t*>(arena[rank_arena] + off_flags) + idx;
-  }
-  // RL_FREE: owner `src` finished reducing from landing slot b (value = use + 1)
-  uint32_t* rl_flag(int rank_arena, int b, int src) const {
-    const uint64_t base = (uint64_t)F_NUM_LAYER_KINDS * n_layers * world + (uint64_t)S_NUM * n_slots * world +
-                          (uint64_t)LF_NUM * n_land * world;
-    return reinterpret_cast<uint32_t*>(arena[rank_arena] + off_flags) + base + (uint64_t)b * world + src;
-  }
-  uint32_t* rsc(int rank_arena, int b) const {
-    return reinterpret_cast<uint32_t*>(arena[rank_arena] + off_rsc) + (uint64_t)b * rsc_chunks;
   }
   uint32_t* ctr(int kind, int idx) const {
     return reinterpret_cast<uint32_t*>(arena[rank] + off_ctr) + (uint64_t)kind * (n_layers + n_slots) + idx;
@@ -129,17 +98,7 @@ struct hpz_ctx {
     s.abort_flag = reinterpret_cast<uint32_t*>(stat(5));
     s.timeouts = stat(4);
     s.host_err = host_err_dev;
-    s.xnode_gbps = xnode_gbps;
-    s.xnode_mask = 0;
     return s;
-  }
-  // emulated inter-node link: bit j set for every rank j on another virtual node
-  uint32_t xnode_mask() const {
-    if (xnode_gbps <= 0.0f) return 0;
-    uint32_t m = 0;
-    for (int j = 0; j < world; ++j)
-      if (j / node_size != rank / node_size) m |= 1u << j;
-    return m;
   }
   int node_first() const { return (rank / node_size) * node_size; }
   int local() const { return rank % node_size; }
@@ -200,10 +159,6 @@ cudaError_t gather_launch(const hpz_ctx* c, const GatherParams& p, cudaStream_t 
 }
 
 cudaError_t rs_launch(const hpz_ctx* c, const RSParams& r, const AdamParams* a, cudaStream_t s) {
-  if (c->rs_push) {
-    const int64_t ch = rs_push_chunk_elems(c->world);
-    return launch_rs_tma(r, a, c->world, grid_for(c, (r.n_vec * 4 + ch - 1) / ch, 1, c->rs_ctas), s, c->grad_bytes == 2 ? 1 : 0, true);
-  }
   if (c->qgz_bits || c->grad_bytes == 2)   // qgZ codes / bf16 gradients: TMA engine only
     return launch_rs_tma(r, a, c->world, grid_for(c, (r.n_vec * 4 + 1023) / 1024, 1, c->rs_ctas), s, c->qgz_bits ? 2 : 1);
   if (c->copy_engine == HPZ_COPY_TMA)
@@ -354,16 +309,7 @@ int hpz_register_flat_params(hpz_ctx* c, int n_layers, const int64_t* numel, int
     if (L.numel_pad > c->slot_numel[L.slot]) c->slot_numel[L.slot] = L.numel_pad;
   }
   // control region: flags | completion counters | fingerprints | stats
-  if (c->world == 1) c->rs_push = false;   // nothing to push
-  int64_t smax = 0;
-  for (int i = 0; i < n_layers; ++i) {
-    const Layer& L = c->layers[i];
-    smax = L.shard > smax ? L.shard : smax;
-  }
-  const int64_t push_chunk = c->rs_push ? rs_push_chunk_elems(c->world) : 1;
-  c->rsc_chunks = c->rs_push ? (smax + push_chunk - 1) / push_chunk : 0;
-  const uint64_t n_flags = (uint64_t)F_NUM_LAYER_KINDS * n_layers * c->world + (uint64_t)S_NUM * n_grad_slots * c->world +
-                           (uint64_t)LF_NUM * c->n_land * c->world + (uint64_t)hpz_ctx::kRsl * c->world;
+  const uint64_t n_flags = (uint64_t)F_NUM_LAYER_KINDS * n_layers * c->world + (uint64_t)S_NUM * n_grad_slots * c->world;
   uint64_t off = 0;
   c->off_flags = off;
   off = align_up(off + n_flags * 4, 256);
@@ -373,8 +319,6 @@ int hpz_register_flat_params(hpz_ctx* c, int n_layers, const int64_t* numel, int
   off = align_up(off + (uint64_t)n_layers * 4 * 8, 256);
   c->off_stats = off;
   off = align_up(off + 8 * 8, 256);
-  c->off_rsc = off;
-  off = align_up(off + (uint64_t)hpz_ctx::kRsl * c->rsc_chunks * 4, 256);
   c->ctrl_bytes = align_up(off, kCtrlAlign);
   off = c->ctrl_bytes;
   for (int i = 0; i < n_layers; ++i) {
@@ -404,25 +348,6 @@ int hpz_register_flat_params(hpz_ctx* c, int n_layers, const int64_t* numel, int
       off = align_up(off + (uint64_t)c->slot_numel[s] / 2, kBufAlign);
       c->off_qparams[s] = off;
       off = align_up(off + (uint64_t)c->slot_numel[s] / kQgzBlock * 8, kBufAlign);
-    }
-  }
-  // landing buffers of the push forward gather: one full layer (largest numel_pad) each
-  uint64_t nmax = 0;
-  for (const Layer& L : c->layers) nmax = nmax > (uint64_t)L.numel_pad ? nmax : (uint64_t)L.numel_pad;
-  c->land_bytes = nmax * elem;
-  c->off_land.assign(c->n_land, 0);
-  c->land_use.assign(c->n_land, 0);
-  c->land_posted.assign(c->n_land, 0);
-  c->land_pending.assign(n_layers, -1);
-  for (int b = 0; b < c->n_land; ++b) {
-    c->off_land[b] = off;
-    off = align_up(off + c->land_bytes, kBufAlign);
-  }
-  if (c->rs_push) {   // landing slots: rank j's slice for me at j * max-shard
-    c->rsl_stride = (uint64_t)smax * c->grad_bytes;
-    for (int b = 0; b < hpz_ctx::kRsl; ++b) {
-      c->off_rsl[b] = off;
-      off = align_up(off + c->rsl_stride * c->world, kBufAlign);
     }
   }
   c->arena_bytes = off;
@@ -667,114 +592,6 @@ int hpz_synth_master(hpz_ctx* c, int layer, uint64_t key, float scale, void* str
   return do_init_shard(c, layer, nullptr, key, scale, static_cast<cudaStream_t>(stream));
 }
 
-// ---- push forward gather (landing buffers in the arena) -------------------------------
-static int land_index(const hpz_ctx* c, const void* full_out) {
-  for (int b = 0; b < c->n_land; ++b)
-    if (full_out == c->arena[c->rank] + c->off_land[b]) return b;
-  return -1;
-}
-
-// phase 0: E4 (node peers finished reading my secondary for step t-1), then publish FREE:
-// my landing buffer b and my secondary may be written for this use of b.
-static int push_post(hpz_ctx* c, int layer, int b, cudaStream_t s) {
-  const int nf = c->node_first();
-  WaitList w{};
-  for (int q = 0; q < c->node_size; ++q) w.ptr[w.n++] = c->flag(c->rank, F_BWD_DONE, layer, nf + q);
-  w.target = epoch(c->t);
-  ReleaseList r{};
-  for (int j = 0; j < c->world; ++j) r.ptr[r.n++] = c->land_flag(j, LF_FREE, b, c->rank);
-  r.value = epoch(c->land_use[b] + 1);
-  cudaError_t e = launch_wait_release(w, r, c->sync(), s);
-  if (e != cudaSuccess) return fail(c, HPZ_ECUDA, "push post launch: %s", cudaGetErrorString(e));
-  c->launches += 1;
-  c->land_posted[b] = 1;
-  return HPZ_OK;
-}
-
-// phase 2: every owner's shard has landed (DATA) -> my full buffer is complete; my
-// secondary slice l(r) is copied from it locally (pushing it from the owners would cost
-// NVLink bytes the pull design gets for free), then SEC_READY (E3) to the node and
-// FWD_DONE (E2) to every owner.
-static int push_finish(hpz_ctx* c, int layer, cudaStream_t s) {
-  const int b = c->land_pending[layer];
-  const int nf = c->node_first();
-  const Layer& L = c->layers[layer];
-  WaitList w{};
-  for (int j = 0; j < c->world; ++j) w.ptr[w.n++] = c->land_flag(c->rank, LF_DATA, b, j);
-  w.target = epoch(c->land_use[b] + 1);
-  ReleaseList r{};
-  for (int q = 0; q < c->node_size; ++q) r.ptr[r.n++] = c->flag(nf + q, F_SEC_READY, layer, c->rank);
-  for (int j = 0; j < c->world; ++j) r.ptr[r.n++] = c->flag(j, F_FWD_DONE, layer, c->rank);
-  r.value = epoch(c->t + 1);
-  const int64_t sec_bytes = L.sec_shard * c->elem;
-  char* land = c->arena[c->rank] + c->off_land[b];
-  cudaError_t e = launch_wait_copy_release(c->arena[c->rank] + L.off_secondary, land + (int64_t)c->local() * sec_bytes,
-                                           sec_bytes, w, c->ctr(C_FIN, layer), r, c->sync(),
-                                           grid_for(c, (sec_bytes / 16 + 255) / 256, 4), s);
-  if (e != cudaSuccess) return fail(c, HPZ_ECUDA, "push finish launch: %s", cudaGetErrorString(e));
-  c->launches += 1;
-  c->land_use[b] += 1;
-  c->land_posted[b] = 0;
-  c->land_pending[layer] = -1;
-  return HPZ_OK;
-}
-
-// phase 1: the push kernel (owner streams its primary shard to every landing buffer).
-static int push_gather(hpz_ctx* c, int layer, int b, cudaStream_t s) {
-  Layer& L = c->layers[layer];
-  const int me = c->rank;
-  const int64_t sb = L.shard * c->elem;
-  PushParams p{};
-  p.src = c->arena[me] + L.off_primary;
-  p.src_bytes = sb;
-  p.src_flag = c->flag(me, F_PRIM_READY, layer, me);
-  p.src_target = epoch(c->t + 1);
-  p.n_dst = c->world;
-  p.word_base = (int64_t)me * sb / 16;
-  for (int q = 0; q < c->world; ++q) {
-    p.land[q] = c->arena[q] + c->off_land[b] + (uint64_t)me * sb;
-    p.sec[q] = nullptr;   // secondaries are filled locally by each receiver (push_finish)
-    p.free_flag[q] = c->land_flag(me, LF_FREE, b, q);
-    if (c->verify != HPZ_VERIFY_NONE)
-      p.fp_dst[q] = reinterpret_cast<unsigned long long*>(c->arena[q] + c->off_fp) + ((uint64_t)layer * 2 + (c->t & 1)) * 2;
-  }
-  p.free_target = epoch(c->land_use[b] + 1);
-  p.done_ctr = c->ctr(C_PUSH, layer);
-  for (int q = 0; q < c->world; ++q) p.rel.ptr[p.rel.n++] = c->land_flag(q, LF_DATA, b, me);
-  p.rel.value = epoch(c->land_use[b] + 1);
-  p.sync = c->sync();
-  cudaError_t e = launch_push_gather(p, grid_for(c, (sb + 32767) / 32768, 1), s);
-  if (e != cudaSuccess) return fail(c, HPZ_ECUDA, "push gather launch: %s", cudaGetErrorString(e));
-  c->launches += 1;
-  c->land_pending[layer] = b;
-  return HPZ_OK;
-}
-
-int hpz_landing_buffer(const hpz_ctx* cc, int idx, void** out) {
-  hpz_ctx* c = const_cast<hpz_ctx*>(cc);
-  if (!c || !out) return HPZ_EINVAL;
-  if (!c->registered || !c->arena[c->rank]) return fail(c, HPZ_ESTATE, "arena not allocated/bound");
-  if (idx < 0 || idx >= c->n_land) return fail(c, HPZ_EINVAL, "landing buffer %d out of range (%d)", idx, c->n_land);
-  *out = c->arena[c->rank] + c->off_land[idx];
-  return HPZ_OK;
-}
-
-int hpz_fwd_gather_post(hpz_ctx* c, int layer, void* full_out, void* stream) {
-  if (int rc = check_ready(c)) return rc;
-  if (int rc = check_layer(c, layer)) return rc;
-  const int b = land_index(c, full_out);
-  if (b < 0) return fail(c, HPZ_EINVAL, "full_out is not a landing buffer");
-  if (c->land_posted[b]) return fail(c, HPZ_ESTATE, "landing buffer %d already posted", b);
-  return push_post(c, layer, b, static_cast<cudaStream_t>(stream));
-}
-
-int hpz_fwd_gather_finish(hpz_ctx* c, int layer, void* stream) {
-  if (int rc = check_ready(c)) return rc;
-  if (int rc = check_layer(c, layer)) return rc;
-  if (c->land_pending[layer] < 0) return fail(c, HPZ_ESTATE, "layer %d has no push gather to finish", layer);
-  return push_finish(c, layer, static_cast<cudaStream_t>(stream));
-}
-
 int hpz_fwd_gather(hpz_ctx* c, int layer, void* full_out, void* stream) {
   if (int rc = check_ready(c)) return rc;
   if (int rc = check_layer(c, layer)) return rc;
@@ -784,17 +601,6 @@ int hpz_fwd_gather(hpz_ctx* c, int layer, void* full_out, void* stream) {
   if (c->qwz_bits && (c->verify == HPZ_VERIFY_EXACT || c->order == HPZ_ORDER_OFF))
     return fail(c, HPZ_ESTATE, "qwZ gathers dequantized weights: EXACT verification and ORDER_OFF compare/read raw primaries");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const int land = land_index(c, full_out);
-  if (land >= 0 && c->order == HPZ_ORDER_FIXED && !c->qwz_bits) {
-    // owner-driven P2P stores into every rank's landing buffer (+ fused secondary stores)
-    if (!c->land_posted[land])
-      if (int rc = push_post(c, layer, land, s)) return rc;
-    if (int rc = push_gather(c, layer, land, s)) return rc;
-    if (!c->split_phases)
-      if (int rc = push_finish(c, layer, s)) return rc;
-    L.fwd_t = c->t;
-    return HPZ_OK;
-  }
   const uint32_t t1 = epoch(c->t + 1);
   GatherParams p{};
   p.n_src = c->world;
@@ -824,7 +630,6 @@ int hpz_fwd_gather(hpz_ctx* c, int layer, void* full_out, void* stream) {
   for (int j = 0; j < c->world; ++j) p.rel.ptr[p.rel.n++] = c->flag(j, F_FWD_DONE, layer, c->rank);            // E2
   p.rel.value = t1;
   p.sync = c->sync();
-  p.sync.xnode_mask = c->xnode_mask();   // sources are the ranks
   cudaError_t e;
   if (c->qwz_bits) {
     // qwZ: pull every owner's INT8 codes + (min, scale) and dequantize (f2, R28)
@@ -895,7 +700,6 @@ int hpz_bwd_gather(hpz_ctx* c, int layer, void* full_out, void* stream) {
   if (!full_out || (reinterpret_cast<uintptr_t>(full_out) & 15)) return fail(c, HPZ_EINVAL, "full_out null or not 16-byte aligned");
   Layer& L = c->layers[layer];
   if (L.fwd_t != c->t) return fail(c, HPZ_ESTATE, "layer %d: backward gather without its forward gather at step %lld", layer, (long long)c->t);
-  if (c->land_pending[layer] >= 0) return fail(c, HPZ_ESTATE, "layer %d: push gather not finished (hpz_fwd_gather_finish)", layer);
   if (L.bwd_t == c->t) return fail(c, HPZ_ESTATE, "layer %d already backward-gathered at step %lld", layer, (long long)c->t);
   if (c->order == HPZ_ORDER_PAPER)   // Alg. 1: "Repeat wait Until MemcpyD2D on L_k,second finishes" (host)
     HPZ_CUDA(c, cudaEventSynchronize(c->copy_ev[layer]));
@@ -951,7 +755,6 @@ int hpz_bwd_gather(hpz_ctx* c, int layer, void* full_out, void* stream) {
     for (int j = 0; j < c->world; ++j) p.rel.ptr[p.rel.n++] = c->flag(j, F_BWDP_DONE, layer, c->rank);
   p.rel.value = t1;
   p.sync = c->sync();
-  if (c->order == HPZ_ORDER_OFF) p.sync.xnode_mask = c->xnode_mask();   // ZeRO-3: every rank
   if (reads_prim) {
     // the primaries read here must still be W_t: they are, because Adam(t) waits for BWDP_DONE
     // and the sources' PRIMARY_READY >= t+1 is acquired per source (OFF) or below (EXACT)
@@ -1028,19 +831,11 @@ static int qgz_quantize(hpz_ctx* c, int layer, cudaStream_t s) {
   return HPZ_OK;
 }
 
-static int rs_push_phase(hpz_ctx* c, int layer, cudaStream_t s);
-
 int hpz_grads_ready(hpz_ctx* c, int layer, void* stream) {
   if (int rc = check_ready(c)) return rc;
   if (int rc = check_layer(c, layer)) return rc;
   const int slot = c->layers[layer].slot;
   if (c->slot_ready_sent[slot]) return fail(c, HPZ_ESTATE, "grads_ready already published for this use of the slot");
-  if (c->rs_push) {   // the owners never read my slot: nothing to publish, except the push itself
-    if (c->split_phases)
-      if (int rc = rs_push_phase(c, layer, static_cast<cudaStream_t>(stream))) return rc;
-    c->slot_ready_sent[slot] = 1;
-    return HPZ_OK;
-  }
   if (c->qgz_bits)
     if (int rc = qgz_quantize(c, layer, static_cast<cudaStream_t>(stream))) return rc;
   cudaError_t e = launch_release(grad_ready_list(c, slot), static_cast<cudaStream_t>(stream));
@@ -1050,77 +845,10 @@ int hpz_grads_ready(hpz_ctx* c, int layer, void* stream) {
   return HPZ_OK;
 }
 
-// Push RS: the landing slot (and its use index) a layer's push / reduce pair goes through;
-// assigned by the push, in the same order on every rank.
-static void rsl_assign(hpz_ctx* c, int layer) {
-  Layer& L = c->layers[layer];
-  if (L.rsl >= 0) return;
-  L.rsl = (int)(c->rs_seq % hpz_ctx::kRsl);
-  L.rsl_use = c->rs_seq / hpz_ctx::kRsl;
-  c->rs_seq += 1;
-}
-
-// Push RS parameters: push_on = my slices go out, reduce_on = I reduce my landing slot.
-static void build_rs_push(hpz_ctx* c, int layer, RSParams& p, bool push_on, bool reduce_on) {
-  Layer& L = c->layers[layer];
-  const int slot = L.slot;
-  const int b = L.rsl;
-  const uint64_t gb = (uint64_t)c->grad_bytes;
-  p = RSParams{};
-  p.push_on = push_on;
-  p.reduce_on = reduce_on;
-  p.self = c->rank;
-  for (int j = 0; j < c->world; ++j)
-    p.src[j] = reinterpret_cast<const float*>(
-        j == c->rank ? c->arena[c->rank] + c->off_slot[slot] + (uint64_t)c->rank * L.shard * gb
-                     : c->arena[c->rank] + c->off_rsl[b] + (uint64_t)j * c->rsl_stride);
-  p.out = reinterpret_cast<float*>(c->arena[c->rank] + L.off_gshard);
-  p.n_vec = L.shard / 4;
-  p.inv_p = (float)(1.0 / c->world);
-  p.chunk_ctr = c->rsc(c->rank, b);
-  p.chunk_target = (uint32_t)(c->world - 1);
-  p.push_src = c->arena[c->rank] + c->off_slot[slot];
-  p.push_shard_bytes = L.shard * (int64_t)gb;
-  for (int q = 0; q < c->world; ++q) {
-    if (q == c->rank) continue;
-    p.push_dst[q] = c->arena[q] + c->off_rsl[b] + (uint64_t)c->rank * c->rsl_stride;
-    p.push_ctr[q] = c->rsc(q, b);
-    p.push_free[q] = c->rl_flag(c->rank, b, q);
-  }
-  p.push_free_target = epoch(L.rsl_use);
-  p.done_ctr = c->ctr(C_RS, c->n_layers + slot);
-  if (reduce_on) {   // my landing slot b may be refilled by every pusher
-    for (int j = 0; j < c->world; ++j)
-      if (j != c->rank) p.rel.ptr[p.rel.n++] = c->rl_flag(j, b, c->rank);
-    p.rel.value = epoch(L.rsl_use + 1);
-  }
-  if (push_on) {     // E6 of my gradient slot: every read of it (the pushes) is complete
-    for (int j = 0; j < c->world; ++j) p.rel2.ptr[p.rel2.n++] = c->slot_flag(c->rank, S_RS_DONE, slot, j);
-    p.rel2.value = epoch(c->slot_use[slot] + 1);
-  }
-  p.sync = c->sync();
-}
-
-static int rs_push_phase(hpz_ctx* c, int layer, cudaStream_t s) {
-  rsl_assign(c, layer);
-  RSParams p;
-  build_rs_push(c, layer, p, true, false);
-  cudaError_t e = rs_launch(c, p, nullptr, s);
-  if (e != cudaSuccess) return fail(c, HPZ_ECUDA, "push reduce-scatter launch: %s", cudaGetErrorString(e));
-  c->launches += 1;
-  return HPZ_OK;
-}
-
 static void build_rs(hpz_ctx* c, int layer, RSParams& p) {
   Layer& L = c->layers[layer];
   const int slot = L.slot;
   const uint32_t u1 = epoch(c->slot_use[slot] + 1);
-  if (c->rs_push) {   // fused push + reduce, or the reduce after a split push phase
-    const bool pushed = L.rsl >= 0;
-    rsl_assign(c, layer);
-    build_rs_push(c, layer, p, !pushed, true);
-    return;
-  }
   p = RSParams{};
   for (int j = 0; j < c->world; ++j)
     p.src[j] = reinterpret_cast<const float*>(c->arena[j] + c->off_slot[slot] + (uint64_t)c->rank * L.shard * c->grad_bytes);
@@ -1134,7 +862,6 @@ static void build_rs(hpz_ctx* c, int layer, RSParams& p) {
   for (int j = 0; j < c->world; ++j) p.rel.ptr[p.rel.n++] = c->slot_flag(j, S_RS_DONE, slot, c->rank);   // E6
   p.rel.value = u1;
   p.sync = c->sync();
-  p.sync.xnode_mask = c->xnode_mask();   // src[j] = rank j
   if (c->qgz_bits) {
     for (int j = 0; j < c->world; ++j) {
       p.qcodes[j] = reinterpret_cast<const uint8_t*>(c->arena[j] + c->off_qcodes[slot]) + (int64_t)c->rank * L.shard / 2;
@@ -1145,7 +872,6 @@ static void build_rs(hpz_ctx* c, int layer, RSParams& p) {
 
 static void rs_issued(hpz_ctx* c, int layer) {
   Layer& L = c->layers[layer];
-  L.rsl = -1;
   c->slot_use[L.slot] += 1;
   c->slot_ready_sent[L.slot] = 0;
   L.rs_t = c->t;
@@ -1287,16 +1013,7 @@ int hpz_set_option(hpz_ctx* c, int option, int64_t value) {
       if (c->registered) return fail(c, HPZ_ESTATE, "qgZ must be chosen before hpz_register_flat_params");
       if (value != 0 && value != 4) return fail(c, HPZ_EINVAL, "qgZ bits must be 0 (off) or 4");
       if (value && c->grad_bytes != 4) return fail(c, HPZ_EINVAL, "qgZ quantizes fp32 gradients");
-      if (value && c->rs_push) return fail(c, HPZ_EINVAL, "qgZ is not available with the push reduce-scatter");
       c->qgz_bits = (int)value;
-      return HPZ_OK;
-    case HPZ_OPT_LANDING_BUFS:
-      if (c->registered) return fail(c, HPZ_ESTATE, "landing buffers must be chosen before hpz_register_flat_params");
-      if (value < 0 || value > 8) return fail(c, HPZ_EINVAL, "landing buffers must be in [0, 8]");
-      c->n_land = (int)value;
-      return HPZ_OK;
-    case HPZ_OPT_SPLIT_PHASES:
-      c->split_phases = value != 0;
       return HPZ_OK;
     case HPZ_OPT_MAX_CTAS:
       if (value < 0 || value > 1 << 20) return fail(c, HPZ_EINVAL, "max_ctas must be >= 0");
@@ -1317,16 +1034,6 @@ int hpz_set_option(hpz_ctx* c, int option, int64_t value) {
     case HPZ_OPT_RS_CTAS:
       if (value < 0 || value > 1 << 20) return fail(c, HPZ_EINVAL, "CTA caps must be >= 0");
       (option == HPZ_OPT_BWD_CTAS ? c->bwd_ctas : c->rs_ctas) = (int)value;
-      return HPZ_OK;
-    case HPZ_OPT_XNODE_MBPS:
-      if (value < 0 || value > 100000000) return fail(c, HPZ_EINVAL, "xnode_mbps must be in [0, 1e8]");
-      c->xnode_gbps = (float)value / 1000.0f;
-      return HPZ_OK;
-    case HPZ_OPT_RS_PUSH:
-      if (c->registered) return fail(c, HPZ_ESTATE, "the push reduce-scatter must be chosen before hpz_register_flat_params");
-      if (value != 0 && value != 1) return fail(c, HPZ_EINVAL, "rs_push must be 0 or 1");
-      if (value && c->qgz_bits) return fail(c, HPZ_EINVAL, "the push reduce-scatter carries fp32 / bf16 gradients, not qgZ codes");
-      c->rs_push = value != 0;
       return HPZ_OK;
     case HPZ_OPT_COPY_ENGINE:
       if (value != HPZ_COPY_LDG && value != HPZ_COPY_TMA) return fail(c, HPZ_EINVAL, "copy engine must be 0 (LDG) or 1 (TMA)");

@@ -7,15 +7,12 @@
 //   * gather_tma_kernel: producer bulk-loads a 32 KiB chunk of source j, then bulk-stores
 //     the same smem stage to the full buffer and (fused secondary store, a2) to the
 //     secondary; optional fingerprint consumer warps read the stage (a7).
-//   * rs_tma_kernel<P, ADAM, MODE, PUSH>: producer bulk-loads the P peers' gradient
-//     slices of a chunk (fp32 / bf16 / qgZ codes; + the master/m/v chunk when ADAM); up to
-//     512 consumer threads sum in the fixed pairwise-by-rank order (R7) and apply Adam (R8)
-//     from smem, storing with STG.128.  PUSH: a push warp bulk-stores this rank's slices
-//     into the owners' landing slots and the producer reduces from the local landing slot
-//     as per-chunk arrival counters complete (HPZ_OPT_RS_PUSH).
+//   * rs_tma_kernel<P, ADAM, MODE>: producer bulk-loads the P peers' gradient slices of a
+//     chunk (fp32 / bf16 / qgZ codes; + the master/m/v chunk when ADAM); up to 512
+//     consumer threads sum in the fixed pairwise-by-rank order (R7) and apply Adam (R8)
+//     from smem, storing with STG.128.
 //   * qgz_quantize_kernel / qwz_quantize_kernel / gather_qwz_kernel: the ZeRO++ qgZ / qwZ
 //     blockwise quantizers and the dequantizing forward gather (f1, f2).
-//   * push_gather_kernel: owner-driven forward gather into landing buffers.
 // Flags are acquired by the producer before the first bulk read of a source; a
 // fence.proxy.async orders the generic-proxy acquire before the async-proxy reads, and
 // the bulk stores are drained (wait_group 0) and proxy-fenced before the grid-wide
@@ -167,21 +164,6 @@ __global__ void __launch_bounds__(32 * (1 + kFpWarps), 1)
     if (lane == 0) {
       uint32_t waited = 0;
       bool war_done = false;
-      const uint64_t xt0 = p.sync.xnode_mask ? globaltimer() : 0;
-      uint64_t xbytes = 0;
-      float xns = 0.0f;   // ns per cross-node byte for this CTA (its share of the link)
-      if (p.sync.xnode_mask) {
-        uint64_t mine = 0;
-        for (int64_t k = 0; k < nk; ++k) {
-          int j;
-          int64_t off;
-          uint32_t bytes;
-          chunk_of(k, j, off, bytes);
-          if ((p.sync.xnode_mask >> j) & 1u) mine += bytes;
-        }
-        const float all = (float)p.src_bytes * (float)__popc(p.sync.xnode_mask & ((1u << n_src) - 1u));
-        xns = mine ? all / ((float)mine * p.sync.xnode_gbps) : 0.0f;
-      }
       auto issue_load = [&](int64_t k) {
         int j;
         int64_t off;
@@ -192,7 +174,6 @@ __global__ void __launch_bounds__(32 * (1 + kFpWarps), 1)
           fence_proxy_async();
           waited |= 1u << j;
         }
-        if ((p.sync.xnode_mask >> j) & 1u) xnode_pace(xt0, xbytes += bytes, xns);
         const int s = (int)(k % kGatherStages);
         mbar_expect_tx(&full_bar[s], bytes);
         tma_load(smem + (size_t)s * kGatherChunk, p.src[j] + off, bytes, &full_bar[s]);
@@ -272,63 +253,38 @@ __global__ void __launch_bounds__(32 * (1 + kFpWarps), 1)
 // ------------------------------------------------------------------ RS (+ Adam) (a5, a6)
 enum RsMode { RS_F32 = 0, RS_BF16 = 1, RS_QGZ = 2 };
 
-// Push reduce-scatter (HPZ_OPT_RS_PUSH) geometry: landing counters count chunks of this size.
-__host__ __device__ constexpr int rs_push_chunk(int P) { return P <= 4 ? 2048 : 1024; }
-
-template <int P, bool ADAM, int MODE, bool PUSH = false>
+template <int P, bool ADAM, int MODE>
 struct RsCfg {
   static constexpr bool QGZ = MODE == RS_QGZ;
   // per stage: P gradient slices (fp32, or qgZ int4 codes + (min, scale) per 64) (+ w, m, v);
   // qgZ chunks are longer so its small code/param copies stay >= 1 KiB / 256 B
   // P=1 (local, HBM-bound): 1024-element chunks keep 6 stages in flight; 2 <= P <= 8: 2048
-  static constexpr int kChunk =
-      PUSH ? rs_push_chunk(P) : (P >= 2 && P <= 8 ? 2 : 1) * (QGZ ? 2 * kRsChunk : kRsChunk);
+  static constexpr int kChunk = (P >= 2 && P <= 8 ? 2 : 1) * (QGZ ? 2 * kRsChunk : kRsChunk);
   static constexpr int kGradBytes = MODE == RS_BF16 ? 2 : 4;
   static constexpr int kCodeBytes = kChunk / 2;
   static constexpr int kParamBytes = kChunk / kQgzBlock * 8;
   static constexpr int kSrcBytes = QGZ ? kCodeBytes + kParamBytes : kChunk * kGradBytes;
   static constexpr int kWmvOff = P * kSrcBytes;
   static constexpr int kStageBytes = kWmvOff + (ADAM ? 3 * kChunk * 4 : 0);
-  // push ring: one unit = one chunk slice for one owner.  A stage is refilled as soon as its
-  // bulk store has READ it (kPushStages - 1 loads run ahead); up to kPushLag stores stay in
-  // flight before the oldest one's completion is awaited and the owner's chunk counter is
-  // incremented (remote write completion takes tens of microseconds under load)
-  static constexpr int kPushStages = 8;
-  static constexpr int kPushLag = 24;
-  static constexpr int kPushBatch = 16;
-  static constexpr int kPushWarps = 1;   // 2 measured: N=2 28.9 vs 27.2 ms, N=4 33.9 vs 34.3
-  static constexpr int kPushUnit = kChunk * kGradBytes;
-  static constexpr int kPushBytes = PUSH ? kPushStages * kPushUnit : 0;
-  static constexpr int kBudget = PUSH ? 216 * 1024 - kPushBytes : 200 * 1024;
+  static constexpr int kBudget = 200 * 1024;
   static constexpr int kStages = kBudget / kStageBytes >= 6 ? 6 : kBudget / kStageBytes;
   // consumer threads: one float4 per thread per chunk, at most 16 warps (idle polling
   // warps would steal issue slots from the working ones)
   static constexpr int kConsumers = kChunk / 4 < kRsMaxConsumers ? kChunk / 4 : kRsMaxConsumers;
-  static constexpr int kLead = PUSH ? 32 * (1 + kPushWarps) : 32;   // producer warp (+ push warps)
+  static constexpr int kLead = 32;   // producer warp
 };
 
-__device__ __forceinline__ void red_relaxed_sys_add(uint32_t* p, uint32_t v) {
-  asm volatile("red.relaxed.sys.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-template <int N>
-__device__ __forceinline__ void bulk_wait() {
-  asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
-}
-
-// Block = 1 producer warp (+ 1 push warp) + consumer warps.  Dynamic smem = kStages *
-// kStageBytes (+ the push ring).
-template <int P, bool ADAM, int MODE, bool PUSH>
-__global__ void __launch_bounds__(RsCfg<P, ADAM, MODE, PUSH>::kLead + RsCfg<P, ADAM, MODE, PUSH>::kConsumers, 1)
+// Block = 1 producer warp + consumer warps.  Dynamic smem = kStages * kStageBytes.
+template <int P, bool ADAM, int MODE>
+__global__ void __launch_bounds__(RsCfg<P, ADAM, MODE>::kLead + RsCfg<P, ADAM, MODE>::kConsumers, 1)
     rs_tma_kernel(const __grid_constant__ RSParams r, const __grid_constant__ AdamParams a) {
-  using C = RsCfg<P, ADAM, MODE, PUSH>;
+  using C = RsCfg<P, ADAM, MODE>;
   constexpr bool QGZ = C::QGZ;
   constexpr bool BF16 = MODE == RS_BF16;
   static_assert(C::kStages >= 2, "stage ring too small");
-  static_assert(!(PUSH && QGZ), "push RS carries fp32 / bf16 gradients");
   extern __shared__ __align__(1024) char smem[];
   __shared__ __align__(8) uint64_t full_bar[C::kStages];
   __shared__ __align__(8) uint64_t empty_bar[C::kStages];
-  __shared__ __align__(8) uint64_t push_bar[PUSH ? C::kPushStages : 1];
   const int64_t n = r.n_vec * 4;   // shard elements (multiple of 256)
   const int64_t total = (n + C::kChunk - 1) / C::kChunk;
   const int64_t nk = blockIdx.x < total ? (total - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
@@ -336,131 +292,32 @@ __global__ void __launch_bounds__(RsCfg<P, ADAM, MODE, PUSH>::kLead + RsCfg<P, A
 
   if (threadIdx.x == 0) {
     griddep_wait();                      // the caller's gradient writes (previous kernel) are done
-    if constexpr (!PUSH) {
-      if (r.ready.n) {
-        __threadfence_system();
-        release_all(r.ready);            // E5
-      }
-      wait_all(r.ready_wait, r.sync);    // E5: every rank's gradient slot is written
-      if (ADAM) wait_all(a.wait, a.sync);  // E2 (+E7): nobody still reads my primary
-      fence_proxy_async();
+    if (r.ready.n) {
+      __threadfence_system();
+      release_all(r.ready);              // E5
     }
+    wait_all(r.ready_wait, r.sync);      // E5: every rank's gradient slot is written
+    if (ADAM) wait_all(a.wait, a.sync);  // E2 (+E7): nobody still reads my primary
+    fence_proxy_async();
     for (int s = 0; s < C::kStages; ++s) {
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], C::kConsumers / 32);
     }
-    if constexpr (PUSH)
-      for (int s = 0; s < C::kPushStages; ++s) mbar_init(&push_bar[s], 1);
     fence_mbar_init();
   }
   __syncthreads();
 
-  if (PUSH && warp >= 1 && warp <= C::kPushWarps) {
-    // push warps: my gradient slot's slice of every chunk this CTA owns, for every other
-    // owner q: local bulk load -> smem -> bulk store into q's landing slot; once the store
-    // is complete, q's chunk counter is incremented.  Push warp pw takes every
-    // kPushWarps-th unit with its own stage ring, so one can sit in a fence while the
-    // other keeps issuing.
-    if (lane == 0 && r.push_on) {
-      constexpr int PW = C::kPushWarps;
-      constexpr int PM1 = P > 1 ? P - 1 : 1;   // push instantiations have P >= 2
-      constexpr int SP = C::kPushStages / PW;   // stages per push warp
-      constexpr int LAG = C::kPushLag / PW, BATCH = C::kPushBatch / PW;
-      const int pw = warp - 1;
-      for (int q = 0; q < P; ++q)
-        if (r.push_free[q] != nullptr) wait_geq(r.push_free[q], r.push_free_target, r.sync);
-      fence_proxy_async();
-      char* ring = smem + (size_t)C::kStages * C::kStageBytes + (size_t)pw * SP * C::kPushUnit;
-      uint64_t* bar = push_bar + pw * SP;
-      const int64_t nu_all = nk * PM1;
-      const int64_t nu = nu_all > pw ? (nu_all - pw + PW - 1) / PW : 0;   // my units i -> x = i*PW + pw
-      auto unit = [&](int64_t i, int& q, int64_t& w, uint32_t& bytes) {
-        const int64_t x = i * PW + pw;
-        const int64_t k = x / PM1;
-        const int d = (int)(x % PM1);
-        q = (r.self + 1 + (d + (int)(blockIdx.x % PM1)) % PM1) % P;   // never self; rotated per CTA
-        w = blockIdx.x + k * gridDim.x;                                       // global chunk index
-        const int64_t rem = n - w * C::kChunk;
-        bytes = (uint32_t)((rem < C::kChunk ? rem : C::kChunk) * C::kGradBytes);
-      };
-      auto issue = [&](int64_t i) {
-        int q;
-        int64_t w;
-        uint32_t bytes;
-        unit(i, q, w, bytes);
-        const int s = (int)(i % SP);
-        mbar_expect_tx(&bar[s], bytes);
-        tma_load(ring + (size_t)s * C::kPushUnit, r.push_src + q * r.push_shard_bytes + w * C::kChunk * C::kGradBytes,
-                 bytes, &bar[s]);
-      };
-      // Completed units are signalled in batches: one system-scope fence (it drains this
-      // thread's outstanding writes: measured 63 ms/step at N=2 with a release per unit vs
-      // 28 ms batched) then relaxed remote increments.
-      int64_t sig_from = 0;   // my units [sig_from, i] are complete but not yet signalled
-      auto signal_upto = [&](int64_t i) {
-        fence_proxy_async();
-        __threadfence_system();
-        for (int64_t y = sig_from; y <= i; ++y) {
-          int q;
-          int64_t w;
-          uint32_t bytes;
-          unit(y, q, w, bytes);
-          red_relaxed_sys_add(r.push_ctr[q] + w, 1u);
-        }
-        sig_from = i + 1;
-      };
-      constexpr int kAhead = SP - 1;
-      for (int64_t i = 0; i < nu && i < kAhead; ++i) issue(i);
-      for (int64_t i = 0; i < nu; ++i) {
-        const int s = (int)(i % SP);
-        mbar_wait(&bar[s], (uint32_t)((i / SP) & 1));
-        int q;
-        int64_t w;
-        uint32_t bytes;
-        unit(i, q, w, bytes);
-        tma_store(r.push_dst[q] + w * C::kChunk * C::kGradBytes, ring + (size_t)s * C::kPushUnit, bytes);
-        bulk_commit();
-        if (i >= LAG && (i - LAG + 1) % BATCH == 0) {
-          bulk_wait<LAG>();           // my units up to i - LAG have landed in their owners' memory
-          signal_upto(i - LAG);
-        }
-        if (i + kAhead < nu) {
-          bulk_wait_read<1>();        // the stage of unit i - 1 has been read by its store
-          issue(i + kAhead);
-        }
-      }
-      bulk_wait_all();
-      if (nu > 0) signal_upto(nu - 1);
-    }
-  } else if (warp == 0) {
-    if (lane == 0 && (!PUSH || r.reduce_on)) {
-      if constexpr (PUSH) {
-        if (ADAM) wait_all(a.wait, a.sync);   // E2 (+E7)
-        fence_proxy_async();
-      }
-      const uint64_t xt0 = r.sync.xnode_mask ? globaltimer() : 0;
-      uint64_t xbytes = 0;
+  if (warp == 0) {
+    if (lane == 0) {
       for (int64_t k = 0; k < nk; ++k) {
         const int s = (int)(k % C::kStages);
         if (k >= C::kStages) mbar_wait_bounded(&empty_bar[s], (uint32_t)(((k / C::kStages) - 1) & 1), r.sync);
         const int64_t e0 = (blockIdx.x + k * gridDim.x) * (int64_t)C::kChunk;
-        if constexpr (PUSH) {
-          // every other rank's slice of this chunk has landed in my landing slot
-          uint32_t* ctr = r.chunk_ctr + (blockIdx.x + k * gridDim.x);
-          wait_geq(ctr, r.chunk_target, r.sync);
-          *ctr = 0u;   // re-armed for the slot's next use (ordered before the RL_FREE release)
-          fence_proxy_async();
-        }
         const int64_t rem = n - e0;
         const uint32_t cnt = (uint32_t)(rem < C::kChunk ? rem : C::kChunk);
         const uint32_t bytes = cnt * 4;
         char* st = smem + (size_t)s * C::kStageBytes;
         const uint32_t src_bytes = QGZ ? cnt / 2 + cnt / kQgzBlock * 8 : (BF16 ? cnt * 2 : bytes);
-        if (r.sync.xnode_mask) {   // emulated inter-node link: pace the cross-node slices
-          xbytes += (uint64_t)src_bytes * __popc(r.sync.xnode_mask);
-          // chunks are dealt round-robin: every CTA carries ~1/gridDim.x of the bytes
-          xnode_pace(xt0, xbytes, (float)gridDim.x / r.sync.xnode_gbps);
-        }
         mbar_expect_tx(&full_bar[s], src_bytes * P + (ADAM ? 3 * bytes : 0));
 #pragma unroll
         for (int j = 0; j < P; ++j) {
@@ -483,7 +340,7 @@ __global__ void __launch_bounds__(RsCfg<P, ADAM, MODE, PUSH>::kLead + RsCfg<P, A
       }
       griddep_launch_dependents();
     }
-  } else if (!PUSH || r.reduce_on) {
+  } else {
     for (int64_t k = 0; k < nk; ++k) {
       const int s = (int)(k % C::kStages);
       mbar_wait(&full_bar[s], (uint32_t)((k / C::kStages) & 1));
@@ -559,9 +416,8 @@ __global__ void __launch_bounds__(RsCfg<P, ADAM, MODE, PUSH>::kLead + RsCfg<P, A
     }
   }
   if (last_cta(r.done_ctr)) {
-    release_all(r.rel);              // E6 (push: my landing slot is free again)
-    if (PUSH) release_all(r.rel2);   // push: E6 of my gradient slot (every push completed)
-    if (ADAM && (!PUSH || r.reduce_on)) release_all(a.rel);   // E1 (t+1)
+    release_all(r.rel);              // E6
+    if (ADAM) release_all(a.rel);    // E1 (t+1)
   }
 }
 
@@ -587,18 +443,28 @@ cudaError_t launch_pdl(void (*kernel)(KArgs...), int grid, int block, int smem, 
   return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
-template <int P, bool ADAM, int MODE, bool PUSH = false>
+// Opt a kernel into `smem` bytes of dynamic shared memory on the CURRENT device (the
+// attribute is per device: a process that drives several GPUs sets it once on each).
+template <auto Kernel>
+cudaError_t set_smem_attr(int smem) {
+  constexpr int kMaxDev = 64;
+  static bool done[kMaxDev] = {};   // one flag array per kernel (template argument)
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev >= 0 && dev < kMaxDev && done[dev]) return cudaSuccess;
+  e = cudaFuncSetAttribute(Kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e == cudaSuccess && dev >= 0 && dev < kMaxDev) done[dev] = true;
+  return e;
+}
+
+template <int P, bool ADAM, int MODE>
 cudaError_t launch_rs_tma_t(const RSParams& r, const AdamParams& a, int grid, cudaStream_t s) {
-  using C = RsCfg<P, ADAM, MODE, PUSH>;
-  const int smem = C::kStages * C::kStageBytes + C::kPushBytes;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e =
-        cudaFuncSetAttribute(rs_tma_kernel<P, ADAM, MODE, PUSH>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
-  return launch_pdl(rs_tma_kernel<P, ADAM, MODE, PUSH>, grid, C::kLead + C::kConsumers, smem, s, r, a);
+  using C = RsCfg<P, ADAM, MODE>;
+  const int smem = C::kStages * C::kStageBytes;
+  cudaError_t e = set_smem_attr<rs_tma_kernel<P, ADAM, MODE>>(smem);
+  if (e != cudaSuccess) return e;
+  return launch_pdl(rs_tma_kernel<P, ADAM, MODE>, grid, C::kLead + C::kConsumers, smem, s, r, a);
 }
 
 // qgZ quantizer: 4 threads per 64-element block, each holding 4 float4s (elements
@@ -656,112 +522,6 @@ __global__ void __launch_bounds__(256, 4) qgz_quantize_kernel(const __grid_const
           (uint16_t)(c[4 * u] | (c[4 * u + 1] << 4) | (c[4 * u + 2] << 8) | (c[4 * u + 3] << 12));
     if (sub == 0) q.params[b] = make_float2(mn, scale);
   }
-}
-
-// ------------------------------------------------------------------ push gather (a2, P2P stores)
-// Owner-driven forward gather: each CTA bulk-loads 32 KiB chunks of MY primary shard into
-// its stage ring (local HBM, read once) and bulk-stores every chunk to all P landing
-// buffers — NVLink posted writes, which this fabric carries ~6% faster than read
-// responses (profiles/r01_p2p_probe_n4.log) — plus the node secondaries whose slice holds
-// my shard (the fused secondary store).  A destination is written only after its owner
-// released FREE for this use of the buffer (its previous contents are dead and its
-// secondary is no longer read, E4); the last CTA releases DATA to every destination.
-template <bool FP>
-__global__ void __launch_bounds__(32 * (1 + kFpWarps), 1) push_gather_kernel(const __grid_constant__ PushParams p) {
-  extern __shared__ __align__(1024) char smem[];
-  __shared__ __align__(8) uint64_t full_bar[kGatherStages];
-  __shared__ __align__(8) uint64_t empty_bar[kGatherStages];
-  __shared__ unsigned long long fp_red[kFpWarps];
-  const int64_t total = (p.src_bytes + kGatherChunk - 1) / kGatherChunk;
-  const int64_t nk = blockIdx.x < total ? (total - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < kGatherStages; ++s) {
-      mbar_init(&full_bar[s], 1);
-      mbar_init(&empty_bar[s], kFpWarps);
-    }
-    fence_mbar_init();
-  }
-  __syncthreads();
-  auto chunk_of = [&](int64_t k, int64_t& off, uint32_t& bytes) {
-    off = (blockIdx.x + k * gridDim.x) * (int64_t)kGatherChunk;
-    const int64_t rem = p.src_bytes - off;
-    bytes = (uint32_t)(rem < kGatherChunk ? rem : kGatherChunk);
-  };
-  if (warp == 0) {
-    if (lane == 0) {
-      uint32_t freed = 0;
-      if (p.src_flag != nullptr) wait_geq(p.src_flag, p.src_target, p.sync);   // my Adam(t-1) done
-      fence_proxy_async();
-      auto issue_load = [&](int64_t k) {
-        int64_t off;
-        uint32_t bytes;
-        chunk_of(k, off, bytes);
-        const int s = (int)(k % kGatherStages);
-        mbar_expect_tx(&full_bar[s], bytes);
-        tma_load(smem + (size_t)s * kGatherChunk, p.src + off, bytes, &full_bar[s]);
-      };
-      const int64_t pre = nk < kGatherStages - 1 ? nk : kGatherStages - 1;
-      for (int64_t k = 0; k < pre; ++k) issue_load(k);
-      for (int64_t k = 0; k < nk; ++k) {
-        const int s = (int)(k % kGatherStages);
-        mbar_wait(&full_bar[s], (uint32_t)((k / kGatherStages) & 1));
-        int64_t off;
-        uint32_t bytes;
-        chunk_of(k, off, bytes);
-        const char* stage = smem + (size_t)s * kGatherChunk;
-        // rotate the destination order per CTA so the P links are loaded evenly
-        for (int d = 0; d < p.n_dst; ++d) {
-          const int q = (d + (int)blockIdx.x) % p.n_dst;
-          if (!((freed >> q) & 1u)) {
-            if (p.free_flag[q] != nullptr) wait_geq(p.free_flag[q], p.free_target, p.sync);
-            fence_proxy_async();
-            freed |= 1u << q;
-          }
-          tma_store(p.land[q] + off, stage, bytes);
-          if (p.sec[q] != nullptr) tma_store(p.sec[q] + off, stage, bytes);
-        }
-        bulk_commit();
-        if (k + kGatherStages - 1 < nk) {
-          bulk_wait_read<1>();
-          if (FP && k >= 1)
-            mbar_wait_bounded(&empty_bar[(k - 1) % kGatherStages], (uint32_t)(((k - 1) / kGatherStages) & 1), p.sync);
-          issue_load(k + kGatherStages - 1);
-        }
-      }
-      bulk_wait_all();
-      fence_proxy_async();
-    }
-  } else if (FP) {
-    uint64_t fp = 0;
-    const int ct = threadIdx.x - 32;
-    for (int64_t k = 0; k < nk; ++k) {
-      const int s = (int)(k % kGatherStages);
-      mbar_wait(&full_bar[s], (uint32_t)((k / kGatherStages) & 1));
-      int64_t off;
-      uint32_t bytes;
-      chunk_of(k, off, bytes);
-      const int4* st = reinterpret_cast<const int4*>(smem + (size_t)s * kGatherChunk);
-      const int64_t gv0 = p.word_base + off / 16;     // word index in the FULL buffer
-      for (uint32_t v = ct; v < bytes / 16; v += 32 * kFpWarps) fp += fp_word((uint32_t)(gv0 + v), st[v]);
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty_bar[s]);
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) fp += __shfl_xor_sync(0xffffffffu, fp, o);
-    if (lane == 0) fp_red[warp - 1] = fp;
-  }
-  __syncthreads();
-  if (FP && threadIdx.x == 0) {
-    // every landing buffer holds the same full parameters: my shard's checksum goes into
-    // every destination's forward accumulator (remote atomics over NVLink)
-    unsigned long long sum = 0;
-    for (int w = 0; w < kFpWarps; ++w) sum += fp_red[w];
-    if (sum)
-      for (int q = 0; q < p.n_dst; ++q)
-        if (p.fp_dst[q]) atomicAdd(p.fp_dst[q], sum);
-  }
-  if (last_cta(p.done_ctr)) release_all(p.rel);   // DATA: my shard is in every landing buffer
 }
 
 // ------------------------------------------------------------------ qwZ (f2)
@@ -882,21 +642,6 @@ __global__ void __launch_bounds__(32 + kQwConsumers, 1) gather_qwz_kernel(const 
   if (warp == 0) {
     if (lane == 0) {
       uint32_t waited = 0;
-      const uint64_t xt0 = p.sync.xnode_mask ? globaltimer() : 0;
-      uint64_t xbytes = 0;
-      float xns = 0.0f;   // ns per cross-node byte for this CTA (its share of the link)
-      if (p.sync.xnode_mask) {
-        uint64_t mine = 0;
-        for (int64_t k = 0; k < nk; ++k) {
-          int j;
-          int64_t off;
-          uint32_t cnt;
-          chunk_of(k, j, off, cnt);
-          if ((p.sync.xnode_mask >> j) & 1u) mine += cnt + cnt / kQwzBlock * 8;
-        }
-        const float all = (float)(n_el + n_el / kQwzBlock * 8) * (float)__popc(p.sync.xnode_mask & ((1u << n_src) - 1u));
-        xns = mine ? all / ((float)mine * p.sync.xnode_gbps) : 0.0f;
-      }
       for (int64_t k = 0; k < nk; ++k) {
         const int s = (int)(k % kQwStages);
         if (k >= kQwStages) mbar_wait_bounded(&empty_bar[s], (uint32_t)(((k / kQwStages) - 1) & 1), p.sync);
@@ -904,7 +649,6 @@ __global__ void __launch_bounds__(32 + kQwConsumers, 1) gather_qwz_kernel(const 
         int64_t off;
         uint32_t cnt;
         chunk_of(k, j, off, cnt);
-        if ((p.sync.xnode_mask >> j) & 1u) xnode_pace(xt0, xbytes += cnt + cnt / kQwzBlock * 8, xns);
         if (!((waited >> j) & 1u)) {
           if (p.src_flag[j] != nullptr) wait_geq(p.src_flag[j], p.src_target, p.sync);   // E1
           fence_proxy_async();
@@ -997,33 +741,11 @@ __global__ void __launch_bounds__(32 + kQwConsumers, 1) gather_qwz_kernel(const 
 
 cudaError_t launch_gather_tma(const GatherParams& p, int grid, cudaStream_t s) {
   const int smem = kGatherStages * kGatherChunk;
-  static bool attr_set[2] = {false, false};
   const bool fp = p.fp_acc != nullptr;
-  if (!attr_set[fp]) {
-    cudaError_t e = fp ? cudaFuncSetAttribute(gather_tma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)
-                       : cudaFuncSetAttribute(gather_tma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    attr_set[fp] = true;
-  }
+  cudaError_t e = fp ? set_smem_attr<gather_tma_kernel<true>>(smem) : set_smem_attr<gather_tma_kernel<false>>(smem);
+  if (e != cudaSuccess) return e;
   return fp ? launch_pdl(gather_tma_kernel<true>, grid, 32 * (1 + kFpWarps), smem, s, p)
             : launch_pdl(gather_tma_kernel<false>, grid, 32, smem, s, p);
-}
-
-cudaError_t launch_push_gather(const PushParams& p, int grid, cudaStream_t s) {
-  const int smem = kGatherStages * kGatherChunk;
-  static bool attr_set[2] = {false, false};
-  const bool fp = p.fp_dst[0] != nullptr;
-  if (!attr_set[fp]) {
-    cudaError_t e = fp ? cudaFuncSetAttribute(push_gather_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)
-                       : cudaFuncSetAttribute(push_gather_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    attr_set[fp] = true;
-  }
-  if (fp)
-    push_gather_kernel<true><<<grid, 32 * (1 + kFpWarps), smem, s>>>(p);
-  else
-    push_gather_kernel<false><<<grid, 32, smem, s>>>(p);
-  return cudaGetLastError();
 }
 
 cudaError_t launch_qwz_quantize(const QwzQuantParams& q, int grid, cudaStream_t s) {
@@ -1033,12 +755,8 @@ cudaError_t launch_qwz_quantize(const QwzQuantParams& q, int grid, cudaStream_t 
 
 cudaError_t launch_gather_qwz(const GatherParams& p, int grid, cudaStream_t s) {
   constexpr int smem = kQwStages * (kQwChunk + kQwChunk / kQwzBlock * 8);
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(gather_qwz_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  cudaError_t e = set_smem_attr<gather_qwz_kernel>(smem);
+  if (e != cudaSuccess) return e;
   gather_qwz_kernel<<<grid, 32 + kQwConsumers, smem, s>>>(p);
   return cudaGetLastError();
 }
@@ -1049,19 +767,8 @@ cudaError_t launch_qgz_quantize(const QuantParams& q, int grid, cudaStream_t s) 
 }
 
 template <int P>
-cudaError_t launch_rs_tma_p(const RSParams& r, const AdamParams* a, int grid, cudaStream_t s, int mode, bool push) {
+cudaError_t launch_rs_tma_p(const RSParams& r, const AdamParams* a, int grid, cudaStream_t s, int mode) {
   AdamParams none{};
-  if constexpr (P >= 2) {
-    if (push) {
-      switch (mode) {
-        case RS_F32: return a ? launch_rs_tma_t<P, true, RS_F32, true>(r, *a, grid, s) : launch_rs_tma_t<P, false, RS_F32, true>(r, none, grid, s);
-        case RS_BF16: return a ? launch_rs_tma_t<P, true, RS_BF16, true>(r, *a, grid, s) : launch_rs_tma_t<P, false, RS_BF16, true>(r, none, grid, s);
-        default: return cudaErrorInvalidValue;
-      }
-    }
-  } else {
-    if (push) return cudaErrorInvalidValue;
-  }
   switch (mode) {
     case RS_F32: return a ? launch_rs_tma_t<P, true, RS_F32>(r, *a, grid, s) : launch_rs_tma_t<P, false, RS_F32>(r, none, grid, s);
     case RS_BF16: return a ? launch_rs_tma_t<P, true, RS_BF16>(r, *a, grid, s) : launch_rs_tma_t<P, false, RS_BF16>(r, none, grid, s);
@@ -1070,13 +777,10 @@ cudaError_t launch_rs_tma_p(const RSParams& r, const AdamParams* a, int grid, cu
   }
 }
 
-int rs_push_chunk_elems(int world) { return rs_push_chunk(world); }
-
-cudaError_t launch_rs_tma(const RSParams& r, const AdamParams* a, int world, int grid, cudaStream_t s, int mode,
-                          bool push) {
+cudaError_t launch_rs_tma(const RSParams& r, const AdamParams* a, int world, int grid, cudaStream_t s, int mode) {
   switch (world) {
 #define HPZ_RST_CASE(P) \
-  case P: return launch_rs_tma_p<P>(r, a, grid, s, mode, push);
+  case P: return launch_rs_tma_p<P>(r, a, grid, s, mode);
     HPZ_RST_CASE(1) HPZ_RST_CASE(2) HPZ_RST_CASE(3) HPZ_RST_CASE(4) HPZ_RST_CASE(5) HPZ_RST_CASE(6)
     HPZ_RST_CASE(7) HPZ_RST_CASE(8) HPZ_RST_CASE(9) HPZ_RST_CASE(10) HPZ_RST_CASE(11) HPZ_RST_CASE(12)
     HPZ_RST_CASE(13) HPZ_RST_CASE(14) HPZ_RST_CASE(15) HPZ_RST_CASE(16)

@@ -28,11 +28,10 @@ EXPORTED = [
     "hpz_counters", "hpz_last_error", "hpz_version", "hpz_set_order", "hpz_set_verify",
     "hpz_set_timeout", "hpz_load_master", "hpz_synth_master", "hpz_fwd_gather", "hpz_bwd_gather",
     "hpz_grad_buffer", "hpz_grad_upload", "hpz_synth_grads", "hpz_grads_ready",
-    "hpz_reduce_scatter", "hpz_step", "hpz_reduce_scatter_adam", "hpz_set_option",
-    "hpz_landing_buffer", "hpz_fwd_gather_post", "hpz_fwd_gather_finish", "hpz_load_state",
+    "hpz_reduce_scatter", "hpz_step", "hpz_reduce_scatter_adam", "hpz_set_option", "hpz_load_state",
 ]
-OPT = {"store_grad_shard": 0, "ctas_per_sm": 1, "copy_engine": 2, "qgz": 3, "grad_dtype": 4, "qwz": 5, "max_ctas": 6, "landing_bufs": 7, "split_phases": 8, "rs_push": 9,
-       "bwd_ctas": 10, "rs_ctas": 11, "xnode_mbps": 12}
+OPT = {"store_grad_shard": 0, "ctas_per_sm": 1, "copy_engine": 2, "qgz": 3, "grad_dtype": 4, "qwz": 5, "max_ctas": 6,
+       "bwd_ctas": 10, "rs_ctas": 11}
 COPY = {"ldg": 0, "tma": 1}
 
 
@@ -94,9 +93,6 @@ def _load() -> ctypes.CDLL:
         "hpz_step": (c_int, [P, c_int, POINTER(hpz_adam), c_void_p]),
         "hpz_reduce_scatter_adam": (c_int, [P, c_int, POINTER(hpz_adam), c_void_p]),
         "hpz_set_option": (c_int, [P, c_int, c_int64]),
-        "hpz_landing_buffer": (c_int, [P, c_int, POINTER(c_void_p)]),
-        "hpz_fwd_gather_post": (c_int, [P, c_int, c_void_p, c_void_p]),
-        "hpz_fwd_gather_finish": (c_int, [P, c_int, c_void_p]),
         "hpz_load_state": (c_int, [P, c_int, c_void_p, c_void_p, c_void_p, c_int64, c_void_p]),
     }
     for name, (res, args) in sig.items():
@@ -269,20 +265,6 @@ def hpz_reduce_scatter_adam(ctx, layer: int, adam: hpz_adam, stream=None):
 def hpz_set_option(ctx, option: str | int, value: int):
     o = OPT[option] if isinstance(option, str) else option
     _check(ctx, "hpz_set_option", LIB.hpz_set_option(ctx, o, c_int64(int(value))))
-
-
-def hpz_landing_buffer(ctx, idx: int) -> int:
-    out = c_void_p()
-    _check(ctx, "hpz_landing_buffer", LIB.hpz_landing_buffer(ctx, idx, byref(out)))
-    return out.value
-
-
-def hpz_fwd_gather_post(ctx, layer: int, full_out_ptr: int, stream=None):
-    _check(ctx, "hpz_fwd_gather_post", LIB.hpz_fwd_gather_post(ctx, layer, c_void_p(full_out_ptr), _stream(stream)))
-
-
-def hpz_fwd_gather_finish(ctx, layer: int, stream=None):
-    _check(ctx, "hpz_fwd_gather_finish", LIB.hpz_fwd_gather_finish(ctx, layer, _stream(stream)))
 
 
 def hpz_load_state(ctx, layer: int, master_ptr: int, m_ptr: int, v_ptr: int, adam_steps_done: int, stream=None):

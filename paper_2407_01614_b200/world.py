@@ -75,12 +75,7 @@ def sum_over_ranks(values: list[float], device=None) -> list[float]:
     return t.tolist()
 
 
-def _register(ctx, numels, dtype, align, n_grad_slots, qgz=False, grad_dtype="f32", qwz=False, landing_bufs=0,
-              rs_push=False):
-    if rs_push:
-        H.hpz_set_option(ctx, "rs_push", 1)    # sizes the arena (landing slots): before register
-    if landing_bufs:
-        H.hpz_set_option(ctx, "landing_bufs", landing_bufs)
+def _register(ctx, numels, dtype, align, n_grad_slots, qgz=False, grad_dtype="f32", qwz=False):
     if qgz:
         H.hpz_set_option(ctx, "qgz", 4)        # sizes the arena: must precede register
     if qwz:
@@ -96,16 +91,13 @@ class EmulatedWorld:
     """P ranks on one GPU in one process (test harness for the multi-rank protocol)."""
 
     def __init__(self, numels, world, node_size, dtype="bf16", align=256, n_grad_slots=None,
-                 device=0, timeout_s=20.0, qgz=False, grad_dtype="f32", qwz=False, landing_bufs=0,
-                 rs_push=False):
+                 device=0, timeout_s=20.0, qgz=False, grad_dtype="f32", qwz=False):
         self.world, self.node_size, self.dtype = world, node_size, dtype
         self.numels = list(numels)
         self.ranks: list[RankCtx] = []
         for r in range(world):
             ctx = H.hpz_init(world, node_size, r, device)
-            _register(ctx, self.numels, dtype, align, n_grad_slots, qgz, grad_dtype, qwz, landing_bufs, rs_push)
-            if landing_bufs or rs_push:
-                H.hpz_set_option(ctx, "split_phases", 1)   # ranks share one stream: phases by hand
+            _register(ctx, self.numels, dtype, align, n_grad_slots, qgz, grad_dtype, qwz)
             H.hpz_arena_alloc(ctx)
             H.hpz_set_timeout(ctx, timeout_s)
             self.ranks.append(RankCtx(ctx, r, world, node_size, self.numels))
@@ -125,8 +117,7 @@ class DistWorld:
     """This process's single rank of a torch.distributed world (one GPU per process)."""
 
     def __init__(self, numels, node_size, dtype="bf16", align=256, n_grad_slots=None, device=None,
-                 group=None, timeout_s=20.0, qgz=False, grad_dtype="f32", qwz=False, landing_bufs=0,
-                 rs_push=False):
+                 group=None, timeout_s=20.0, qgz=False, grad_dtype="f32", qwz=False):
         import torch.distributed as dist
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
@@ -135,8 +126,7 @@ class DistWorld:
         self.numels = list(numels)
         dev = torch.cuda.current_device() if device is None else device
         ctx = H.hpz_init(self.world, node_size, self.rank, dev)
-        self.arena_bytes = _register(ctx, self.numels, dtype, align, n_grad_slots, qgz, grad_dtype, qwz,
-                                     landing_bufs, rs_push)
+        self.arena_bytes = _register(ctx, self.numels, dtype, align, n_grad_slots, qgz, grad_dtype, qwz)
         handle = H.hpz_arena_alloc(ctx)
         H.hpz_set_timeout(ctx, timeout_s)
         virtual_nodes(self.world, node_size)         # validates the topology early
@@ -162,10 +152,9 @@ def full_buffers(world_obj, n_bufs: int = 1, device=None):
 
 
 def run_step(ranks: list[RankCtx], fwd_out, bwd_out, adam, stream=None, grad_fn=None,
-             emulated: bool = False, layer_hook=None, fused: bool = False, push: bool = False):
+             emulated: bool = False, layer_hook=None, fused: bool = False):
     """One step of Algorithm 1 for the given ranks (all P in emulation, or this process's one).
 
-    push=True: fwd_out are landing buffers (owner-driven P2P-store gather).
     fused=True replaces each layer's reduce-scatter and the final optimizer step by the
     fused per-layer RS+Adam kernel (same bits).
     fwd_out[r](i) / bwd_out[r](i) return the device pointer of the caller-owned full buffer
@@ -174,17 +163,8 @@ def run_step(ranks: list[RankCtx], fwd_out, bwd_out, adam, stream=None, grad_fn=
     the next phase, in the SPMD order of the real world."""
     L = len(ranks[0].numels)
     for i in range(L):                                      # forward, i = 1..N (PAPER.md:100-106)
-        if emulated and push:
-            # push gather on a shared stream: every rank's post, then pushes, then finishes
-            for rc in ranks:
-                H.hpz_fwd_gather_post(rc.ctx, i, fwd_out[rc.rank](i), stream)
-            for rc in ranks:
-                H.hpz_fwd_gather(rc.ctx, i, fwd_out[rc.rank](i), stream)
-            for rc in ranks:
-                H.hpz_fwd_gather_finish(rc.ctx, i, stream)
-        else:
-            for rc in ranks:
-                H.hpz_fwd_gather(rc.ctx, i, fwd_out[rc.rank](i), stream)
+        for rc in ranks:
+            H.hpz_fwd_gather(rc.ctx, i, fwd_out[rc.rank](i), stream)
         if layer_hook:
             layer_hook("fwd", i)
     for i in reversed(range(L)):                            # backward, i = N..1 (PAPER.md:109-116)

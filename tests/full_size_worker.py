@@ -34,8 +34,7 @@ def main():
     node = world // 2 if world >= 2 else 1
     numels = shapes.numels(model)
     L = len(numels)
-    rs_push = os.environ.get("HPZ_FULL_RS_PUSH", "0") == "1"     # owner-driven reduce-scatter
-    W = DistWorld(numels, node, n_grad_slots=L, device=local, rs_push=rs_push) if world > 1 else \
+    W = DistWorld(numels, node, n_grad_slots=L, device=local) if world > 1 else \
         EmulatedWorld(numels, 1, 1, n_grad_slots=L, device=local)
     rc = W.ranks[0]
     ctx = rc.ctx

@@ -29,17 +29,16 @@ class ParityRun:
     def __init__(self, numels, world, node_size, dtype="bf16", align=256, order="fixed",
                  verify="exact", grad_kind="uniform", n_grad_slots=None, stock_schedule="program",
                  fused=False, store_grad_shard=True, copy_engine="tma", qgz=False, grad_dtype="f32",
-                 qwz=False, push=False, load_initial=True, rs_push=False):
+                 qwz=False, load_initial=True):
         from paper_2407_01614_b200 import hpz as H
         from paper_2407_01614_b200.world import EmulatedWorld
         self.H = H
         self.numels, self.P, self.Pp, self.dtype = list(numels), world, node_size, dtype
         self.grad_kind = grad_kind
         self.fused, self.store_grad_shard = fused, store_grad_shard
-        self.qgz, self.grad_dtype, self.qwz, self.push = qgz, grad_dtype, qwz, push
+        self.qgz, self.grad_dtype, self.qwz = qgz, grad_dtype, qwz
         self.w = EmulatedWorld(numels, world, node_size, dtype=dtype, align=align, n_grad_slots=n_grad_slots,
-                               timeout_s=10.0, qgz=qgz, grad_dtype=grad_dtype, qwz=qwz,
-                               landing_bufs=len(numels) if push else 0, rs_push=rs_push)
+                               timeout_s=10.0, qgz=qgz, grad_dtype=grad_dtype, qwz=qwz)
         self.o = O.HpzOracle(self.numels, world, node_size, align=align, param_dtype=dtype,
                              order="fixed" if order == "paper" else order,
                              stock_schedule=stock_schedule, grad_kind=grad_kind, qgz=qgz, grad_dtype=grad_dtype,
@@ -52,13 +51,8 @@ class ParityRun:
             H.hpz_set_option(rc.ctx, "copy_engine", H.COPY[copy_engine])
         tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
         L = len(self.numels)
-        if push:   # one landing buffer per layer (arena-owned, peer-mapped) so every layer stays checkable
-            from paper_2407_01614_b200.world import device_view
-            self.fwd = [[device_view(H.hpz_landing_buffer(rc.ctx, i), rc.infos[i].numel_pad, dtype)
-                         for i in range(L)] for rc in self.w.ranks]
-        else:
-            self.fwd = [[torch.zeros(rc.infos[i].numel_pad, dtype=tdt, device="cuda") for i in range(L)]
-                        for rc in self.w.ranks]
+        self.fwd = [[torch.zeros(rc.infos[i].numel_pad, dtype=tdt, device="cuda") for i in range(L)]
+                    for rc in self.w.ranks]
         self.bwd = [[torch.zeros(rc.infos[i].numel_pad, dtype=tdt, device="cuda") for i in range(L)] for rc in self.w.ranks]
         for i, n in enumerate(self.numels if load_initial else []):
             w0 = torch.from_numpy(S.layer_params(i, n)).cuda()
@@ -80,7 +74,7 @@ class ParityRun:
         self._keep = []
         run_step(self.w.ranks, [lambda i, r=r: self.fwd[r][i].data_ptr() for r in range(self.P)],
                  [lambda i, r=r: self.bwd[r][i].data_ptr() for r in range(self.P)], self.adam,
-                 stream=self.stream, grad_fn=self.grad_fn, emulated=True, fused=self.fused, push=self.push)
+                 stream=self.stream, grad_fn=self.grad_fn, emulated=True, fused=self.fused)
         torch.cuda.synchronize()
         rec = self.o.step() if run_oracle else None
         self.t += 1

@@ -35,8 +35,6 @@ def main():
     ap.add_argument("--qgz", type=int, default=0)
     ap.add_argument("--grad-dtype", default="f32")
     ap.add_argument("--qwz", type=int, default=0)
-    ap.add_argument("--push", type=int, default=0)
-    ap.add_argument("--rs-push", type=int, default=0)
     ap.add_argument("--grad-slots", type=int, default=0)
     args = ap.parse_args()
     local = int(os.environ["LOCAL_RANK"])
@@ -48,8 +46,7 @@ def main():
     numels = [int(x) for x in args.numels.split(",")]
     P, r = dist.get_world_size(), dist.get_rank()
     W = DistWorld(numels, args.node_size, timeout_s=20.0, qgz=bool(args.qgz), grad_dtype=args.grad_dtype,
-                  qwz=bool(args.qwz), landing_bufs=len(numels) if args.push else 0, rs_push=bool(args.rs_push),
-                  n_grad_slots=args.grad_slots or None)
+                  qwz=bool(args.qwz), n_grad_slots=args.grad_slots or None)
     rc = W.ranks[0]
     s = torch.cuda.current_stream()
     H.hpz_set_order(rc.ctx, args.order, stock_delay_us=args.stock_delay_us, stock_poison=args.order == "stock")
@@ -59,11 +56,7 @@ def main():
         w0 = torch.from_numpy(S.layer_params(i, n)).cuda()
         H.hpz_load_master(rc.ctx, i, w0.data_ptr(), s)
     torch.cuda.synchronize()
-    if args.push:   # arena landing buffers: owner-driven P2P-store forward gather
-        from paper_2407_01614_b200.world import device_view
-        fwd = [device_view(H.hpz_landing_buffer(rc.ctx, i), x.numel_pad, "bf16") for i, x in enumerate(rc.infos)]
-    else:
-        fwd = [torch.zeros(x.numel_pad, dtype=torch.bfloat16, device="cuda") for x in rc.infos]
+    fwd = [torch.zeros(x.numel_pad, dtype=torch.bfloat16, device="cuda") for x in rc.infos]
     bwd = [torch.zeros(x.numel_pad, dtype=torch.bfloat16, device="cuda") for x in rc.infos]
     o = O.HpzOracle(numels, P, args.node_size, order="off" if args.order == "off" else "fixed",
                     qgz=bool(args.qgz), grad_dtype=args.grad_dtype, qwz=bool(args.qwz))

@@ -163,33 +163,6 @@ def test_c_client_compiles_and_links(H, tmp_path):
     assert "numel_pad=207071232" in out.stdout
 
 
-def test_rs_push_option_sizes_arena(H):
-    """HPZ_OPT_RS_PUSH adds 2 landing slots of P x max-shard gradient elements (+ chunk
-    counters in the control region); it excludes qgZ and is a no-op at P = 1."""
-    numels = [1_000_000, 2048]
-    sizes = {}
-    for P, push, gd in [(8, 0, "f32"), (8, 1, "f32"), (8, 1, "bf16"), (1, 0, "f32"), (1, 1, "f32")]:
-        ctx = H.hpz_init(P, max(1, P // 2), 0, -1)
-        try:
-            if gd == "bf16":
-                H.hpz_set_option(ctx, "grad_dtype", H.HPZ_BF16)
-            H.hpz_set_option(ctx, "rs_push", push)
-            with pytest.raises(H.HpzError):
-                H.hpz_set_option(ctx, "qgz", 4) if push else H.hpz_set_option(ctx, "rs_push", 2)
-            sizes[(P, push, gd)] = H.hpz_register_flat_params(ctx, numels)
-            with pytest.raises(H.HpzError) as e:
-                H.hpz_set_option(ctx, "rs_push", 1 - push)
-            assert e.value.code == H.HPZ_ESTATE
-        finally:
-            H.hpz_finalize(ctx)
-    shard = 1_001_472 // 8                                     # N̂ = ceil(1e6 / 2048) * 2048
-    extra = sizes[(8, 1, "f32")] - sizes[(8, 0, "f32")]
-    assert 2 * 8 * shard * 4 <= extra <= 2 * 8 * shard * 4 + 3 * 65536 + 2 * 4096
-    # bf16 gradient slots: the landing slots hold bf16 too
-    assert sizes[(8, 1, "bf16")] < sizes[(8, 1, "f32")]
-    assert sizes[(1, 1, "f32")] == sizes[(1, 0, "f32")]
-
-
 def test_quantized_options_need_block_aligned_shards(H):
     for opt, val in (("qgz", 4), ("qwz", 8)):
         ctx = H.hpz_init(4, 2, 0, -1)
@@ -204,18 +177,20 @@ def test_quantized_options_need_block_aligned_shards(H):
 
 
 def test_experiment_options_validation(H):
-    """Grid caps and the emulated inter-node link: accepted ranges, rejected values, and
-    they may change after registration (they size nothing)."""
+    """Grid caps: accepted ranges, rejected values, and they may change after registration
+    (they size nothing); removed option numbers are rejected."""
     ctx = H.hpz_init(4, 2, 1, -1)
     try:
         H.hpz_register_flat_params(ctx, [100_000], 1, 256)
-        for opt, good, bad in (("bwd_ctas", 48, -1), ("rs_ctas", 100, -5), ("xnode_mbps", 25_000, -1)):
+        for opt, good, bad in (("bwd_ctas", 48, -1), ("rs_ctas", 100, -5)):
             H.hpz_set_option(ctx, opt, good)
             H.hpz_set_option(ctx, opt, 0)
             with pytest.raises(H.HpzError) as e:
                 H.hpz_set_option(ctx, opt, bad)
             assert e.value.code == H.HPZ_EINVAL
-        with pytest.raises(H.HpzError):
-            H.hpz_set_option(ctx, "xnode_mbps", 10 ** 9)
+        for gone in (7, 8, 9, 12):   # push gather / split phases / push RS / emulated inter-node link
+            with pytest.raises(H.HpzError) as e:
+                H.hpz_set_option(ctx, gone, 1)
+            assert e.value.code == H.HPZ_EINVAL
     finally:
         H.hpz_finalize(ctx)

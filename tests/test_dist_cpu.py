@@ -63,7 +63,7 @@ def test_bench_reference_arm_torchrun_gloo():
     """--impl reference under torchrun (2 ranks): rank 0 alone prints one JSON line."""
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
            "--master-addr", "127.0.0.1", "--master-port=29741", os.path.join(ROOT, "bench.py"),
-           "--impl", "reference", "--gpus", "2", "--steps", "1", "--warmup", "0", "--cpu-seconds", "0.5"]
+           "--impl", "reference", "--gpus", "2", "--steps", "1", "--warmup", "0", "--oracle-numel", "200000"]
     res = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT)
     assert res.returncode == 0, res.stderr[-2000:]
     lines = [l for l in res.stdout.splitlines() if l.startswith("{")]
@@ -72,3 +72,28 @@ def test_bench_reference_arm_torchrun_gloo():
     assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
     assert d["cpu_baseline"]["kind"] == "oracle"
     assert d["e2e"]["h2d_bytes_per_step"] == 0
+    assert d["cpu_baseline"]["cores"] >= 1 and "extrapolated_step_s" in d["cpu_baseline"]
+    assert d["config"]["world"] == 2 and d["config"]["node_size"] == 1
+
+
+def test_bench_reference_arm_without_launcher():
+    """The driver starts `python bench.py --impl reference --gpus N` without torchrun: the
+    oracle arm simulates all N ranks in this one process and prints one line (exit 0), with
+    the same `config` the GPU arm prints for that N (2 x 4 virtual nodes at N = 8)."""
+    cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--gpus", "8", "--steps", "2",
+           "--warmup", "1", "--oracle-numel", "65536"]
+    res = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT,
+                         env={k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")})
+    assert res.returncode == 0, res.stderr[-2000:]
+    lines = [l for l in res.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 8 and d["config"]["node_size"] == 4 and d["config"]["virtual_nodes"] == 2
+    assert d["steps"] == 2 and d["warmup"] == 1 and d["value"] > 0
+    import bench
+    import argparse
+    args = argparse.Namespace(model="falcon7b", order="fixed", verify="fingerprint", copy_engine="tma", overlap_bwd=0,
+                              qgz=False, grad_dtype="f32", qwz=False)
+    from paper_2407_01614_b200 import shapes
+    n = shapes.numels("falcon7b")
+    assert d["config"] == bench.make_config(args, 8, 4, len(n), sum(n), len(n))

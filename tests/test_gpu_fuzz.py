@@ -3,7 +3,7 @@
 Each case draws a world (P, P'), layer sizes (incl. layers smaller than P*A and ragged
 tails), parameter dtype, alignment and a legal combination of the options — copy engine,
 verification, fused RS+Adam, ordering (fixed / paper / off), bf16 or qgZ gradients, qwZ,
-push forward gather, push reduce-scatter, shared gradient slots — then checks two steps
+shared gradient slots — then checks two steps
 element by element with the same bars as test_gpu_parity (gathers, secondaries, RS,
 master/m/v, primaries bit-exact).  Seeded: the cases are the same every run."""
 import numpy as np
@@ -31,13 +31,11 @@ def _draw(seed):
         str(rng.choice(["fingerprint", "none"]))
     order = "fixed" if qwz else str(rng.choice(["fixed", "fixed", "paper", "off"]))
     grad_dtype = "bf16" if (not qgz and rng.random() < 0.3) else "f32"
-    push = bool(order == "fixed" and not qwz and rng.random() < 0.25)
-    rs_push = bool(P >= 2 and not qgz and rng.random() < 0.35)
     fused = bool(rng.random() < 0.6)
     slots = int(rng.integers(1, len(numels) + 1))
     return dict(numels=numels, world=P, node_size=Pp, dtype=dtype, align=align, copy_engine=engine,
-                verify=verify, order=order, grad_dtype=grad_dtype, qgz=qgz, qwz=qwz, push=push,
-                rs_push=rs_push, fused=fused, n_grad_slots=slots)
+                verify=verify, order=order, grad_dtype=grad_dtype, qgz=qgz, qwz=qwz,
+                fused=fused, n_grad_slots=slots)
 
 
 @pytest.mark.parametrize("case", range(N_CASES))

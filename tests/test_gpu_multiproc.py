@@ -67,24 +67,6 @@ def test_multiproc_parity_qwz_qgz(n, node):
     _run(n, node, extra=("--qwz", "1", "--qgz", "1"), port=30011 + n * 10 + node)
 
 
-@pytest.mark.parametrize("n,node", [(2, 1), (2, 2), (4, 2), (4, 1), (4, 4)])
-def test_multiproc_parity_push(n, node):
-    if n > NGPU:
-        pytest.skip(f"needs {n} GPUs")
-    _run(n, node, extra=("--push", "1"), port=30211 + n * 10 + node)
-
-
-@pytest.mark.parametrize("n,node,extra", [(2, 1, ()), (2, 2, ("--grad-dtype", "bf16")), (4, 2, ()),
-                                          (4, 4, ("--fused", "0")), (4, 2, ("--grad-slots", "2")),
-                                          (8, 4, ())])
-def test_multiproc_parity_rs_push(n, node, extra):
-    """Owner-driven reduce-scatter over NVLink (P2P bulk stores + per-chunk counters), one
-    fused push+reduce kernel per layer: bit-exact vs the oracle."""
-    if n > NGPU:
-        pytest.skip(f"needs {n} GPUs")
-    _run(n, node, extra=("--rs-push", "1", *extra), port=30411 + n * 10 + node + 3 * len(extra))
-
-
 def _mp_draw(seed):
     import numpy as np
     rng = np.random.default_rng(2000 + seed)
@@ -104,10 +86,6 @@ def _mp_draw(seed):
         extra += ["--grad-dtype", "bf16"]
     if qwz:
         extra += ["--qwz", "1"]
-    if order == "fixed" and not qwz and rng.random() < 0.3:
-        extra += ["--push", "1"]
-    if not qgz and rng.random() < 0.4:
-        extra += ["--rs-push", "1"]
     return n, node, order, extra
 
 

@@ -160,52 +160,6 @@ def test_parity_paper_order(P, Pp):
         run.close()
 
 
-@pytest.mark.parametrize("P,Pp", TOPOS)
-def test_parity_push_gather(P, Pp):
-    """Owner-driven forward gather (P2P TMA stores into arena landing buffers + fused
-    secondary stores): same bits as the oracle, fingerprints agree with the pulled backward."""
-    run = ParityRun(NUMELS, P, Pp, push=True, fused=True, verify="fingerprint")
-    try:
-        for _ in range(3):
-            _check_step(run, run.step())
-        c = run.counters()
-        assert c["timeouts"] == 0 and c["fp_mismatches"] == 0 and c["fp_checked"] == 3 * len(NUMELS) * P
-    finally:
-        run.close()
-
-
-@pytest.mark.parametrize("P,Pp", [(2, 1), (2, 2), (3, 1), (4, 2), (8, 4), (8, 8), (16, 4)])
-@pytest.mark.parametrize("fused", [True, False])
-@pytest.mark.parametrize("grad_dtype", ["f32", "bf16"])
-def test_parity_push_reduce_scatter(P, Pp, fused, grad_dtype):
-    """Owner-driven reduce-scatter (HPZ_OPT_RS_PUSH): every rank bulk-stores its slices into
-    the owners' landing slots, owners reduce as chunk counters complete — same R7 order, so
-    the reduced shard, master/m/v and primaries match the oracle bit for bit.  Two layers
-    share each of the 2 landing slots, so the landing-slot reuse edge is exercised."""
-    if grad_dtype == "bf16" and P in (3, 16):
-        pytest.skip("bf16 push covered at P = 2, 4, 8")
-    run = ParityRun(NUMELS, P, Pp, fused=fused, verify="fingerprint", grad_dtype=grad_dtype, rs_push=True)
-    try:
-        for _ in range(3):
-            _check_step(run, run.step())
-        c = run.counters()
-        assert c["timeouts"] == 0 and c["fp_mismatches"] == 0
-    finally:
-        run.close()
-
-
-def test_parity_push_reduce_scatter_shared_slots():
-    """Push RS with 2 gradient slots for 4 layers: the slot E6 comes from the pusher's own
-    kernel (its pushes are the only reads of the slot)."""
-    run = ParityRun(NUMELS, 4, 2, n_grad_slots=2, fused=True, verify="fingerprint", rs_push=True)
-    try:
-        for _ in range(3):
-            _check_step(run, run.step())
-        assert run.counters()["timeouts"] == 0
-    finally:
-        run.close()
-
-
 def test_parity_fused_off_order():
     run = ParityRun(NUMELS, 4, 2, order="off", fused=True)
     try:
@@ -528,54 +482,5 @@ def test_paper_order_with_one_reused_full_buffer():
             for rc in w.ranks:
                 got = buffer_view(rc, i, "master", "f32").cpu().numpy()
                 assert np.array_equal(got.view(np.uint32), o.state[i][rc.rank].master.view(np.uint32)), (i, rc.rank)
-    finally:
-        w.close()
-
-
-def test_xnode_throttle_paces_cross_node_reads_and_keeps_bits():
-    """HPZ_OPT_XNODE_MBPS (emulated constrained inter-node network): results stay bit-exact,
-    and a forward gather's cross-node bytes take at least bytes / rate."""
-    from paper_2407_01614_b200 import hpz as H
-    run = ParityRun(NUMELS, 4, 2, fused=True, verify="fingerprint")
-    try:
-        for rc in run.w.ranks:
-            H.hpz_set_option(rc.ctx, "xnode_mbps", 20_000)
-        for _ in range(2):
-            _check_step(run, run.step())
-        assert run.counters()["timeouts"] == 0
-    finally:
-        run.close()
-    from paper_2407_01614_b200.world import EmulatedWorld
-    n = 50_000_000
-    w = EmulatedWorld([n], 4, 2, timeout_s=20.0)
-    try:
-        s = torch.cuda.current_stream()
-        for rc in w.ranks:
-            H.hpz_synth_master(rc.ctx, 0, 1234, 2.0 ** -5, s)
-        out = torch.empty(w.ranks[0].infos[0].numel_pad, dtype=torch.bfloat16, device="cuda")
-        times = {}
-        for mbps in (0, 20_000):
-            H.hpz_set_option(w.ranks[0].ctx, "xnode_mbps", mbps)
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(s)
-            H.hpz_fwd_gather(w.ranks[0].ctx, 0, out.data_ptr(), s)
-            b.record(s)
-            torch.cuda.synchronize()
-            times[mbps] = a.elapsed_time(b)
-            for rc in w.ranks[1:]:                 # keep the SPMD sequence of the step consistent
-                H.hpz_fwd_gather(rc.ctx, 0, out.data_ptr(), s)
-            for rc in w.ranks:
-                H.hpz_bwd_gather(rc.ctx, 0, out.data_ptr(), s)
-            for rc in w.ranks:
-                H.hpz_synth_grads(rc.ctx, 0, 99, 2.0 ** -12, 0, s)
-            for rc in w.ranks:
-                H.hpz_grads_ready(rc.ctx, 0, s)
-            for rc in w.ranks:
-                H.hpz_reduce_scatter_adam(rc.ctx, 0, H.make_adam(), s)
-        torch.cuda.synchronize()
-        xbytes = w.ranks[0].infos[0].numel_pad * 2 // 2          # the other node's half of the parameters
-        floor_ms = xbytes / 20e9 * 1e3
-        assert times[20_000] >= 0.9 * floor_ms, times
-        assert times[20_000] <= 1.5 * floor_ms + times[0] + 1.0, times
     finally:
         w.close()

@@ -36,7 +36,7 @@ for line in sass.splitlines():
             if re.search(r"\b" + op + r"\b|\b" + op + r"\.", line):
                 ops[cur][op] += 1
 keep = re.compile(r"gather_tma_kernel|rs_tma_kernel<(1|2|4|8), true, 0, (false|true)>|qgz_quantize|qwz_quantize|"
-                  r"gather_qwz|push_gather|rs_tma_kernel<4, true, (1|2), false>|gather_kernel<true|\badam_kernel")
+                  r"gather_qwz|rs_tma_kernel<4, true, (1|2)>|gather_kernel<true|\badam_kernel")
 lines = ["# Resource usage and SASS evidence of the hot kernels (`python tools/resource_report.py`)", "",
          "| kernel | regs | static smem B | local (spill) B | UBLKCP (TMA bulk) | SYNCS (mbarrier) | MEMBAR | RED/ATOM | LDG/STG |",
          "|---|---|---|---|---|---|---|---|---|"]

@@ -28,8 +28,6 @@ def run(order, args, world, rank, local, node_size, numels):
     from synth import inputs as S
     kw = dict(n_grad_slots=2, timeout_s=60.0, qgz=args.qgz, qwz=args.qwz, grad_dtype=args.grad_dtype)
     if world > 1:
-        kw["rs_push"] = args.rs_push
-    if world > 1:
         W = DistWorld(numels, node_size, device=local, **kw)
     else:
         W = EmulatedWorld(numels, 1, 1, device=local, **kw)
@@ -79,7 +77,6 @@ def main():
     ap.add_argument("--qwz", action="store_true")
     ap.add_argument("--grad-dtype", default="f32")
     ap.add_argument("--verify", default="exact", choices=["exact", "fingerprint"])
-    ap.add_argument("--rs-push", action="store_true", help="owner-driven reduce-scatter (HPZ_OPT_RS_PUSH)")
     args = ap.parse_args()
     import torch
     import torch.distributed as dist
@@ -97,7 +94,7 @@ def main():
         res.append(run("stock", args, world, rank, local, node_size, numels))
     if rank == 0:
         out = {"config": f"C5 stress: {args.model} ({len(numels)} x {numels[0]} elements), P={world}, P'={node_size}",
-               "options": {"qgz": args.qgz, "qwz": args.qwz, "grad_dtype": args.grad_dtype, "rs_push": args.rs_push},
+               "options": {"qgz": args.qgz, "qwz": args.qwz, "grad_dtype": args.grad_dtype},
                "runs": res,
                "pass": res[0]["mismatched_elements"] == 0 and res[0]["fingerprint_mismatched_layers"] == 0
                and res[0]["timeouts"] == 0

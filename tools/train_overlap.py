@@ -39,8 +39,6 @@ def run(order, depth, args, world, rank, local, node_size):
     H.hpz_set_verify(rc.ctx, "fingerprint")
     if args.max_ctas:
         H.hpz_set_option(rc.ctx, "max_ctas", args.max_ctas)
-    if args.xnode_mbps:   # emulated constrained inter-node network between the virtual nodes
-        H.hpz_set_option(rc.ctx, "xnode_mbps", args.xnode_mbps)
     s = torch.cuda.current_stream()
     for i in range(args.layers):
         H.hpz_synth_master(rc.ctx, i, S.stream_key(S.SEED_PARAMS, i, 0, 0), args.init_scale, s)
@@ -81,8 +79,6 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--model", default="mlp", choices=["mlp", "transformer"])
     ap.add_argument("--qgz", action="store_true", help="INT4 gradient all-to-all (fp32 gradient slots)")
-    ap.add_argument("--xnode-mbps", type=int, default=0,
-                    help="emulate a constrained inter-node link: cross-virtual-node reads paced to this MB/s per GPU")
     ap.add_argument("--ffn", type=int, default=5632, help="transformer MLP width")
     ap.add_argument("--heads", type=int, default=16)
     ap.add_argument("--seq", type=int, default=1024, help="transformer sequence length (tokens = batch x seq)")
@@ -116,7 +112,7 @@ def main():
                 f"pre-norm transformer blocks (h {args.h}, {args.heads} heads, GELU MLP {args.ffn}, seq {args.seq}, "
                 f"activation checkpointing)")
         out = {"experiment": f"f3 Table 1/2 analog: {what}, bf16 compute + hpZ collectives on a comm stream",
-               "model": args.model, "qgz": args.qgz, "xnode_mbps": args.xnode_mbps, "world": world,
+               "model": args.model, "qgz": args.qgz, "world": world,
                "node_size": node_size, "h": args.h,
                "layers": args.layers,
                "tokens_per_rank": args.tokens, "max_ctas": args.max_ctas, "runs": res}
