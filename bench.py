@@ -498,8 +498,10 @@ def main():
     if not fused:
         share["adam"] = adam_ms
     dom = max(share, key=share.get)
+    # P' == P: the secondary is the primary (no secondary store)
+    sec_bytes = 0 if (node_size == world and not args.qwz) else ag_bytes / node_size
     if world == 1:
-        hbm_alg = {"fwd_gather": 3 * ag_bytes,     # read primary, write full out + secondary (P'=1)
+        hbm_alg = {"fwd_gather": 2 * ag_bytes + sec_bytes,   # read primary, write full out (+ secondary)
                    "bwd_gather": 2 * ag_bytes, "reduce_scatter": 2 * rs_bytes, "adam": adam_bytes,
                    # fused at P=1: read grad slot 4 + w,m,v 12; write w,m,v 12 + primary e
                    "reduce_scatter+adam": sum(x.shard for x in infos) * (28 + e)}
@@ -536,7 +538,7 @@ def main():
     # per rank and step: NVLink ingress as above; HBM = every byte each kernel must read or
     # write in this GPU's memory (incl. the shards it serves to peers)
     shard_sum = sum(x.shard for x in infos)
-    hbm_k = {"fwd_gather": ag_bytes + ag_bytes + ag_bytes / Pp,       # serve primary; write out + secondary
+    hbm_k = {"fwd_gather": ag_bytes + ag_bytes + sec_bytes,          # serve primary; write out (+ secondary)
              "bwd_gather": ag_bytes + ag_bytes,                       # serve secondary; write out
              # RS: my slot is read once in total (by its owners); fused Adam: w, m, v read +
              # written (24 B) and the primary refreshed (e); unfused: the fp32 shard written

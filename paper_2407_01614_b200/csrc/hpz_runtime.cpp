@@ -48,6 +48,11 @@ struct hpz_ctx {
   std::vector<uint8_t> slot_ready_sent;   // E5 already released for the current use
   uint64_t off_flags = 0, off_ctr = 0, off_fp = 0, off_stats = 0, ctrl_bytes = 0, arena_bytes = 0;
   bool registered = false, bound = false, owns_arena = false;
+  // P' == P (one node): the secondary slice of rank r is its own primary shard
+  // (Eq. (1) with P' = P), so the layout aliases it instead of storing a second copy; the
+  // forward gather writes no secondary and the backward gather reads the node's primaries
+  // (E1 acquire, E7 release).  Not with qwZ, whose secondary holds dequantized weights.
+  bool alias_sec = false;
   char* arena[kMaxWorld] = {};            // mapped arena base of every rank
   bool opened[kMaxWorld] = {};            // arena[j] was opened via IPC here
   int64_t t = 0;                          // current step (flag epochs)
@@ -290,6 +295,7 @@ int hpz_register_flat_params(hpz_ctx* c, int n_layers, const int64_t* numel, int
     return fail(c, HPZ_EINVAL, "qgZ needs align_elems to be a multiple of 256");
   c->dtype = param_dtype;
   c->elem = elem;
+  c->alias_sec = c->node_size == c->world && !c->qwz_bits;
   c->align = align_elems;
   c->n_layers = n_layers;
   c->n_slots = n_grad_slots;
@@ -328,8 +334,12 @@ int hpz_register_flat_params(hpz_ctx* c, int n_layers, const int64_t* numel, int
     L.off_m = off;         off = align_up(off + (uint64_t)L.shard * 4, kBufAlign);
     L.off_v = off;         off = align_up(off + (uint64_t)L.shard * 4, kBufAlign);
     L.off_gshard = off;    off = align_up(off + (uint64_t)L.shard * 4, kBufAlign);
-    L.off_secondary = off;
-    off = align_up(off + (uint64_t)L.sec_shard * elem, kBufAlign);
+    if (c->alias_sec) {
+      L.off_secondary = L.off_primary;   // secondary == primary (P' == P)
+    } else {
+      L.off_secondary = off;
+      off = align_up(off + (uint64_t)L.sec_shard * elem, kBufAlign);
+    }
     if (c->qwz_bits) {   // int8 codes + (min, scale) per 256 elements of the primary shard
       L.off_qw_codes = off;
       off = align_up(off + (uint64_t)L.shard, kBufAlign);
@@ -615,7 +625,8 @@ int hpz_fwd_gather(hpz_ctx* c, int layer, void* full_out, void* stream) {
   p.valid_bytes = L.numel * c->elem;
   const int l = c->local();
   const int nf = c->node_first();
-  if (c->order == HPZ_ORDER_FIXED) {
+  const bool write_sec = c->order == HPZ_ORDER_FIXED && !c->alias_sec;
+  if (write_sec) {
     // fused secondary store: my secondary slice l holds primaries l*k .. l*k+k-1 (R2 nesting)
     p.sec = c->arena[c->rank] + L.off_secondary;
     p.sec_lo = l * c->k;
@@ -625,7 +636,7 @@ int hpz_fwd_gather(hpz_ctx* c, int layer, void* full_out, void* stream) {
   }
   if (c->verify != HPZ_VERIFY_NONE) p.fp_acc = c->fp(layer, (int)(c->t & 1), 0);
   p.done_ctr = c->ctr(C_FWD, layer);
-  if (c->order == HPZ_ORDER_FIXED)
+  if (write_sec)
     for (int q = 0; q < c->node_size; ++q) p.rel.ptr[p.rel.n++] = c->flag(nf + q, F_SEC_READY, layer, c->rank);   // E3
   for (int j = 0; j < c->world; ++j) p.rel.ptr[p.rel.n++] = c->flag(j, F_FWD_DONE, layer, c->rank);            // E2
   p.rel.value = t1;
@@ -644,7 +655,7 @@ int hpz_fwd_gather(hpz_ctx* c, int layer, void* full_out, void* stream) {
   }
   if (e != cudaSuccess) return fail(c, HPZ_ECUDA, "fwd gather launch: %s", cudaGetErrorString(e));
   c->launches += 1;
-  if (c->order == HPZ_ORDER_STOCK || c->order == HPZ_ORDER_PAPER) {
+  if ((c->order == HPZ_ORDER_STOCK || c->order == HPZ_ORDER_PAPER) && !c->alias_sec) {
     // L_i,second <- empty(); async MemcpyD2D on another stream.  STOCK:
     // no edge to the backward AllGather (the race).  PAPER: the copy is
     // followed by an event the backward gather waits for on the HOST (Alg. 1 blue lines)
@@ -706,10 +717,12 @@ int hpz_bwd_gather(hpz_ctx* c, int layer, void* full_out, void* stream) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const uint32_t t1 = epoch(c->t + 1);
   const int nf = c->node_first();
-  const bool reads_prim = c->order == HPZ_ORDER_OFF || c->verify == HPZ_VERIFY_EXACT;
+  const bool from_prim = c->order == HPZ_ORDER_OFF || c->alias_sec;
+  const bool reads_prim = from_prim || c->verify == HPZ_VERIFY_EXACT;
   GatherParams p{};
-  if (c->order == HPZ_ORDER_OFF) {
-    // no hpZ: AllGather(L_i, P) from the primaries again (ZeRO-3 backward)
+  if (from_prim) {
+    // no hpZ: AllGather(L_i, P) from the primaries again (ZeRO-3 backward);
+    // P' == P: the node's secondaries ARE the primaries, same gather
     p.n_src = c->world;
     p.src_bytes = L.shard * c->elem;
     for (int j = 0; j < c->world; ++j) {
@@ -758,7 +771,7 @@ int hpz_bwd_gather(hpz_ctx* c, int layer, void* full_out, void* stream) {
   if (reads_prim) {
     // the primaries read here must still be W_t: they are, because Adam(t) waits for BWDP_DONE
     // and the sources' PRIMARY_READY >= t+1 is acquired per source (OFF) or below (EXACT)
-    if (c->order != HPZ_ORDER_OFF) {
+    if (!from_prim) {
       WaitList w{};
       for (int j = 0; j < c->world; ++j) w.ptr[w.n++] = c->flag(c->rank, F_PRIM_READY, layer, j);
       w.target = t1;
@@ -925,7 +938,7 @@ static void build_adam(hpz_ctx* c, int layer, const hpz_adam* a, AdamParams& p) 
   p.lr_wd = (float)(a->lr * a->weight_decay);
   const uint32_t t1 = epoch(c->t + 1);
   for (int j = 0; j < c->world; ++j) p.wait.ptr[p.wait.n++] = c->flag(c->rank, F_FWD_DONE, layer, j);   // E2
-  if (c->order == HPZ_ORDER_OFF || c->verify == HPZ_VERIFY_EXACT)
+  if (c->order == HPZ_ORDER_OFF || c->verify == HPZ_VERIFY_EXACT || c->alias_sec)
     for (int j = 0; j < c->world; ++j) p.wait.ptr[p.wait.n++] = c->flag(c->rank, F_BWDP_DONE, layer, j);   // E7
   p.wait.target = t1;
   p.done_ctr = c->ctr(C_ADAM, layer);

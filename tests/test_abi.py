@@ -100,9 +100,14 @@ def test_layout_matches_oracle(H):
                 assert (info.numel, info.numel_pad, info.shard, info.sec_shard) == \
                     (lay.numel, lay.numel_pad, lay.shard, lay.sec_shard)
                 elem = 2 if dtype == 1 else 4
-                offs = sorted([(info.off_primary, lay.shard * elem), (info.off_master, lay.shard * 4),
-                               (info.off_m, lay.shard * 4), (info.off_v, lay.shard * 4),
-                               (info.off_grad_shard, lay.shard * 4), (info.off_secondary, lay.sec_shard * elem)])
+                bufs = [(info.off_primary, lay.shard * elem), (info.off_master, lay.shard * 4),
+                        (info.off_m, lay.shard * 4), (info.off_v, lay.shard * 4),
+                        (info.off_grad_shard, lay.shard * 4)]
+                if P == Pp:      # secondary aliased to the primary
+                    assert info.off_secondary == info.off_primary and info.sec_shard == info.shard
+                else:
+                    bufs.append((info.off_secondary, lay.sec_shard * elem))
+                offs = sorted(bufs)
                 for (o, sz) in offs:
                     assert o % 4096 == 0 and o >= prev_end     # aligned, non-overlapping
                     prev_end = o + sz
@@ -161,6 +166,26 @@ def test_c_client_compiles_and_links(H, tmp_path):
     out = subprocess.run([str(exe)], capture_output=True, text=True)
     assert out.returncode == 0, out.stdout + out.stderr
     assert "numel_pad=207071232" in out.stdout
+
+
+def test_secondary_aliased_at_full_node(H):
+    """P' == P: the secondary is the primary — same arena offset, no extra bytes.
+    qwZ keeps a separate secondary (it holds the dequantized weights)."""
+    numels = [1_000_000, 4099]
+    sizes = {}
+    for P, Pp, qwz in [(4, 4, 0), (4, 2, 0), (4, 4, 1), (1, 1, 0)]:
+        ctx = H.hpz_init(P, Pp, 0, -1)
+        try:
+            if qwz:
+                H.hpz_set_option(ctx, "qwz", 8)
+            sizes[(P, Pp, qwz)] = H.hpz_register_flat_params(ctx, numels)
+            for i in range(len(numels)):
+                info = H.hpz_layer_info(ctx, i)
+                assert (info.off_secondary == info.off_primary) == (P == Pp and not qwz)
+        finally:
+            H.hpz_finalize(ctx)
+    # (4,2) stores a secondary of N̂/2 bf16 elements per layer that (4,4) does not
+    assert sizes[(4, 2, 0)] - sizes[(4, 4, 0)] >= (1_001_472 // 2) * 2
 
 
 def test_quantized_options_need_block_aligned_shards(H):

@@ -40,10 +40,13 @@ def _check_step(run: ParityRun, rec, check_all=True, check_secondary=True):
             grads = [O.bf16_to_f32(O.bf16_rne(g)) for g in grads]
         for r, rc in enumerate(run.w.ranks):
             st = run.o.state[i][r]
-            # a2 secondary store == oracle's Eq. (1) slice
+            # a2 secondary store == oracle's Eq. (1) slice; at P' == P the library aliases the
+            # secondary to the primary, which after the step holds W_{t+1}
+            aliased = run.Pp == P and not run.qwz
             if run.o.order == "fixed" and check_secondary:   # (paper maps to fixed)
                 sec = bits_np(buffer_view(rc, i, "secondary", dtype), dtype)
-                assert np.array_equal(sec, O.param_bits(st.sec, dtype)), f"secondary layer {i} rank {r}"
+                want = st.prim if aliased else st.sec
+                assert np.array_equal(sec, O.param_bits(want, dtype)), f"secondary layer {i} rank {r}"
             # a5 reduce-scatter bit-exact in the fixed order
             if run.store_grad_shard:
                 g_gpu = buffer_view(rc, i, "grad_shard", "f32").cpu().numpy()
@@ -156,6 +159,27 @@ def test_parity_paper_order(P, Pp):
             _check_step(run, run.step())
         c = run.counters()
         assert c["mismatches"] == 0 and c["timeouts"] == 0
+    finally:
+        run.close()
+
+
+@pytest.mark.parametrize("P", [1, 2, 4, 8])
+def test_secondary_aliased_when_node_is_the_world(P):
+    """P' == P: secondary == primary, so the library stores no second copy —
+    the secondary buffer IS the primary — the forward gather writes no secondary and the
+    backward gather (reading the node's primaries) still returns W_t bitwise, with the
+    optimizer ordered after it (E7).  EXACT verification re-reads the owners' primaries."""
+    from paper_2407_01614_b200 import hpz as H
+    run = ParityRun(NUMELS, P, P, fused=True, verify="exact", copy_engine="ldg")
+    try:
+        for rc in run.w.ranks:
+            for i in range(len(NUMELS)):
+                assert H.hpz_buffer(rc.ctx, i, "secondary") == (H.hpz_buffer(rc.ctx, i, "primary")[0],
+                                                                 run.w.ranks[0].infos[i].shard)
+        for _ in range(3):
+            _check_step(run, run.step())
+        c = run.counters()
+        assert c["mismatches"] == 0 and c["nan_reads"] == 0 and c["timeouts"] == 0
     finally:
         run.close()
 
