@@ -62,6 +62,9 @@ def parse():
     ap.add_argument("--trace", default=None, help="write a JSONL op trace (one line per hpz_* call) of the "
                     "instrumented breakdown steps to this file (per rank: FILE.rankR)")
     ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--graph", type=int, default=1,
+                    help="1: device-side epochs, one whole step captured in a CUDA graph and replayed each timed "
+                         "step (fixed/off orders); 0: every call issued eagerly")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-nccl", action="store_true")
@@ -263,6 +266,8 @@ def make_config(args, world, node_size, n_layers, n_params, n_slots):
             "world": world, "node_size": node_size, "virtual_nodes": world // node_size,
             "parallelism": f"hpZ dp{world} (P={world}, P'={node_size})", "order": args.order,
             "verify": args.verify, "copy_engine": args.copy_engine,
+            "launch": ("one step captured in a CUDA graph (device-side epochs), replayed per timed step"
+                       if args.graph and args.order in ("fixed", "off") else "eager calls"),
             "reduce_scatter": "pull" if world > 1 else "local",
             "overlap_bwd": (f"backward gathers on a second stream ({args.overlap_bwd} CTAs) beside "
                             f"the reduce-scatters") if args.overlap_bwd else None,
@@ -327,7 +332,11 @@ def main():
     if args.ctas_per_sm:
         H.hpz_set_option(ctx, "ctas_per_sm", args.ctas_per_sm)
     H.hpz_set_option(ctx, "copy_engine", H.COPY[args.copy_engine])
-    stream = torch.cuda.current_stream()
+    stream = torch.cuda.Stream(device=dev)      # a non-default stream: CUDA graphs capture on it
+    torch.cuda.set_stream(stream)
+    use_graph = bool(args.graph) and args.order in ("fixed", "off")
+    if use_graph:
+        H.hpz_set_option(ctx, "device_epoch", 1)     # epochs from the device: a step can be replayed
     gstream = torch.cuda.Stream(device=dev) if args.overlap_bwd else stream   # backward gathers
     if args.overlap_bwd:
         n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
@@ -421,6 +430,18 @@ def main():
 
     for _ in range(args.warmup):
         one_step()
+    graph = None
+    if use_graph:
+        # capture ONE whole step (every layer's gathers and fused RS+Adam); each replay is
+        # a new step: flag epochs and Adam scalars come from the device step counter
+        torch.cuda.synchronize()
+        l0 = H.hpz_counters(ctx)["launches"]
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=stream):
+            one_step()
+        graph_launches = H.hpz_counters(ctx)["launches"] - l0
+        graph.replay()            # one more warm-up step (the captured one)
+        torch.cuda.synchronize()
     H.hpz_counters(ctx, reset=True)
     launches0 = H.hpz_counters(ctx)["launches"]
     clocks = ClockSampler(list(range(world)) if rank == 0 else [])
@@ -433,14 +454,19 @@ def main():
     t_end = torch.cuda.Event(enable_timing=True)
     t_start.record(stream)
     for _ in range(args.steps):
-        one_step()
+        if graph is not None:
+            graph.replay()
+        else:
+            one_step()
     t_end.record(stream)
     barrier()
     clk = clocks.stop() if rank == 0 else None
     barrier()        # rank 0 spent ~0.25 s stopping the sampler: realign before the breakdown steps
     cnt = H.hpz_counters(ctx)
-    launches = cnt["launches"] - launches0
     K = args.steps
+    launches = graph_launches * K if graph is not None else cnt["launches"] - launches0
+    if graph is not None:
+        H.hpz_resync_step(ctx)    # host bookkeeping = the device step counter, for the eager steps below
     step_ms = t_start.elapsed_time(t_end) / K
     # per-kernel breakdown: extra instrumented steps (events around every call), after the
     # timed region; used for the breakdown and the roofline's per-kernel durations
@@ -484,7 +510,7 @@ def main():
     vals = max_over_ranks([step_ms, tot["fwd"], tot["bwd"], tot["rs"], tot["adam"],
                            tot["fwd"] + tot["bwd"] + tot["rs"] + tot["q"], tot["q"], tot["g"]], device=dev)
     stats = sum_over_ranks([cnt["fp_mismatches"], cnt["mismatches"], cnt["nan_reads"], cnt["timeouts"],
-                            cnt["fp_checked"], launches], device=dev)
+                            cnt["fp_checked"], launches, cnt["fp_fwd_mismatches"], cnt["fp_fwd_checked"]], device=dev)
     step_ms, fwd_ms, bwd_ms, rs_ms, adam_ms, coll_ms, q_ms, g_ms = vals
     # whole-job throughput of the step: the collectives' algorithmic bytes of all ranks per
     # step / the max-over-ranks time of the whole step (incl. the optimizer)
@@ -608,7 +634,12 @@ def main():
             "config": make_config(args, world, node_size, L, sum(x.numel for x in infos), n_slots),
             "stale_param_mismatches": {"fingerprint_layers": int(stats[0]), "exact_elements": int(stats[1]),
                                        "nan_reads": int(stats[2]), "timeouts": int(stats[3]),
-                                       "layers_checked": int(stats[4])},
+                                       "layers_checked": int(stats[4]),
+                                       "fwd_vs_owner_fingerprint_layers": int(stats[6]),
+                                       "fwd_layers_checked": int(stats[7]),
+                                       "what": "timed steps; FINGERPRINT: backward vs forward gather of every "
+                                               "layer (E3/E4) and forward gather vs the checksum the owners "
+                                               "emitted when writing their primaries (E1/E2); EXACT: elements"},
             "breakdown_steps": KB,
             "breakdown_ms_per_step": {"fwd_gather": round(fwd_ms, 3), "bwd_gather": round(bwd_ms, 3),
                                       rs_name: round(rs_ms, 3), "adam": round(adam_ms, 3),

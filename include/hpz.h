@@ -89,8 +89,13 @@ typedef enum { HPZ_ORDER_FIXED = 0, HPZ_ORDER_STOCK = 1, HPZ_ORDER_OFF = 2, HPZ_
  *  NONE        : off.
  *  FINGERPRINT : an order-independent 64-bit checksum of every gathered 16-byte word is
  *                accumulated by the forward and the backward gather of each layer; a
- *                layer whose two checksums differ counts one fp_mismatch (cheap, on in
- *                the bench).
+ *                layer whose two checksums differ counts one fp_mismatch (E3/E4: the
+ *                backward read stale / half-written secondaries).  The kernel that writes
+ *                a primary shard (Adam, the qwZ quantizer, load) also emits the checksum
+ *                of the words it wrote into every reader's slot for the step that will
+ *                gather them; a forward gather whose checksum differs from the owners'
+ *                counts one fp_fwd_mismatch (E1/E2: the forward read pre-step or
+ *                half-updated primaries).  Cheap; on in the bench.
  *  EXACT       : the backward gather additionally reads every element's owner primary
  *                and counts elements whose bits differ (mismatches) and NaN elements
  *                read (nan_reads).  Test/stress mode; doubles backward traffic. */
@@ -133,6 +138,8 @@ typedef struct {
   uint64_t fp_checked;      /* FINGERPRINT: layer-gathers compared                          */
   uint64_t timeouts;        /* device flag waits that timed out                              */
   uint64_t launches;        /* kernels this context launched (host count)                   */
+  uint64_t fp_fwd_mismatches; /* FINGERPRINT: forward gathers whose checksum != the owners'   */
+  uint64_t fp_fwd_checked;    /* FINGERPRINT: forward gathers compared with the owners'       */
 } hpz_counters_t;
 
 /* ---- lifecycle ------------------------------------------------------------------ */
@@ -186,6 +193,10 @@ HPZ_API int hpz_arena_ptr(const hpz_ctx* ctx, int rank, void** out);
 HPZ_API int hpz_buffer(const hpz_ctx* ctx, int layer, int kind, void** dev_ptr, int64_t* numel);
 /* The step t the next forward gather belongs to (0-based). */
 HPZ_API int hpz_current_step(const hpz_ctx* ctx, int64_t* t);
+/* Device epochs only (HPZ_OPT_DEVICE_EPOCH): after replaying a captured step graph, set the
+ * host's step bookkeeping to the device step counter (synchronizes the device).  Call
+ * between complete steps, before issuing hot-path calls eagerly again or capturing anew. */
+HPZ_API int hpz_resync_step(hpz_ctx* ctx);
 /* Read (synchronising the device) and optionally reset the detection counters. */
 HPZ_API int hpz_counters(hpz_ctx* ctx, hpz_counters_t* out, int reset);
 HPZ_API const char* hpz_last_error(const hpz_ctx* ctx);
@@ -315,11 +326,36 @@ typedef enum {
   HPZ_OPT_MAX_CTAS = 6,          /* cap on the CTAs of every launch (0 = whole GPU): bounds the SMs
                                     the collectives occupy while compute overlaps them (f3) */
   HPZ_OPT_BWD_CTAS = 10,         /* CTA cap of the backward gathers (0 = none) and ... */
-  HPZ_OPT_RS_CTAS = 11           /* ... of the reduce-scatters: with caps summing to at most the
+  HPZ_OPT_RS_CTAS = 11,          /* ... of the reduce-scatters: with caps summing to at most the
                                     SM count, a backward gather on one stream and a
                                     reduce-scatter on another run side by side (no kernel of
                                     either waits on the other, so they may share the GPU) */
+  HPZ_OPT_DEVICE_EPOCH = 13,     /* 0 (default) / 1: the rank's step counter lives in device
+                                    memory and every kernel derives its flag epochs (and the
+                                    Adam bias-correction scalars, from a host-filled table) from
+                                    it, so a whole step can be captured in a CUDA graph and
+                                    replayed (SURVEY §8(b) conventions).  The call that
+                                    completes a step (last hpz_step / hpz_reduce_scatter_adam)
+                                    advances the counter on its stream, so every other call of
+                                    the step must be stream-ordered before it and the next
+                                    step's calls after it (one graph replay after another on
+                                    one stream does this).  ORDER_FIXED / ORDER_OFF only (the
+                                    stock / paper side-stream copies cannot be captured).  Set
+                                    between steps with the device idle; bound arenas only. */
+  HPZ_OPT_FAULT = 14,            /* TEST ONLY, 0 = off: HPZ_FAULT_* bits remove an ordering
+                                    edge on purpose to prove the detector sees the violation */
+  HPZ_OPT_ALIAS_SECONDARY = 15   /* 1 (default) / 0, before hpz_register_flat_params.  With
+                                    P' = P (one node) the secondary slice of a rank IS its primary
+                                    shard (Eq. (1) with P' = P): the arena stores no
+                                    second copy, the forward gather writes no secondary and the
+                                    backward gather reads the node's primaries (E1 acquire, E7
+                                    release; every order behaves so, the stock race included).
+                                    0 keeps a separate secondary at P' = P — needed only to
+                                    reproduce the stock / paper copy on a one-node world.  No
+                                    effect with qwZ (its secondary holds dequantized weights). */
 } hpz_option;
+#define HPZ_FAULT_SKIP_E1 1   /* forward gathers read primaries without acquiring PRIMARY_READY */
+#define HPZ_FAULT_SKIP_E2 2   /* Adam overwrites the primary without waiting for its readers   */
 /* Copy engine of the gathers and the reduce-scatter: TMA 1-D bulk copies through a
  * shared-memory stage ring (cp.async.bulk, one persistent CTA per SM), or 16-byte
  * LDG/STG streams (several CTAs per SM).  EXACT verification always uses LDG/STG. */

@@ -3,6 +3,7 @@
 // grid completion, the fingerprint, and the R7 reduction / R8 Adam arithmetic that both
 // copy engines must evaluate identically.
 #pragma once
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -48,12 +49,24 @@ __device__ __forceinline__ bool wait_geq(const uint32_t* flag, uint32_t target, 
   return true;
 }
 
+// The rank's device step counter (device-epoch mode) or 0 (host epochs are absolute).
+// Written only by the epoch-advance kernel of the previous step's last call, so a plain
+// load after kernel start sees it.
+__device__ __forceinline__ uint32_t epoch_base(const SyncCommon& s) {
+  return s.epoch ? *(const volatile uint32_t*)s.epoch : 0u;
+}
+// A layer-flag value (one use per step): relative value + epoch.
+__device__ __forceinline__ uint32_t layer_epoch(uint32_t v, const SyncCommon& s) { return v + epoch_base(s); }
+
+// mul 0 means 1 (a layer flag: one use per step).
 __device__ __forceinline__ void wait_all(const WaitList& w, const SyncCommon& s) {
-  for (int k = 0; k < w.n; ++k) wait_geq(w.ptr[k], w.target, s);
+  const uint32_t target = w.target + (w.mul ? w.mul : 1u) * epoch_base(s);
+  for (int k = 0; k < w.n; ++k) wait_geq(w.ptr[k], target, s);
 }
 
-__device__ __forceinline__ void release_all(const ReleaseList& r) {
-  for (int k = 0; k < r.n; ++k) st_release_sys(r.ptr[k], r.value);
+__device__ __forceinline__ void release_all(const ReleaseList& r, const SyncCommon& s) {
+  const uint32_t v = r.value + (r.mul ? r.mul : 1u) * epoch_base(s);
+  for (int k = 0; k < r.n; ++k) st_release_sys(r.ptr[k], v);
 }
 
 // Last-CTA detection: returns true in thread 0 of the CTA that finishes last.  Every
@@ -88,6 +101,39 @@ __device__ __forceinline__ uint64_t fp_word(uint32_t gi, const int4& w) {
   return ((uint64_t)h2 << 32) | h;
 }
 
+// Fingerprint contribution of the primary elements a thread of an Adam kernel just wrote:
+// float4 index i of the shard.  fp32 primary: the float4 is one 16-byte word.  bf16
+// primary: the 8-byte halves of word i/2 are held by lanes i and i^1 of one warp, which
+// must both call this (warp-uniform: `valid` false contributes nothing but still shuffles).
+__device__ __forceinline__ uint64_t prim_word_fp(bool bf16, bool valid, int64_t i, const float4& w, const uint2& pk,
+                                                 int64_t word_base) {
+  if (!bf16) return valid ? fp_word((uint32_t)(word_base + i), *reinterpret_cast<const int4*>(&w)) : 0ull;
+  const uint32_t ox = __shfl_xor_sync(0xffffffffu, pk.x, 1);
+  const uint32_t oy = __shfl_xor_sync(0xffffffffu, pk.y, 1);
+  if (!valid || (i & 1)) return 0ull;
+  const int4 word = make_int4((int)pk.x, (int)pk.y, (int)ox, (int)oy);
+  return fp_word((uint32_t)(word_base + i / 2), word);
+}
+
+// Block-wide sum of per-thread fingerprints, added (thread 0) into every reader's slot of
+// the step parity.  Every thread of the block must call it.
+__device__ __forceinline__ void emit_fp(uint64_t fp, const FpEmit& e, const SyncCommon& s) {
+  __shared__ unsigned long long red[32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) fp += __shfl_xor_sync(0xffffffffu, fp, o);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) red[wid] = fp;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t = 0;
+    for (int k = 0; k < (int)((blockDim.x + 31) / 32); ++k) t += red[k];
+    const int par = (int)((e.par + epoch_base(s)) & 1u);
+    if (t)
+      for (int q = 0; q < e.n_dst; ++q) atomicAdd(e.dst[q] + par, t);
+  }
+}
+
 __device__ __forceinline__ float4 add4(const float4& a, const float4& b) {
   return make_float4(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y), __fadd_rn(a.z, b.z), __fadd_rn(a.w, b.w));
 }
@@ -105,14 +151,35 @@ __device__ __forceinline__ float4 pairwise_sum(float4 (&x)[P]) {
   return x[0];
 }
 
+// The step's bias-corrected scalars (step_size = lr / (1 - beta1^t), bc2_sqrt =
+// sqrt(1 - beta2^t)): host-computed for the call (host epochs), or looked up for the device
+// step (device epochs) in the host-filled table.
+__device__ __forceinline__ float2 adam_scalars(const AdamParams& p) {
+  if (p.tab == nullptr) return make_float2(p.step_size, p.bc2_sqrt);
+  int64_t k = p.tab_k0 + (int64_t)epoch_base(p.sync);
+  if (k >= p.tab_len) k = p.tab_len - 1;
+  return p.tab[k];
+}
+
 // One Adam element (reading R8), exactly the oracle's operation sequence: every
 // operation is an explicit round-to-nearest intrinsic, so nothing is contracted to fma.
-__device__ __forceinline__ void adam1(float& w, float& m, float& v, float g, const AdamParams& p) {
+// sc = adam_scalars(p).
+__device__ __forceinline__ void adam1(float& w, float& m, float& v, float g, const AdamParams& p, const float2 sc) {
   m = __fadd_rn(__fmul_rn(p.beta1, m), __fmul_rn(p.omb1, g));
   v = __fadd_rn(__fmul_rn(p.beta2, v), __fmul_rn(__fmul_rn(p.omb2, g), g));
-  const float d = __fadd_rn(__fdiv_rn(__fsqrt_rn(v), p.bc2_sqrt), p.eps);
+  const float d = __fadd_rn(__fdiv_rn(__fsqrt_rn(v), sc.y), p.eps);
   if (p.lr_wd != 0.0f) w = __fsub_rn(w, __fmul_rn(p.lr_wd, w));
-  w = __fsub_rn(w, __fmul_rn(p.step_size, __fdiv_rn(m, d)));
+  w = __fsub_rn(w, __fmul_rn(sc.x, __fdiv_rn(m, d)));
+}
+
+// bf16 RNE of 4 fp32 values packed as 8 bytes (cvt.rn.bf16x2.f32).
+__device__ __forceinline__ uint2 pack_bf16x4(const float4& w) {
+  __nv_bfloat162 lo = __floats2bfloat162_rn(w.x, w.y);
+  __nv_bfloat162 hi = __floats2bfloat162_rn(w.z, w.w);
+  uint2 pk;
+  pk.x = *reinterpret_cast<uint32_t*>(&lo);
+  pk.y = *reinterpret_cast<uint32_t*>(&hi);
+  return pk;
 }
 
 // Blockwise quantization code round-half-even((v - mn) / scale) clamped to [0, maxc] —
@@ -157,6 +224,30 @@ __device__ __forceinline__ void quant_codes(const float (&e)[N], float mn, float
     const int ci = __float2int_rn(q[k]);
     c[k] = ci < 0 ? 0 : (ci > maxc ? maxc : ci);
   }
+}
+
+// The last CTA of a gather: (forward) compare the gathered fingerprint with the one the
+// owners emitted when they wrote their primaries (catches a forward read of stale or
+// half-updated primaries: E1 / E2); (backward) compare it with the forward one (E3 / E4);
+// then release the kernel's flags.  Slots are zeroed for their next use two steps later.
+__device__ __forceinline__ void gather_finish(const GatherParams& p) {
+  const int par = (int)((p.fp_par + epoch_base(p.sync)) & 1u);
+  if (p.fp_exp != nullptr) {
+    wait_all(p.exp_wait, p.sync);      // every owner's emission for this step is complete
+    const unsigned long long got = *(volatile unsigned long long*)(p.fp_acc + 2 * par);
+    const unsigned long long want = atomicExch(p.fp_exp + par, 0ull);
+    atomicAdd(p.fpx_checked, 1ull);
+    if (got != want) atomicAdd(p.fpx_mism, 1ull);
+    __threadfence_system();            // the zeroed slot before the release that lets owners refill it
+  }
+  if (p.fp_a != nullptr) {
+    wait_all(p.cmp_wait, p.sync);      // the forward checksum of this step is complete
+    const unsigned long long a = atomicExch(p.fp_a + 2 * par, 0ull);
+    const unsigned long long b = atomicExch(p.fp_b + 2 * par, 0ull);
+    atomicAdd(p.fp_checked, 1ull);
+    if (a != b) atomicAdd(p.fp_mism, 1ull);
+  }
+  release_all(p.rel, p.sync);
 }
 
 }  // namespace

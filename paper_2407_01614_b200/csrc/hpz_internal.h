@@ -10,26 +10,47 @@ namespace hpz {
 
 constexpr int kMaxWorld = HPZ_MAX_WORLD;
 
-// Device-side error/timeout plumbing shared by every waiting kernel.
+// Device-side error/timeout plumbing shared by every waiting kernel, and the epoch base.
+//
+// Flag values are epochs.  Host-epoch mode (default): every value / target
+// in a kernel's parameters is absolute, computed on the host from its step counter, and
+// `epoch` is nullptr.  Device-epoch mode (HPZ_OPT_DEVICE_EPOCH, for CUDA-graph capture):
+// parameters hold values RELATIVE to the step the call was issued in, and the kernel adds
+// mul * (*epoch), the rank's step counter in device memory, which the call that completes
+// a step advances on the device.  A captured step therefore replays with fresh epochs.
 struct SyncCommon {
   uint64_t timeout_ns;                 // per-wait timeout
   uint32_t* abort_flag;                // local arena: set after the first timeout -> later waits skip
   unsigned long long* timeouts;        // local arena counter
   volatile uint32_t* host_err;         // host-mapped pinned word polled by the runtime
+  const uint32_t* epoch;               // device step counter (device-epoch mode) or nullptr
 };
 
-// A list of flags to release (st.release.sys of `value`), possibly in peer arenas.
+// A list of flags to release (st.release.sys of value + mul * epoch), possibly in peer arenas.
 struct ReleaseList {
   uint32_t* ptr[2 * kMaxWorld];
   int n;
   uint32_t value;
+  uint32_t mul;                        // per-step increment of the value (device-epoch mode)
 };
 
-// A list of local flags to acquire (ld.acquire.sys until >= target).
+// A list of local flags to acquire (ld.acquire.sys until >= target + mul * epoch).
 struct WaitList {
   const uint32_t* ptr[2 * kMaxWorld];
   int n;
   uint32_t target;
+  uint32_t mul;
+};
+
+// Owner-emitted primary fingerprints (a7, E1/E2 coverage): the kernel that writes a primary
+// shard (Adam, the qwZ quantizer, the init / resume refresh) adds the fingerprint of every
+// 16-byte word it wrote (the word as the forward gather will read it) into every reader's
+// "expected forward fingerprint" accumulator of the step that will gather it.
+struct FpEmit {
+  unsigned long long* dst[kMaxWorld];  // reader q's accumulator (parity-0 slot), nullptr: off
+  int n_dst;
+  int par;                             // parity of the gathering step (+ epoch in device mode)
+  int64_t word_base;                   // my shard's first 16-byte word in the full buffer
 };
 
 // Forward / backward gather (a2 / a4): out[j*src_bytes ...] = src[j][...] for j < n_src.
@@ -44,7 +65,9 @@ struct GatherParams {
   char* sec;
   int sec_lo, sec_hi;
   WaitList war;                        // acquired before the first secondary store (E4)
-  // verification (a7)
+  // verification (a7).  Accumulators are parity-0 slots; the step's slot is +2*par with
+  // par = (fp_par + epoch) & 1
+  int fp_par;
   unsigned long long* fp_acc;          // fingerprint accumulator (nullptr: off)
   const char* prim[kMaxWorld];         // EXACT: primaries of all ranks
   int64_t prim_bytes;                  // EXACT: bytes per primary shard
@@ -61,6 +84,12 @@ struct GatherParams {
   WaitList cmp_wait;
   unsigned long long* fp_mism;
   unsigned long long* fp_checked;
+  // forward: compare my gathered fingerprint (fp_acc) with the owners' emitted one (fp_exp,
+  // parity-0 slot, +par) once every owner released E1 (exp_wait); zero fp_exp
+  unsigned long long* fp_exp;
+  WaitList exp_wait;
+  unsigned long long* fpx_mism;
+  unsigned long long* fpx_checked;
   // qwZ (f2): src[j] are INT8 codes (1 byte per element, src_bytes = shard elements) and
   // qw_params[j] their (min, scale) per 256 elements; the kernel dequantizes to elem_bytes
   const float2* qw_params[kMaxWorld];
@@ -89,6 +118,7 @@ struct QwzQuantParams {
   int64_t n;
   uint32_t* done_ctr;
   ReleaseList rel;                     // E1
+  FpEmit fpe;                          // expected fingerprint of the DEQUANTIZED words
   SyncCommon sync;
 };
 
@@ -118,9 +148,15 @@ struct AdamParams {
   int prim_bf16;
   int64_t n_vec;                       // shard / 4
   float beta1, beta2, omb1, omb2, step_size, bc2_sqrt, eps, lr_wd;
+  // device-epoch mode: (step_size, bc2_sqrt) of 1-based Adam step k at tab[k - 1] (host
+  // computed in double, rounded once), k = tab_k0 + epoch + 1, clamped to the last entry
+  // (the scalars are constant from there on)
+  const float2* tab;
+  int64_t tab_k0, tab_len;
   WaitList wait;                       // E2 (+ backward-primary readers)
   uint32_t* done_ctr;
   ReleaseList rel;                     // E1 for t+1
+  FpEmit fpe;                          // expected fingerprint of the new primary (nullptr dst: off)
   SyncCommon sync;
 };
 
@@ -141,7 +177,12 @@ cudaError_t launch_qwz_quantize(const QwzQuantParams& q, int grid, cudaStream_t 
 // qwZ forward gather: TMA-pulls codes + params, dequantizes, STG to out (+ secondary).
 cudaError_t launch_gather_qwz(const GatherParams& p, int grid, cudaStream_t s);
 cudaError_t launch_wait(const WaitList& w, const SyncCommon& sync, cudaStream_t s);
-cudaError_t launch_release(const ReleaseList& r, cudaStream_t s);
+cudaError_t launch_release(const ReleaseList& r, const SyncCommon& sync, cudaStream_t s);
+// *epoch += 1 (device-epoch mode: the call that completes a step)
+cudaError_t launch_epoch_advance(uint32_t* epoch, cudaStream_t s);
+// fingerprint of a freshly written primary shard (init / resume) into the readers' slots
+cudaError_t launch_prim_fp(const void* prim, int64_t n_words, const FpEmit& fpe, const SyncCommon& sync, int grid,
+                           cudaStream_t s);
 cudaError_t launch_copy(void* dst, const void* src, int64_t bytes, int grid, cudaStream_t s);
 cudaError_t launch_refresh_primary(const float* master, void* prim, int prim_bf16, int64_t n, int grid, cudaStream_t s);
 cudaError_t launch_fill_u32(void* dst, uint32_t value, int64_t bytes, int grid, cudaStream_t s);

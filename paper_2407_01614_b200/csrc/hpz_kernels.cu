@@ -96,12 +96,13 @@ __global__ void __launch_bounds__(kThreads) gather_kernel(const __grid_constant_
   bool war_done = false;
   uint64_t fp = 0;
   unsigned long long mism = 0, nans = 0;
+  const uint32_t src_target = layer_epoch(p.src_target, p.sync);
 
   for (int64_t w = blockIdx.x; w < n_tiles; w += gridDim.x) {
     const int j = (int)(w % n_src);
     const int64_t tile = w / n_src;
     if (!((waited >> j) & 1u)) {
-      if (threadIdx.x == 0 && p.src_flag[j] != nullptr) wait_geq(p.src_flag[j], p.src_target, p.sync);
+      if (threadIdx.x == 0 && p.src_flag[j] != nullptr) wait_geq(p.src_flag[j], src_target, p.sync);
       __syncthreads();
       waited |= 1u << j;
     }
@@ -144,7 +145,8 @@ __global__ void __launch_bounds__(kThreads) gather_kernel(const __grid_constant_
 
   if (FP) {
     const uint64_t s = block_sum<unsigned long long>(fp);
-    if (threadIdx.x == 0 && s) atomicAdd(p.fp_acc, (unsigned long long)s);
+    const int par = (int)((p.fp_par + epoch_base(p.sync)) & 1u);
+    if (threadIdx.x == 0 && s) atomicAdd(p.fp_acc + 2 * par, (unsigned long long)s);
   }
   if (EXACT) {
     const unsigned long long sm = block_sum<unsigned long long>(mism);
@@ -154,16 +156,7 @@ __global__ void __launch_bounds__(kThreads) gather_kernel(const __grid_constant_
       if (sn) atomicAdd(p.nans, sn);
     }
   }
-  if (last_cta(p.done_ctr)) {
-    if (p.fp_a != nullptr) {
-      wait_all(p.cmp_wait, p.sync);    // the forward checksum of this step is complete
-      const unsigned long long a = atomicExch(p.fp_a, 0ull);
-      const unsigned long long b = atomicExch(p.fp_b, 0ull);
-      atomicAdd(p.fp_checked, 1ull);
-      if (a != b) atomicAdd(p.fp_mism, 1ull);
-    }
-    release_all(p.rel);
-  }
+  if (last_cta(p.done_ctr)) gather_finish(p);
 }
 
 // ------------------------------------------------------------------ reduce-scatter (a5)
@@ -178,7 +171,7 @@ __global__ void __launch_bounds__(kThreads) rs_kernel(const __grid_constant__ RS
   if (threadIdx.x == 0) {
     if (p.ready.n) {
       __threadfence_system();   // this rank's gradient slot (written earlier on the stream)
-      release_all(p.ready);
+      release_all(p.ready, p.sync);
     }
     wait_all(p.ready_wait, p.sync);
   }
@@ -208,17 +201,34 @@ __global__ void __launch_bounds__(kThreads) rs_kernel(const __grid_constant__ RS
       }
     }
   }
-  if (last_cta(p.done_ctr)) release_all(p.rel);
+  if (last_cta(p.done_ctr)) release_all(p.rel, p.sync);
 }
 
 // ------------------------------------------------------------------ Adam (a6)
 
+__device__ __forceinline__ uint2 store_prim(void* prim, int bf16, int64_t i, const float4& w) {
+  uint2 pk = make_uint2(0u, 0u);
+  if (bf16) {
+    pk = pack_bf16x4(w);
+    reinterpret_cast<uint2*>(prim)[i] = pk;
+  } else {
+    reinterpret_cast<float4*>(prim)[i] = w;
+  }
+  return pk;
+}
+
+// Grid-stride loops below run a warp-uniform trip count (per-lane predicate `ok`) so the
+// fingerprint shuffle of prim_word_fp always has the whole warp.
 __global__ void __launch_bounds__(kThreads) adam_kernel(const __grid_constant__ AdamParams p) {
   if (threadIdx.x == 0) wait_all(p.wait, p.sync);   // E2: peers finished reading my primary
   __syncthreads();
+  const float2 sc = adam_scalars(p);
+  const bool emit = p.fpe.n_dst > 0;
+  uint64_t fp = 0;
   const int64_t stride = (int64_t)gridDim.x * kThreads * kAdamUnroll;
-  for (int64_t base = (int64_t)blockIdx.x * kThreads * kAdamUnroll + threadIdx.x; base < p.n_vec;
-       base += stride) {
+  const int64_t warp0 = (int64_t)blockIdx.x * kThreads * kAdamUnroll + (threadIdx.x & ~31);
+  for (int64_t wb = warp0; wb < p.n_vec; wb += stride) {
+    const int64_t base = wb + (threadIdx.x & 31);
     float4 w[kAdamUnroll], m[kAdamUnroll], v[kAdamUnroll], g[kAdamUnroll];
 #pragma unroll
     for (int u = 0; u < kAdamUnroll; ++u) {
@@ -233,41 +243,23 @@ __global__ void __launch_bounds__(kThreads) adam_kernel(const __grid_constant__ 
 #pragma unroll
     for (int u = 0; u < kAdamUnroll; ++u) {
       const int64_t i = base + (int64_t)u * kThreads;
-      if (i < p.n_vec) {
-        adam1(w[u].x, m[u].x, v[u].x, g[u].x, p);
-        adam1(w[u].y, m[u].y, v[u].y, g[u].y, p);
-        adam1(w[u].z, m[u].z, v[u].z, g[u].z, p);
-        adam1(w[u].w, m[u].w, v[u].w, g[u].w, p);
+      const bool ok = i < p.n_vec;
+      uint2 pk = make_uint2(0u, 0u);
+      if (ok) {
+        adam1(w[u].x, m[u].x, v[u].x, g[u].x, p, sc);
+        adam1(w[u].y, m[u].y, v[u].y, g[u].y, p, sc);
+        adam1(w[u].z, m[u].z, v[u].z, g[u].z, p, sc);
+        adam1(w[u].w, m[u].w, v[u].w, g[u].w, p, sc);
         reinterpret_cast<float4*>(p.w)[i] = w[u];
         reinterpret_cast<float4*>(p.m)[i] = m[u];
         reinterpret_cast<float4*>(p.v)[i] = v[u];
-        if (p.prim_bf16) {
-          __nv_bfloat162 lo = __floats2bfloat162_rn(w[u].x, w[u].y);   // cvt.rn.bf16x2.f32
-          __nv_bfloat162 hi = __floats2bfloat162_rn(w[u].z, w[u].w);
-          uint2 pk;
-          pk.x = *reinterpret_cast<uint32_t*>(&lo);
-          pk.y = *reinterpret_cast<uint32_t*>(&hi);
-          reinterpret_cast<uint2*>(p.prim)[i] = pk;
-        } else {
-          reinterpret_cast<float4*>(p.prim)[i] = w[u];
-        }
+        pk = store_prim(p.prim, p.prim_bf16, i, w[u]);
       }
+      if (emit) fp += prim_word_fp(p.prim_bf16, ok, i, w[u], pk, p.fpe.word_base);
     }
   }
-  if (last_cta(p.done_ctr)) release_all(p.rel);   // E1: primary of step t+1 is ready
-}
-
-__device__ __forceinline__ void store_prim(void* prim, int bf16, int64_t i, const float4& w) {
-  if (bf16) {
-    __nv_bfloat162 lo = __floats2bfloat162_rn(w.x, w.y);
-    __nv_bfloat162 hi = __floats2bfloat162_rn(w.z, w.w);
-    uint2 pk;
-    pk.x = *reinterpret_cast<uint32_t*>(&lo);
-    pk.y = *reinterpret_cast<uint32_t*>(&hi);
-    reinterpret_cast<uint2*>(prim)[i] = pk;
-  } else {
-    reinterpret_cast<float4*>(prim)[i] = w;
-  }
+  if (emit) emit_fp(fp, p.fpe, p.sync);
+  if (last_cta(p.done_ctr)) release_all(p.rel, p.sync);   // E1: primary of step t+1 is ready
 }
 
 // ------------------------------------------------------------------ fused RS + Adam (a5 + a6)
@@ -281,14 +273,19 @@ __global__ void __launch_bounds__(kThreads) rs_adam_kernel(const __grid_constant
   if (threadIdx.x == 0) {
     if (r.ready.n) {
       __threadfence_system();
-      release_all(r.ready);                  // E5
+      release_all(r.ready, r.sync);          // E5
     }
     wait_all(r.ready_wait, r.sync);          // E5: every rank's slot is written
     wait_all(a.wait, a.sync);                // E2 (+E7): nobody still reads my primary
   }
   __syncthreads();
+  const float2 sc = adam_scalars(a);
+  const bool emit = a.fpe.n_dst > 0;
+  uint64_t fp = 0;
   const int64_t stride = (int64_t)gridDim.x * kThreads * U;
-  for (int64_t base = (int64_t)blockIdx.x * kThreads * U + threadIdx.x; base < r.n_vec; base += stride) {
+  const int64_t warp0 = (int64_t)blockIdx.x * kThreads * U + (threadIdx.x & ~31);
+  for (int64_t wb = warp0; wb < r.n_vec; wb += stride) {
+    const int64_t base = wb + (threadIdx.x & 31);
     float4 x[U][P];
     float4 w[U], m[U], v[U];
 #pragma unroll
@@ -305,27 +302,31 @@ __global__ void __launch_bounds__(kThreads) rs_adam_kernel(const __grid_constant
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t i = base + (int64_t)u * kThreads;
-      if (i < r.n_vec) {
+      const bool ok = i < r.n_vec;
+      uint2 pk = make_uint2(0u, 0u);
+      if (ok) {
         float4 g = pairwise_sum<P>(x[u]);
         g.x = __fmul_rn(g.x, r.inv_p);
         g.y = __fmul_rn(g.y, r.inv_p);
         g.z = __fmul_rn(g.z, r.inv_p);
         g.w = __fmul_rn(g.w, r.inv_p);
         if (r.out) reinterpret_cast<float4*>(r.out)[i] = g;    // optional (inspection/tests)
-        adam1(w[u].x, m[u].x, v[u].x, g.x, a);
-        adam1(w[u].y, m[u].y, v[u].y, g.y, a);
-        adam1(w[u].z, m[u].z, v[u].z, g.z, a);
-        adam1(w[u].w, m[u].w, v[u].w, g.w, a);
+        adam1(w[u].x, m[u].x, v[u].x, g.x, a, sc);
+        adam1(w[u].y, m[u].y, v[u].y, g.y, a, sc);
+        adam1(w[u].z, m[u].z, v[u].z, g.z, a, sc);
+        adam1(w[u].w, m[u].w, v[u].w, g.w, a, sc);
         reinterpret_cast<float4*>(a.w)[i] = w[u];
         reinterpret_cast<float4*>(a.m)[i] = m[u];
         reinterpret_cast<float4*>(a.v)[i] = v[u];
-        store_prim(a.prim, a.prim_bf16, i, w[u]);
+        pk = store_prim(a.prim, a.prim_bf16, i, w[u]);
       }
+      if (emit) fp += prim_word_fp(a.prim_bf16, ok, i, w[u], pk, a.fpe.word_base);
     }
   }
+  if (emit) emit_fp(fp, a.fpe, a.sync);
   if (last_cta(r.done_ctr)) {
-    release_all(r.rel);   // E6: my reads of every slot are done
-    release_all(a.rel);   // E1: my primary of step t+1 is ready
+    release_all(r.rel, r.sync);   // E6: my reads of every slot are done
+    release_all(a.rel, a.sync);   // E1: my primary of step t+1 is ready
   }
 }
 
@@ -334,11 +335,24 @@ __global__ void wait_kernel(const WaitList w, const SyncCommon s) {
   if (threadIdx.x == 0) wait_all(w, s);
 }
 
-__global__ void release_kernel(const ReleaseList r) {
+__global__ void release_kernel(const ReleaseList r, const SyncCommon s) {
   if (threadIdx.x == 0) {
     __threadfence_system();
-    release_all(r);
+    release_all(r, s);
   }
+}
+
+__global__ void epoch_advance_kernel(uint32_t* epoch) {
+  if (threadIdx.x == 0) *epoch += 1u;
+}
+
+// Fingerprint of a primary shard written by init / resume (n_words 16-byte words).
+__global__ void __launch_bounds__(kThreads) prim_fp_kernel(const int4* prim, int64_t n_words, const FpEmit e,
+                                                           const SyncCommon s) {
+  uint64_t fp = 0;
+  for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n_words; i += (int64_t)gridDim.x * kThreads)
+    fp += fp_word((uint32_t)(e.word_base + i), ld_stream(prim + i));
+  emit_fp(fp, e, s);
 }
 
 __global__ void __launch_bounds__(kThreads) copy_kernel(int4* dst, const int4* src, int64_t n_vec) {
@@ -484,8 +498,19 @@ cudaError_t launch_wait(const WaitList& w, const SyncCommon& sync, cudaStream_t 
   return cudaGetLastError();
 }
 
-cudaError_t launch_release(const ReleaseList& r, cudaStream_t s) {
-  release_kernel<<<1, 32, 0, s>>>(r);
+cudaError_t launch_release(const ReleaseList& r, const SyncCommon& sync, cudaStream_t s) {
+  release_kernel<<<1, 32, 0, s>>>(r, sync);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_epoch_advance(uint32_t* epoch, cudaStream_t s) {
+  epoch_advance_kernel<<<1, 32, 0, s>>>(epoch);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_prim_fp(const void* prim, int64_t n_words, const FpEmit& fpe, const SyncCommon& sync, int grid,
+                           cudaStream_t s) {
+  prim_fp_kernel<<<grid, kThreads, 0, s>>>(reinterpret_cast<const int4*>(prim), n_words, fpe, sync);
   return cudaGetLastError();
 }
 

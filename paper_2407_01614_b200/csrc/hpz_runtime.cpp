@@ -32,6 +32,7 @@ struct Layer {
   int slot;
   // host bookkeeping of the step t the layer's ops were issued for (-1: never)
   int64_t fwd_t = -1, bwd_t = -1, rs_t = -1, step_t = -1;
+  int64_t fpx_t = -1;    // step whose forward gather the owner's last fingerprint emission targets
 };
 
 }  // namespace
@@ -53,6 +54,7 @@ struct hpz_ctx {
   // forward gather writes no secondary and the backward gather reads the node's primaries
   // (E1 acquire, E7 release).  Not with qwZ, whose secondary holds dequantized weights.
   bool alias_sec = false;
+  bool alias_opt = true;                  // HPZ_OPT_ALIAS_SECONDARY
   char* arena[kMaxWorld] = {};            // mapped arena base of every rank
   bool opened[kMaxWorld] = {};            // arena[j] was opened via IPC here
   int64_t t = 0;                          // current step (flag epochs)
@@ -75,6 +77,14 @@ struct hpz_ctx {
   int max_ctas = 0;                       // cap on every grid (0 = all SMs)
   int bwd_ctas = 0, rs_ctas = 0;          // caps of the backward gathers / reduce-scatters (overlap)
   std::vector<uint64_t> off_qcodes, off_qparams;   // per grad slot (qgZ)
+  std::vector<uint32_t> slot_uses;        // layers sharing each gradient slot (uses per step)
+  uint64_t off_fpx = 0, off_epoch = 0;    // expected-forward-fingerprint slots; device step counter
+  std::vector<int64_t> fpx_for;           // per layer: the step whose forward the last emission targets
+  bool dev_epoch = false;                 // HPZ_OPT_DEVICE_EPOCH
+  int fault = 0;                          // HPZ_OPT_FAULT (test-only ordering faults)
+  float2* adam_tab = nullptr;             // device-epoch Adam scalars (cudaMalloc'd)
+  int64_t adam_tab_len = 0;
+  double adam_tab_key[4] = {-1, -1, -1, -1};
   std::string err;
 
   // ---- arena addressing (identical on every rank) ----
@@ -93,18 +103,31 @@ struct hpz_ctx {
   unsigned long long* fp(int layer, int parity, int which) const {
     return reinterpret_cast<unsigned long long*>(arena[rank] + off_fp) + ((uint64_t)layer * 2 + parity) * 2 + which;
   }
-  // stats: 0 mismatches, 1 nans, 2 fp_mism, 3 fp_checked, 4 timeouts, 5 abort flag (u32)
+  // stats: 0 mismatches, 1 nans, 2 fp_mism, 3 fp_checked, 4 timeouts, 5 abort flag (u32),
+  // 6 fwd-vs-owner fingerprint mismatches, 7 ... checked
   unsigned long long* stat(int i) const {
     return reinterpret_cast<unsigned long long*>(arena[rank] + off_stats) + i;
   }
+  // rank `r`'s expected-forward-fingerprint slot pair of `layer` (parity 0; +1 = parity 1)
+  unsigned long long* fpx(int r, int layer) const {
+    return reinterpret_cast<unsigned long long*>(arena[r] + off_fpx) + (uint64_t)layer * 2;
+  }
+  uint32_t* epoch_word() const { return reinterpret_cast<uint32_t*>(arena[rank] + off_epoch); }
   SyncCommon sync() const {
     SyncCommon s;
     s.timeout_ns = (uint64_t)(timeout_s * 1e9);
     s.abort_flag = reinterpret_cast<uint32_t*>(stat(5));
     s.timeouts = stat(4);
     s.host_err = host_err_dev;
+    s.epoch = dev_epoch ? epoch_word() : nullptr;
     return s;
   }
+  // Flag value for the absolute epoch x of a layer flag: absolute (host epochs) or relative
+  // to the current step t, the kernel adding its device step counter (device epochs).
+  uint32_t lv(int64_t x) const { return (uint32_t)(dev_epoch ? x - t : x); }
+  // ... of a gradient-slot flag (slot_uses[slot] uses per step); the list's mul is set by sl()
+  uint32_t sv(int slot, int64_t x) const { return (uint32_t)(dev_epoch ? x - t * (int64_t)slot_uses[slot] : x); }
+  uint32_t sl(int slot) const { return slot_uses[slot]; }
   int node_first() const { return (rank / node_size) * node_size; }
   int local() const { return rank % node_size; }
 };
@@ -150,7 +173,6 @@ int grid_for(const hpz_ctx* c, int64_t work_items, int per_sm, int cap = 0) {
   return g < 1 ? 1 : (int)g;
 }
 
-uint32_t epoch(int64_t x) { return (uint32_t)x; }
 
 // Pick the gather kernel: TMA bulk pipeline (one CTA/SM) or the LDG/STG kernel (EXACT
 // verification, or when selected with HPZ_OPT_COPY_ENGINE).
@@ -172,9 +194,22 @@ cudaError_t rs_launch(const hpz_ctx* c, const RSParams& r, const AdamParams* a, 
   return a ? launch_rs_adam(r, *a, c->world, grid, s) : launch_reduce_scatter(r, c->world, grid, s);
 }
 
+// Owner-side fingerprint emission (a7): into every reader's expected-forward slot of the
+// step `for_t` whose forward gather will read what the emitting kernel writes.
+FpEmit fp_emit(hpz_ctx* c, int layer, int64_t for_t) {
+  FpEmit e{};
+  const Layer& L = c->layers[layer];
+  for (int q = 0; q < c->world; ++q) e.dst[e.n_dst++] = c->fpx(q, layer);
+  e.par = (int)(c->lv(for_t) & 1u);
+  e.word_base = (int64_t)c->rank * L.shard * c->elem / 16;
+  c->layers[layer].fpx_t = for_t;
+  return e;
+}
+
 // qwZ: quantize my primary shard of `layer` (just written by Adam or the init) and release
 // E1 (value) from the quantizer's last CTA: peers gather the codes, not the primary.
-int qwz_quantize(hpz_ctx* c, int layer, uint32_t value, cudaStream_t s) {
+// `emit`: also emit the expected forward fingerprint (of the dequantized words) for step for_t.
+int qwz_quantize(hpz_ctx* c, int layer, uint32_t value, cudaStream_t s, bool emit, int64_t for_t) {
   const Layer& L = c->layers[layer];
   char* a = c->arena[c->rank];
   QwzQuantParams q{};
@@ -186,12 +221,15 @@ int qwz_quantize(hpz_ctx* c, int layer, uint32_t value, cudaStream_t s) {
   q.done_ctr = c->ctr(C_QWZ, layer);
   for (int j = 0; j < c->world; ++j) q.rel.ptr[q.rel.n++] = c->flag(j, F_PRIM_READY, layer, c->rank);
   q.rel.value = value;
+  if (emit) q.fpe = fp_emit(c, layer, for_t);
   q.sync = c->sync();
   cudaError_t e = launch_qwz_quantize(q, grid_for(c, (L.shard / kQwzBlock + 31) / 32, 4), s);   // one wave of 4 CTAs/SM, 8 warps x 4 blocks per CTA step
   if (e != cudaSuccess) return fail(c, HPZ_ECUDA, "qwZ quantize launch: %s", cudaGetErrorString(e));
   c->launches += 1;
   return HPZ_OK;
 }
+
+int publish_primary(hpz_ctx* c, int layer, cudaStream_t s);
 
 int do_init_shard(hpz_ctx* c, int layer, const float* src, uint64_t key, float scale, cudaStream_t s) {
   Layer& L = c->layers[layer];
@@ -203,12 +241,24 @@ int do_init_shard(hpz_ctx* c, int layer, const float* src, uint64_t key, float s
                                     grid_for(c, (L.shard + 255) / 256, 8), s);
   if (e != cudaSuccess) return fail(c, HPZ_ECUDA, "init_shard launch: %s", cudaGetErrorString(e));
   c->launches += 1;
-  if (c->qwz_bits) return qwz_quantize(c, layer, epoch(c->t + 1), s);   // E1 from the quantizer
-  // E1 for step 0: PRIMARY_READY_j[layer][me] = 1 in every rank's arena
+  return publish_primary(c, layer, s);
+}
+
+// A freshly loaded primary (init / resume): its expected forward fingerprint for the current
+// step (always: one pass over the shard, once), then E1 (the qwZ quantizer's, with qwZ).
+int publish_primary(hpz_ctx* c, int layer, cudaStream_t s) {
+  const Layer& L = c->layers[layer];
+  if (c->qwz_bits) return qwz_quantize(c, layer, c->lv(c->t + 1), s, true, c->t);   // E1 from the quantizer
+  const int64_t words = L.shard * c->elem / 16;
+  cudaError_t e = launch_prim_fp(c->arena[c->rank] + L.off_primary, words, fp_emit(c, layer, c->t), c->sync(),
+                                 grid_for(c, (words + 255) / 256, 4), s);
+  if (e != cudaSuccess) return fail(c, HPZ_ECUDA, "fingerprint launch: %s", cudaGetErrorString(e));
+  c->launches += 1;
+  // E1 for the current step: PRIMARY_READY_j[layer][me] = t+1 in every rank's arena
   ReleaseList r{};
   for (int j = 0; j < c->world; ++j) r.ptr[r.n++] = c->flag(j, F_PRIM_READY, layer, c->rank);
-  r.value = epoch(c->t + 1);
-  e = launch_release(r, s);
+  r.value = c->lv(c->t + 1);
+  e = launch_release(r, c->sync(), s);
   if (e != cudaSuccess) return fail(c, HPZ_ECUDA, "release launch: %s", cudaGetErrorString(e));
   c->launches += 1;
   return HPZ_OK;
@@ -221,7 +271,8 @@ int slot_acquire(hpz_ctx* c, int layer, cudaStream_t s) {
   if (use == 0) return HPZ_OK;
   WaitList w{};
   for (int j = 0; j < c->world; ++j) w.ptr[w.n++] = c->slot_flag(c->rank, S_RS_DONE, slot, j);
-  w.target = epoch(use);
+  w.target = c->sv(slot, use);
+  w.mul = c->sl(slot);
   cudaError_t e = launch_wait(w, c->sync(), s);
   if (e != cudaSuccess) return fail(c, HPZ_ECUDA, "wait launch: %s", cudaGetErrorString(e));
   c->launches += 1;
@@ -231,7 +282,8 @@ int slot_acquire(hpz_ctx* c, int layer, cudaStream_t s) {
 ReleaseList grad_ready_list(hpz_ctx* c, int slot) {
   ReleaseList r{};
   for (int j = 0; j < c->world; ++j) r.ptr[r.n++] = c->slot_flag(j, S_GRAD_READY, slot, c->rank);
-  r.value = epoch(c->slot_use[slot] + 1);
+  r.value = c->sv(slot, c->slot_use[slot] + 1);
+  r.mul = c->sl(slot);
   return r;
 }
 
@@ -295,7 +347,7 @@ int hpz_register_flat_params(hpz_ctx* c, int n_layers, const int64_t* numel, int
     return fail(c, HPZ_EINVAL, "qgZ needs align_elems to be a multiple of 256");
   c->dtype = param_dtype;
   c->elem = elem;
-  c->alias_sec = c->node_size == c->world && !c->qwz_bits;
+  c->alias_sec = c->alias_opt && c->node_size == c->world && !c->qwz_bits;
   c->align = align_elems;
   c->n_layers = n_layers;
   c->n_slots = n_grad_slots;
@@ -303,6 +355,7 @@ int hpz_register_flat_params(hpz_ctx* c, int n_layers, const int64_t* numel, int
   c->slot_numel.assign(n_grad_slots, 0);
   c->slot_use.assign(n_grad_slots, 0);
   c->slot_ready_sent.assign(n_grad_slots, 0);
+  c->slot_uses.assign(n_grad_slots, 0);
   const int64_t q = (int64_t)c->world * align_elems;
   for (int i = 0; i < n_layers; ++i) {
     if (numel[i] < 1) return fail(c, HPZ_EINVAL, "layer %d: numel must be >= 1", i);
@@ -312,6 +365,7 @@ int hpz_register_flat_params(hpz_ctx* c, int n_layers, const int64_t* numel, int
     L.shard = L.numel_pad / c->world;
     L.sec_shard = L.numel_pad / c->node_size;
     L.slot = i % n_grad_slots;
+    c->slot_uses[L.slot] += 1;
     if (L.numel_pad > c->slot_numel[L.slot]) c->slot_numel[L.slot] = L.numel_pad;
   }
   // control region: flags | completion counters | fingerprints | stats
@@ -325,6 +379,10 @@ int hpz_register_flat_params(hpz_ctx* c, int n_layers, const int64_t* numel, int
   off = align_up(off + (uint64_t)n_layers * 4 * 8, 256);
   c->off_stats = off;
   off = align_up(off + 8 * 8, 256);
+  c->off_fpx = off;
+  off = align_up(off + (uint64_t)n_layers * 2 * 8, 256);
+  c->off_epoch = off;
+  off = align_up(off + 4, 256);
   c->ctrl_bytes = align_up(off, kCtrlAlign);
   off = c->ctrl_bytes;
   for (int i = 0; i < n_layers; ++i) {
@@ -457,6 +515,7 @@ int hpz_finalize(hpz_ctx* c) {
   for (auto ev : c->copy_ev)
     if (ev) cudaEventDestroy(ev);
   if (c->host_err) cudaFreeHost(c->host_err);
+  if (c->adam_tab) cudaFree(c->adam_tab);
   delete c;
   return HPZ_OK;
 }
@@ -519,13 +578,35 @@ int hpz_current_step(const hpz_ctx* c, int64_t* t) {
   return HPZ_OK;
 }
 
+int hpz_resync_step(hpz_ctx* c) {
+  if (int rc = check_ready(c)) return rc;
+  if (!c->dev_epoch) return fail(c, HPZ_ESTATE, "hpz_resync_step needs device epochs");
+  HPZ_CUDA(c, cudaSetDevice(c->device));
+  HPZ_CUDA(c, cudaDeviceSynchronize());
+  uint32_t d = 0;
+  HPZ_CUDA(c, cudaMemcpy(&d, c->epoch_word(), 4, cudaMemcpyDeviceToHost));
+  for (const Layer& L : c->layers)
+    if (L.step_t != c->t - 1) return fail(c, HPZ_ESTATE, "hpz_resync_step between complete steps only");
+  const int64_t t = (int64_t)d;
+  for (Layer& L : c->layers) {
+    L.fwd_t = L.bwd_t = L.rs_t = L.step_t = t - 1;
+    if (L.fpx_t == c->t) L.fpx_t = t;   // the last step's emission targets step t's forward
+  }
+  for (size_t k = 0; k < c->slot_use.size(); ++k) {
+    c->slot_use[k] = (uint64_t)t * c->slot_uses[k];
+    c->slot_ready_sent[k] = 0;
+  }
+  c->t = t;
+  return HPZ_OK;
+}
+
 int hpz_counters(hpz_ctx* c, hpz_counters_t* out, int reset) {
   if (!c || !out) return HPZ_EINVAL;
   if (c->device < 0) return fail(c, HPZ_ESTATE, "host-only context has no counters");
   if (!c->registered || !c->arena[c->rank]) return fail(c, HPZ_ESTATE, "arena not allocated/bound");
   HPZ_CUDA(c, cudaSetDevice(c->device));
   HPZ_CUDA(c, cudaDeviceSynchronize());
-  unsigned long long s[5];
+  unsigned long long s[8];
   HPZ_CUDA(c, cudaMemcpy(s, c->stat(0), sizeof s, cudaMemcpyDeviceToHost));
   out->mismatches = s[0];
   out->nan_reads = s[1];
@@ -533,7 +614,12 @@ int hpz_counters(hpz_ctx* c, hpz_counters_t* out, int reset) {
   out->fp_checked = s[3];
   out->timeouts = s[4];
   out->launches = c->launches;
-  if (reset) HPZ_CUDA(c, cudaMemset(c->stat(0), 0, 4 * sizeof(unsigned long long)));
+  out->fp_fwd_mismatches = s[6];
+  out->fp_fwd_checked = s[7];
+  if (reset) {
+    HPZ_CUDA(c, cudaMemset(c->stat(0), 0, 4 * sizeof(unsigned long long)));
+    HPZ_CUDA(c, cudaMemset(c->stat(6), 0, 2 * sizeof(unsigned long long)));
+  }
   return HPZ_OK;
 }
 
@@ -586,14 +672,7 @@ int hpz_load_state(hpz_ctx* c, int layer, const float* master, const float* m, c
   if (e != cudaSuccess) return fail(c, HPZ_ECUDA, "refresh launch: %s", cudaGetErrorString(e));
   c->launches += 1;
   c->adam_base = adam_steps_done;
-  if (c->qwz_bits) return qwz_quantize(c, layer, epoch(c->t + 1), s);
-  ReleaseList r{};
-  for (int j = 0; j < c->world; ++j) r.ptr[r.n++] = c->flag(j, F_PRIM_READY, layer, c->rank);
-  r.value = epoch(c->t + 1);
-  e = launch_release(r, s);
-  if (e != cudaSuccess) return fail(c, HPZ_ECUDA, "release launch: %s", cudaGetErrorString(e));
-  c->launches += 1;
-  return HPZ_OK;
+  return publish_primary(c, layer, s);
 }
 
 int hpz_synth_master(hpz_ctx* c, int layer, uint64_t key, float scale, void* stream) {
@@ -611,13 +690,16 @@ int hpz_fwd_gather(hpz_ctx* c, int layer, void* full_out, void* stream) {
   if (c->qwz_bits && (c->verify == HPZ_VERIFY_EXACT || c->order == HPZ_ORDER_OFF))
     return fail(c, HPZ_ESTATE, "qwZ gathers dequantized weights: EXACT verification and ORDER_OFF compare/read raw primaries");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const uint32_t t1 = epoch(c->t + 1);
+  if (c->dev_epoch && (c->order == HPZ_ORDER_STOCK || c->order == HPZ_ORDER_PAPER))
+    return fail(c, HPZ_ESTATE, "device epochs (graph capture) support ORDER_FIXED and ORDER_OFF only");
+  const uint32_t t1 = c->lv(c->t + 1);
   GatherParams p{};
   p.n_src = c->world;
   p.src_bytes = L.shard * c->elem;
   for (int j = 0; j < c->world; ++j) {
     p.src[j] = c->arena[j] + L.off_primary;
-    p.src_flag[j] = c->flag(c->rank, F_PRIM_READY, layer, j);    // E1
+    // E1 (HPZ_FAULT_SKIP_E1: test-only, the data reads skip it; the fingerprint check keeps it)
+    p.src_flag[j] = (c->fault & HPZ_FAULT_SKIP_E1) ? nullptr : c->flag(c->rank, F_PRIM_READY, layer, j);
   }
   p.src_target = t1;
   p.out = static_cast<char*>(full_out);
@@ -632,9 +714,20 @@ int hpz_fwd_gather(hpz_ctx* c, int layer, void* full_out, void* stream) {
     p.sec_lo = l * c->k;
     p.sec_hi = (l + 1) * c->k;
     for (int q = 0; q < c->node_size; ++q) p.war.ptr[p.war.n++] = c->flag(c->rank, F_BWD_DONE, layer, nf + q);   // E4
-    p.war.target = epoch(c->t);
+    p.war.target = c->lv(c->t);
   }
-  if (c->verify != HPZ_VERIFY_NONE) p.fp_acc = c->fp(layer, (int)(c->t & 1), 0);
+  p.fp_par = (int)(c->lv(c->t) & 1u);
+  if (c->verify != HPZ_VERIFY_NONE) {
+    p.fp_acc = c->fp(layer, 0, 0);
+    if (L.fpx_t == c->t) {
+      // the owners emitted this step's expected fingerprint (a7, E1/E2): compare once all E1s
+      p.fp_exp = c->fpx(c->rank, layer);
+      for (int j = 0; j < c->world; ++j) p.exp_wait.ptr[p.exp_wait.n++] = c->flag(c->rank, F_PRIM_READY, layer, j);
+      p.exp_wait.target = t1;
+      p.fpx_mism = c->stat(6);
+      p.fpx_checked = c->stat(7);
+    }
+  }
   p.done_ctr = c->ctr(C_FWD, layer);
   if (write_sec)
     for (int q = 0; q < c->node_size; ++q) p.rel.ptr[p.rel.n++] = c->flag(nf + q, F_SEC_READY, layer, c->rank);   // E3
@@ -667,7 +760,7 @@ int hpz_fwd_gather(hpz_ctx* c, int layer, void* full_out, void* stream) {
       // E4 (P2P needs it; NCCL's rendezvous would cover it): node peers' step t-1 reads done
       WaitList w{};
       for (int q = 0; q < c->node_size; ++q) w.ptr[w.n++] = c->flag(c->rank, F_BWD_DONE, layer, nf + q);
-      w.target = epoch(c->t);
+      w.target = c->lv(c->t);
       e = launch_wait(w, c->sync(), c->side);
       if (e != cudaSuccess) return fail(c, HPZ_ECUDA, "wait launch: %s", cudaGetErrorString(e));
       c->launches += 1;
@@ -691,7 +784,7 @@ int hpz_fwd_gather(hpz_ctx* c, int layer, void* full_out, void* stream) {
       ReleaseList r{};
       for (int q = 0; q < c->node_size; ++q) r.ptr[r.n++] = c->flag(nf + q, F_SEC_READY, layer, c->rank);
       r.value = t1;
-      e = launch_release(r, c->side);
+      e = launch_release(r, c->sync(), c->side);
       if (e != cudaSuccess) return fail(c, HPZ_ECUDA, "release launch: %s", cudaGetErrorString(e));
       c->launches += 1;
       HPZ_CUDA(c, cudaEventRecord(c->copy_ev[layer], c->side));
@@ -715,7 +808,7 @@ int hpz_bwd_gather(hpz_ctx* c, int layer, void* full_out, void* stream) {
   if (c->order == HPZ_ORDER_PAPER)   // Alg. 1: "Repeat wait Until MemcpyD2D on L_k,second finishes" (host)
     HPZ_CUDA(c, cudaEventSynchronize(c->copy_ev[layer]));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const uint32_t t1 = epoch(c->t + 1);
+  const uint32_t t1 = c->lv(c->t + 1);
   const int nf = c->node_first();
   const bool from_prim = c->order == HPZ_ORDER_OFF || c->alias_sec;
   const bool reads_prim = from_prim || c->verify == HPZ_VERIFY_EXACT;
@@ -750,11 +843,11 @@ int hpz_bwd_gather(hpz_ctx* c, int layer, void* full_out, void* stream) {
     p.mism = c->stat(0);
     p.nans = c->stat(1);
   }
+  p.fp_par = (int)(c->lv(c->t) & 1u);
   if (c->verify != HPZ_VERIFY_NONE) {
-    const int par = (int)(c->t & 1);
-    p.fp_acc = c->fp(layer, par, 1);
-    p.fp_a = c->fp(layer, par, 0);
-    p.fp_b = c->fp(layer, par, 1);
+    p.fp_acc = c->fp(layer, 0, 1);
+    p.fp_a = c->fp(layer, 0, 0);
+    p.fp_b = c->fp(layer, 0, 1);
     p.cmp_wait.ptr[p.cmp_wait.n++] = c->flag(c->rank, F_FWD_DONE, layer, c->rank);   // my forward finished
     p.cmp_wait.target = t1;
     p.fp_mism = c->stat(2);
@@ -835,7 +928,8 @@ static int qgz_quantize(hpz_ctx* c, int layer, cudaStream_t s) {
   q.n = L.numel_pad;
   if (c->slot_use[slot] > 0) {
     for (int j = 0; j < c->world; ++j) q.war.ptr[q.war.n++] = c->slot_flag(c->rank, S_RS_DONE, slot, j);
-    q.war.target = epoch(c->slot_use[slot]);
+    q.war.target = c->sv(slot, c->slot_use[slot]);
+    q.war.mul = c->sl(slot);
   }
   q.sync = c->sync();
   cudaError_t e = launch_qgz_quantize(q, grid_for(c, (L.numel_pad / kQgzBlock + 63) / 64, 4), s);   // 4 resident CTAs/SM: one wave
@@ -851,7 +945,7 @@ int hpz_grads_ready(hpz_ctx* c, int layer, void* stream) {
   if (c->slot_ready_sent[slot]) return fail(c, HPZ_ESTATE, "grads_ready already published for this use of the slot");
   if (c->qgz_bits)
     if (int rc = qgz_quantize(c, layer, static_cast<cudaStream_t>(stream))) return rc;
-  cudaError_t e = launch_release(grad_ready_list(c, slot), static_cast<cudaStream_t>(stream));
+  cudaError_t e = launch_release(grad_ready_list(c, slot), c->sync(), static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return fail(c, HPZ_ECUDA, "release launch: %s", cudaGetErrorString(e));
   c->launches += 1;
   c->slot_ready_sent[slot] = 1;
@@ -861,7 +955,7 @@ int hpz_grads_ready(hpz_ctx* c, int layer, void* stream) {
 static void build_rs(hpz_ctx* c, int layer, RSParams& p) {
   Layer& L = c->layers[layer];
   const int slot = L.slot;
-  const uint32_t u1 = epoch(c->slot_use[slot] + 1);
+  const uint32_t u1 = c->sv(slot, c->slot_use[slot] + 1);
   p = RSParams{};
   for (int j = 0; j < c->world; ++j)
     p.src[j] = reinterpret_cast<const float*>(c->arena[j] + c->off_slot[slot] + (uint64_t)c->rank * L.shard * c->grad_bytes);
@@ -871,9 +965,11 @@ static void build_rs(hpz_ctx* c, int layer, RSParams& p) {
   if (!c->slot_ready_sent[slot]) p.ready = grad_ready_list(c, slot);   // E5 release
   for (int j = 0; j < c->world; ++j) p.ready_wait.ptr[p.ready_wait.n++] = c->slot_flag(c->rank, S_GRAD_READY, slot, j);
   p.ready_wait.target = u1;
+  p.ready_wait.mul = c->sl(slot);
   p.done_ctr = c->ctr(C_RS, c->n_layers + slot);
   for (int j = 0; j < c->world; ++j) p.rel.ptr[p.rel.n++] = c->slot_flag(j, S_RS_DONE, slot, c->rank);   // E6
   p.rel.value = u1;
+  p.rel.mul = c->sl(slot);
   p.sync = c->sync();
   if (c->qgz_bits) {
     for (int j = 0; j < c->world; ++j) {
@@ -914,7 +1010,38 @@ static int check_adam(hpz_ctx* c, const hpz_adam* a) {
   return HPZ_OK;
 }
 
-static void build_adam(hpz_ctx* c, int layer, const hpz_adam* a, AdamParams& p) {
+// Device epochs: the per-step Adam scalars as a device table (Adam step k at [k - 1]),
+// computed exactly like build_adam's host path, up to the step from which they no longer
+// change in fp32.  Rebuilt (synchronously) when the hyper-parameters change; not while a
+// stream is being captured.
+static int adam_table(hpz_ctx* c, const hpz_adam* a, cudaStream_t s) {
+  const double key[4] = {a->lr, a->beta1, a->beta2, (double)c->adam_base};
+  if (c->adam_tab && !std::memcmp(key, c->adam_tab_key, sizeof key)) return HPZ_OK;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  HPZ_CUDA(c, cudaStreamIsCapturing(s, &cs));
+  if (cs != cudaStreamCaptureStatusNone)
+    return fail(c, HPZ_ESTATE, "device epochs: run one step with these Adam hyper-parameters before capturing");
+  std::vector<float2> tab;
+  constexpr int64_t kMax = 1 << 22;
+  const float lr_f = (float)a->lr;
+  for (int64_t k = 1;; ++k) {
+    const double bc1 = 1.0 - std::pow(a->beta1, (double)k);
+    const double bc2 = 1.0 - std::pow(a->beta2, (double)k);
+    const float2 v = make_float2((float)(a->lr / bc1), (float)std::sqrt(bc2));
+    tab.push_back(v);
+    if (v.x == lr_f && v.y == 1.0f) break;   // constant from here on (monotone, rounded)
+    if (k == kMax) return fail(c, HPZ_EINVAL, "device epochs: beta1/beta2 too close to 1 for the scalar table");
+  }
+  if (c->adam_tab) cudaFree(c->adam_tab);
+  c->adam_tab = nullptr;
+  HPZ_CUDA(c, cudaMalloc(&c->adam_tab, tab.size() * sizeof(float2)));
+  HPZ_CUDA(c, cudaMemcpy(c->adam_tab, tab.data(), tab.size() * sizeof(float2), cudaMemcpyHostToDevice));
+  c->adam_tab_len = (int64_t)tab.size();
+  std::memcpy(c->adam_tab_key, key, sizeof key);
+  return HPZ_OK;
+}
+
+static int build_adam(hpz_ctx* c, int layer, const hpz_adam* a, AdamParams& p, cudaStream_t s) {
   Layer& L = c->layers[layer];
   const int64_t tad = a->step > 0 ? a->step : c->adam_base + c->t + 1;    // 1-based Adam count (R24)
   const double bc1 = 1.0 - std::pow(a->beta1, (double)tad);
@@ -936,23 +1063,44 @@ static void build_adam(hpz_ctx* c, int layer, const hpz_adam* a, AdamParams& p) 
   p.bc2_sqrt = (float)std::sqrt(bc2);
   p.eps = (float)a->eps;
   p.lr_wd = (float)(a->lr * a->weight_decay);
-  const uint32_t t1 = epoch(c->t + 1);
-  for (int j = 0; j < c->world; ++j) p.wait.ptr[p.wait.n++] = c->flag(c->rank, F_FWD_DONE, layer, j);   // E2
+  if (c->dev_epoch && a->step <= 0) {   // scalars of the device step, from the table
+    if (int rc = adam_table(c, a, s)) return rc;
+    p.tab = c->adam_tab;
+    p.tab_k0 = c->adam_base;
+    p.tab_len = c->adam_tab_len;
+  }
+  const uint32_t t1 = c->lv(c->t + 1);
+  if (!(c->fault & HPZ_FAULT_SKIP_E2))   // test-only fault: overwrite the primary under its readers
+    for (int j = 0; j < c->world; ++j) p.wait.ptr[p.wait.n++] = c->flag(c->rank, F_FWD_DONE, layer, j);   // E2
   if (c->order == HPZ_ORDER_OFF || c->verify == HPZ_VERIFY_EXACT || c->alias_sec)
     for (int j = 0; j < c->world; ++j) p.wait.ptr[p.wait.n++] = c->flag(c->rank, F_BWDP_DONE, layer, j);   // E7
   p.wait.target = t1;
   p.done_ctr = c->ctr(C_ADAM, layer);
-  if (!c->qwz_bits)   // with qwZ the quantizer launched after Adam releases E1
+  if (!c->qwz_bits) {   // with qwZ the quantizer launched after Adam releases E1 (and emits)
     for (int j = 0; j < c->world; ++j) p.rel.ptr[p.rel.n++] = c->flag(j, F_PRIM_READY, layer, c->rank);   // E1
-  p.rel.value = epoch(c->t + 2);
+    if (c->verify != HPZ_VERIFY_NONE) p.fpe = fp_emit(c, layer, c->t + 1);
+  }
+  p.rel.value = c->lv(c->t + 2);
   p.sync = c->sync();
+  return HPZ_OK;
 }
 
-static void stepped(hpz_ctx* c, int layer) {
+// The call that completes step t: host t advances; with device epochs the device step
+// counter advances too, after every kernel this call enqueued on `s`.
+static int advance_step(hpz_ctx* c, cudaStream_t s) {
+  c->t += 1;
+  if (!c->dev_epoch) return HPZ_OK;
+  cudaError_t e = launch_epoch_advance(c->epoch_word(), s);
+  if (e != cudaSuccess) return fail(c, HPZ_ECUDA, "epoch advance launch: %s", cudaGetErrorString(e));
+  c->launches += 1;
+  return HPZ_OK;
+}
+
+static int stepped(hpz_ctx* c, int layer, cudaStream_t s) {
   c->layers[layer].step_t = c->t;
   bool all = true;
   for (int i = 0; i < c->n_layers; ++i) all = all && c->layers[i].step_t == c->t;
-  if (all) c->t += 1;
+  return all ? advance_step(c, s) : HPZ_OK;
 }
 
 static int step_one(hpz_ctx* c, int layer, const hpz_adam* a, cudaStream_t s) {
@@ -960,11 +1108,11 @@ static int step_one(hpz_ctx* c, int layer, const hpz_adam* a, cudaStream_t s) {
   if (L.rs_t != c->t) return fail(c, HPZ_ESTATE, "layer %d: step without its reduce-scatter at step %lld", layer, (long long)c->t);
   if (L.step_t == c->t) return fail(c, HPZ_ESTATE, "layer %d already stepped at step %lld", layer, (long long)c->t);
   AdamParams p;
-  build_adam(c, layer, a, p);
+  if (int rc = build_adam(c, layer, a, p, s)) return rc;
   cudaError_t e = launch_adam(p, grid_for(c, (p.n_vec + 511) / 512, c->ctas_per_sm), s);
   if (e != cudaSuccess) return fail(c, HPZ_ECUDA, "adam launch: %s", cudaGetErrorString(e));
   c->launches += 1;
-  if (c->qwz_bits) return qwz_quantize(c, layer, epoch(c->t + 2), s);
+  if (c->qwz_bits) return qwz_quantize(c, layer, c->lv(c->t + 2), s, c->verify != HPZ_VERIFY_NONE, c->t + 1);
   return HPZ_OK;
 }
 
@@ -981,13 +1129,11 @@ int hpz_step(hpz_ctx* c, int layer, const hpz_adam* a, void* stream) {
       if (int rc = step_one(c, i, a, s)) return rc;
       c->layers[i].step_t = t;
     }
-    c->t += 1;
-    return HPZ_OK;
+    return advance_step(c, s);
   }
   if (int rc = check_layer(c, layer)) return rc;
   if (int rc = step_one(c, layer, a, s)) return rc;
-  stepped(c, layer);
-  return HPZ_OK;
+  return stepped(c, layer, s);
 }
 
 int hpz_reduce_scatter_adam(hpz_ctx* c, int layer, const hpz_adam* a, void* stream) {
@@ -999,8 +1145,9 @@ int hpz_reduce_scatter_adam(hpz_ctx* c, int layer, const hpz_adam* a, void* stre
   if (L.step_t == c->t) return fail(c, HPZ_ESTATE, "layer %d already stepped at step %lld", layer, (long long)c->t);
   RSParams r;
   AdamParams p;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
   build_rs(c, layer, r);
-  build_adam(c, layer, a, p);
+  if (int rc = build_adam(c, layer, a, p, s)) return rc;
   if (!c->store_grad_shard) r.out = nullptr;
   if (c->qgz_bits && !c->slot_ready_sent[L.slot])
     if (int rc = qgz_quantize(c, layer, static_cast<cudaStream_t>(stream))) return rc;
@@ -1008,10 +1155,9 @@ int hpz_reduce_scatter_adam(hpz_ctx* c, int layer, const hpz_adam* a, void* stre
   if (e != cudaSuccess) return fail(c, HPZ_ECUDA, "rs+adam launch: %s", cudaGetErrorString(e));
   c->launches += 1;
   if (c->qwz_bits)
-    if (int rc = qwz_quantize(c, layer, epoch(c->t + 2), static_cast<cudaStream_t>(stream))) return rc;
+    if (int rc = qwz_quantize(c, layer, c->lv(c->t + 2), s, c->verify != HPZ_VERIFY_NONE, c->t + 1)) return rc;
   rs_issued(c, layer);
-  stepped(c, layer);
-  return HPZ_OK;
+  return stepped(c, layer, s);
 }
 
 int hpz_set_option(hpz_ctx* c, int option, int64_t value) {
@@ -1047,6 +1193,26 @@ int hpz_set_option(hpz_ctx* c, int option, int64_t value) {
     case HPZ_OPT_RS_CTAS:
       if (value < 0 || value > 1 << 20) return fail(c, HPZ_EINVAL, "CTA caps must be >= 0");
       (option == HPZ_OPT_BWD_CTAS ? c->bwd_ctas : c->rs_ctas) = (int)value;
+      return HPZ_OK;
+    case HPZ_OPT_DEVICE_EPOCH: {
+      if (value != 0 && value != 1) return fail(c, HPZ_EINVAL, "device_epoch must be 0 or 1");
+      if (!c->bound) return fail(c, HPZ_ESTATE, "device epochs need a bound arena");
+      // between steps, device idle: the device counter starts at the host's step
+      HPZ_CUDA(c, cudaSetDevice(c->device));
+      HPZ_CUDA(c, cudaDeviceSynchronize());
+      const uint32_t t32 = (uint32_t)c->t;
+      HPZ_CUDA(c, cudaMemcpy(c->epoch_word(), &t32, 4, cudaMemcpyHostToDevice));
+      c->dev_epoch = value != 0;
+      return HPZ_OK;
+    }
+    case HPZ_OPT_ALIAS_SECONDARY:
+      if (c->registered) return fail(c, HPZ_ESTATE, "the secondary layout must be chosen before hpz_register_flat_params");
+      if (value != 0 && value != 1) return fail(c, HPZ_EINVAL, "alias_secondary must be 0 or 1");
+      c->alias_opt = value != 0;
+      return HPZ_OK;
+    case HPZ_OPT_FAULT:
+      if (value < 0 || value > (HPZ_FAULT_SKIP_E1 | HPZ_FAULT_SKIP_E2)) return fail(c, HPZ_EINVAL, "bad fault mask");
+      c->fault = (int)value;
       return HPZ_OK;
     case HPZ_OPT_COPY_ENGINE:
       if (value != HPZ_COPY_LDG && value != HPZ_COPY_TMA) return fail(c, HPZ_EINVAL, "copy engine must be 0 (LDG) or 1 (TMA)");

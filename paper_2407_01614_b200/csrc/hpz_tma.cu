@@ -164,13 +164,14 @@ __global__ void __launch_bounds__(32 * (1 + kFpWarps), 1)
     if (lane == 0) {
       uint32_t waited = 0;
       bool war_done = false;
+      const uint32_t src_target = layer_epoch(p.src_target, p.sync);
       auto issue_load = [&](int64_t k) {
         int j;
         int64_t off;
         uint32_t bytes;
         chunk_of(k, j, off, bytes);
         if (!((waited >> j) & 1u)) {
-          if (p.src_flag[j] != nullptr) wait_geq(p.src_flag[j], p.src_target, p.sync);   // E1 / E3
+          if (p.src_flag[j] != nullptr) wait_geq(p.src_flag[j], src_target, p.sync);   // E1 / E3
           fence_proxy_async();
           waited |= 1u << j;
         }
@@ -236,18 +237,9 @@ __global__ void __launch_bounds__(32 * (1 + kFpWarps), 1)
   if (FP && threadIdx.x == 0) {
     unsigned long long s = 0;
     for (int w = 0; w < kFpWarps; ++w) s += fp_red[w];
-    if (s) atomicAdd(p.fp_acc, s);
+    if (s) atomicAdd(p.fp_acc + 2 * ((p.fp_par + epoch_base(p.sync)) & 1u), s);
   }
-  if (last_cta(p.done_ctr)) {
-    if (p.fp_a != nullptr) {
-      wait_all(p.cmp_wait, p.sync);
-      const unsigned long long a = atomicExch(p.fp_a, 0ull);
-      const unsigned long long b = atomicExch(p.fp_b, 0ull);
-      atomicAdd(p.fp_checked, 1ull);
-      if (a != b) atomicAdd(p.fp_mism, 1ull);
-    }
-    release_all(p.rel);
-  }
+  if (last_cta(p.done_ctr)) gather_finish(p);
 }
 
 // ------------------------------------------------------------------ RS (+ Adam) (a5, a6)
@@ -285,6 +277,7 @@ __global__ void __launch_bounds__(RsCfg<P, ADAM, MODE>::kLead + RsCfg<P, ADAM, M
   extern __shared__ __align__(1024) char smem[];
   __shared__ __align__(8) uint64_t full_bar[C::kStages];
   __shared__ __align__(8) uint64_t empty_bar[C::kStages];
+  uint64_t fp = 0;                 // consumers: fingerprint of the primary words written
   const int64_t n = r.n_vec * 4;   // shard elements (multiple of 256)
   const int64_t total = (n + C::kChunk - 1) / C::kChunk;
   const int64_t nk = blockIdx.x < total ? (total - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
@@ -294,7 +287,7 @@ __global__ void __launch_bounds__(RsCfg<P, ADAM, MODE>::kLead + RsCfg<P, ADAM, M
     griddep_wait();                      // the caller's gradient writes (previous kernel) are done
     if (r.ready.n) {
       __threadfence_system();
-      release_all(r.ready);              // E5
+      release_all(r.ready, r.sync);      // E5
     }
     wait_all(r.ready_wait, r.sync);      // E5: every rank's gradient slot is written
     if (ADAM) wait_all(a.wait, a.sync);  // E2 (+E7): nobody still reads my primary
@@ -341,6 +334,7 @@ __global__ void __launch_bounds__(RsCfg<P, ADAM, MODE>::kLead + RsCfg<P, ADAM, M
       griddep_launch_dependents();
     }
   } else {
+    const float2 sc = ADAM ? adam_scalars(a) : make_float2(0.f, 0.f);
     for (int64_t k = 0; k < nk; ++k) {
       const int s = (int)(k % C::kStages);
       mbar_wait(&full_bar[s], (uint32_t)((k / C::kStages) & 1));
@@ -349,8 +343,14 @@ __global__ void __launch_bounds__(RsCfg<P, ADAM, MODE>::kLead + RsCfg<P, ADAM, M
       const int cnt = (int)(rem < C::kChunk ? rem : C::kChunk);
       const char* stc = smem + (size_t)s * C::kStageBytes;
       const float4* wmv = reinterpret_cast<const float4*>(stc + C::kWmvOff);
-      // one float4 `ct` of the chunk: fixed-order sum (R7) of the P slices, then Adam (R8)
-      auto process = [&](const int ct) {
+      // one float4 `ct` of the chunk: fixed-order sum (R7) of the P slices, then Adam (R8);
+      // returns the fingerprint contribution of the primary word(s) written (warp-uniform
+      // call: `ok` false only computes nothing)
+      auto process = [&](const int ct, const bool ok) -> uint64_t {
+        uint2 pk = make_uint2(0u, 0u);
+        float4 w = make_float4(0.f, 0.f, 0.f, 0.f);
+        const int64_t i = e0 / 4 + ct;   // float4 index in the shard
+        if (ok) {
         float4 x[P];
 #pragma unroll
         for (int j = 0; j < P; ++j) {
@@ -377,47 +377,50 @@ __global__ void __launch_bounds__(RsCfg<P, ADAM, MODE>::kLead + RsCfg<P, ADAM, M
         g.y = __fmul_rn(g.y, r.inv_p);
         g.z = __fmul_rn(g.z, r.inv_p);
         g.w = __fmul_rn(g.w, r.inv_p);
-        const int64_t i = e0 / 4 + ct;   // float4 index in the shard
         if (r.out) reinterpret_cast<float4*>(r.out)[i] = g;
         if (ADAM) {
-          float4 w = wmv[0 * (C::kChunk / 4) + ct];
+          w = wmv[0 * (C::kChunk / 4) + ct];
           float4 m = wmv[1 * (C::kChunk / 4) + ct];
           float4 v = wmv[2 * (C::kChunk / 4) + ct];
-          adam1(w.x, m.x, v.x, g.x, a);
-          adam1(w.y, m.y, v.y, g.y, a);
-          adam1(w.z, m.z, v.z, g.z, a);
-          adam1(w.w, m.w, v.w, g.w, a);
+          adam1(w.x, m.x, v.x, g.x, a, sc);
+          adam1(w.y, m.y, v.y, g.y, a, sc);
+          adam1(w.z, m.z, v.z, g.z, a, sc);
+          adam1(w.w, m.w, v.w, g.w, a, sc);
           reinterpret_cast<float4*>(a.w)[i] = w;
           reinterpret_cast<float4*>(a.m)[i] = m;
           reinterpret_cast<float4*>(a.v)[i] = v;
           if (a.prim_bf16) {
-            __nv_bfloat162 lo = __floats2bfloat162_rn(w.x, w.y);
-            __nv_bfloat162 hi = __floats2bfloat162_rn(w.z, w.w);
-            uint2 pk;
-            pk.x = *reinterpret_cast<uint32_t*>(&lo);
-            pk.y = *reinterpret_cast<uint32_t*>(&hi);
+            pk = pack_bf16x4(w);
             reinterpret_cast<uint2*>(a.prim)[i] = pk;
           } else {
             reinterpret_cast<float4*>(a.prim)[i] = w;
           }
         }
+        }
+        if (!ADAM || a.fpe.n_dst == 0) return 0ull;
+        return prim_word_fp(a.prim_bf16, ok, i, w, pk, a.fpe.word_base);
       };
       // consumer thread ct handles float4 ct of the chunk (and ct + kConsumers, ... when the
       // chunk holds more float4s than there are consumers).  The single-pass form is a
       // separate branch: compiled as a loop it measured ~13% slower.
       if constexpr (C::kConsumers * 4 == C::kChunk) {
         const int ct = threadIdx.x - C::kLead;
-        if (ct * 4 < cnt) process(ct);
+        fp += process(ct, ct * 4 < cnt);
       } else {
-        for (int ct = threadIdx.x - C::kLead; ct * 4 < cnt; ct += C::kConsumers) process(ct);
+#pragma unroll
+        for (int it = 0; it < C::kChunk / (4 * C::kConsumers); ++it) {
+          const int ct = threadIdx.x - C::kLead + it * C::kConsumers;
+          fp += process(ct, ct * 4 < cnt);
+        }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty_bar[s]);
     }
   }
+  if (ADAM && a.fpe.n_dst > 0) emit_fp(fp, a.fpe, a.sync);
   if (last_cta(r.done_ctr)) {
-    release_all(r.rel);              // E6
-    if (ADAM) release_all(a.rel);    // E1 (t+1)
+    release_all(r.rel, r.sync);             // E6
+    if (ADAM) release_all(a.rel, a.sync);   // E1 (t+1)
   }
 }
 
@@ -535,6 +538,8 @@ __global__ void __launch_bounds__(256, 4) qwz_quantize_kernel(const __grid_const
   const int64_t n_blocks = q.n / kQwzBlock;
   const int64_t warp_id = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
   const int64_t n_warps = (int64_t)gridDim.x * (blockDim.x / 32);
+  const bool emit = q.fpe.n_dst > 0;
+  uint64_t fp = 0;
   for (int64_t b0 = warp_id * U; b0 < n_blocks; b0 += n_warps * U) {
     float v[U][8];
 #pragma unroll
@@ -590,9 +595,32 @@ __global__ void __launch_bounds__(256, 4) qwz_quantize_kernel(const __grid_const
       }
       reinterpret_cast<uint2*>(q.codes)[b * 32 + lane] = make_uint2(lo, hi);
       if (lane == 0) q.params[b] = make_float2(mn, scale);
+      if (emit) {
+        // the words the forward gather will produce from these codes: min + code * scale in
+        // fp32, rounded to the parameter dtype (gather_qwz_kernel's arithmetic)
+        float d[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const uint32_t code = ((k < 4 ? lo : hi) >> (8 * (k & 3))) & 0xFFu;
+          d[k] = __fadd_rn(mn, __fmul_rn((float)code, scale));
+        }
+        const int64_t e = b * kQwzBlock + lane * 8;   // shard element of d[0]
+        if (q.prim_bf16) {
+          const uint2 a = pack_bf16x4(make_float4(d[0], d[1], d[2], d[3]));
+          const uint2 c = pack_bf16x4(make_float4(d[4], d[5], d[6], d[7]));
+          fp += fp_word((uint32_t)(q.fpe.word_base + e / 8), make_int4((int)a.x, (int)a.y, (int)c.x, (int)c.y));
+        } else {
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+            fp += fp_word((uint32_t)(q.fpe.word_base + e / 4 + h),
+                          make_int4(__float_as_int(d[4 * h]), __float_as_int(d[4 * h + 1]),
+                                    __float_as_int(d[4 * h + 2]), __float_as_int(d[4 * h + 3])));
+        }
+      }
     }
   }
-  if (last_cta(q.done_ctr)) release_all(q.rel);   // E1: codes of step t+1 are ready
+  if (emit) emit_fp(fp, q.fpe, q.sync);
+  if (last_cta(q.done_ctr)) release_all(q.rel, q.sync);   // E1: codes of step t+1 are ready
 }
 
 // qwZ forward gather: producer TMA-pulls 8192-element chunks of source j's codes (8 KiB)
@@ -650,7 +678,7 @@ __global__ void __launch_bounds__(32 + kQwConsumers, 1) gather_qwz_kernel(const 
         uint32_t cnt;
         chunk_of(k, j, off, cnt);
         if (!((waited >> j) & 1u)) {
-          if (p.src_flag[j] != nullptr) wait_geq(p.src_flag[j], p.src_target, p.sync);   // E1
+          if (p.src_flag[j] != nullptr) wait_geq(p.src_flag[j], layer_epoch(p.src_target, p.sync), p.sync);   // E1
           fence_proxy_async();
           waited |= 1u << j;
         }
@@ -723,18 +751,9 @@ __global__ void __launch_bounds__(32 + kQwConsumers, 1) gather_qwz_kernel(const 
   if (p.fp_acc && threadIdx.x == 0) {
     unsigned long long sum = 0;
     for (int w = 0; w < kQwConsumers / 32; ++w) sum += fp_red[w];
-    if (sum) atomicAdd(p.fp_acc, sum);
+    if (sum) atomicAdd(p.fp_acc + 2 * ((p.fp_par + epoch_base(p.sync)) & 1u), sum);
   }
-  if (last_cta(p.done_ctr)) {
-    if (p.fp_a != nullptr) {
-      wait_all(p.cmp_wait, p.sync);
-      const unsigned long long a = atomicExch(p.fp_a, 0ull);
-      const unsigned long long b = atomicExch(p.fp_b, 0ull);
-      atomicAdd(p.fp_checked, 1ull);
-      if (a != b) atomicAdd(p.fp_mism, 1ull);
-    }
-    release_all(p.rel);
-  }
+  if (last_cta(p.done_ctr)) gather_finish(p);
 }
 
 }  // namespace

@@ -29,9 +29,12 @@ EXPORTED = [
     "hpz_set_timeout", "hpz_load_master", "hpz_synth_master", "hpz_fwd_gather", "hpz_bwd_gather",
     "hpz_grad_buffer", "hpz_grad_upload", "hpz_synth_grads", "hpz_grads_ready",
     "hpz_reduce_scatter", "hpz_step", "hpz_reduce_scatter_adam", "hpz_set_option", "hpz_load_state",
+    "hpz_resync_step",
 ]
 OPT = {"store_grad_shard": 0, "ctas_per_sm": 1, "copy_engine": 2, "qgz": 3, "grad_dtype": 4, "qwz": 5, "max_ctas": 6,
-       "bwd_ctas": 10, "rs_ctas": 11}
+       "bwd_ctas": 10, "rs_ctas": 11, "device_epoch": 13, "fault": 14,
+       "alias_secondary": 15}
+FAULT_SKIP_E1, FAULT_SKIP_E2 = 1, 2
 COPY = {"ldg": 0, "tma": 1}
 
 
@@ -49,7 +52,8 @@ class hpz_layer_info_t(ctypes.Structure):
 
 class hpz_counters_t(ctypes.Structure):
     _fields_ = [("mismatches", c_uint64), ("nan_reads", c_uint64), ("fp_mismatches", c_uint64),
-                ("fp_checked", c_uint64), ("timeouts", c_uint64), ("launches", c_uint64)]
+                ("fp_checked", c_uint64), ("timeouts", c_uint64), ("launches", c_uint64),
+                ("fp_fwd_mismatches", c_uint64), ("fp_fwd_checked", c_uint64)]
 
 
 class HpzError(RuntimeError):
@@ -76,6 +80,7 @@ def _load() -> ctypes.CDLL:
         "hpz_arena_ptr": (c_int, [P, c_int, POINTER(c_void_p)]),
         "hpz_buffer": (c_int, [P, c_int, c_int, POINTER(c_void_p), POINTER(c_int64)]),
         "hpz_current_step": (c_int, [P, POINTER(c_int64)]),
+        "hpz_resync_step": (c_int, [P]),
         "hpz_counters": (c_int, [P, POINTER(hpz_counters_t), c_int]),
         "hpz_last_error": (c_char_p, [P]),
         "hpz_set_order": (c_int, [P, c_int, c_int, c_int]),
@@ -185,6 +190,10 @@ def hpz_current_step(ctx) -> int:
     t = c_int64()
     _check(ctx, "hpz_current_step", LIB.hpz_current_step(ctx, byref(t)))
     return t.value
+
+
+def hpz_resync_step(ctx):
+    _check(ctx, "hpz_resync_step", LIB.hpz_resync_step(ctx))
 
 
 def hpz_counters(ctx, reset: bool = False) -> dict:

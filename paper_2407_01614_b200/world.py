@@ -75,7 +75,9 @@ def sum_over_ranks(values: list[float], device=None) -> list[float]:
     return t.tolist()
 
 
-def _register(ctx, numels, dtype, align, n_grad_slots, qgz=False, grad_dtype="f32", qwz=False):
+def _register(ctx, numels, dtype, align, n_grad_slots, qgz=False, grad_dtype="f32", qwz=False, alias_secondary=True):
+    if not alias_secondary:
+        H.hpz_set_option(ctx, "alias_secondary", 0)   # keep a separate secondary at P' == P
     if qgz:
         H.hpz_set_option(ctx, "qgz", 4)        # sizes the arena: must precede register
     if qwz:
@@ -91,13 +93,13 @@ class EmulatedWorld:
     """P ranks on one GPU in one process (test harness for the multi-rank protocol)."""
 
     def __init__(self, numels, world, node_size, dtype="bf16", align=256, n_grad_slots=None,
-                 device=0, timeout_s=20.0, qgz=False, grad_dtype="f32", qwz=False):
+                 device=0, timeout_s=20.0, qgz=False, grad_dtype="f32", qwz=False, alias_secondary=True):
         self.world, self.node_size, self.dtype = world, node_size, dtype
         self.numels = list(numels)
         self.ranks: list[RankCtx] = []
         for r in range(world):
             ctx = H.hpz_init(world, node_size, r, device)
-            _register(ctx, self.numels, dtype, align, n_grad_slots, qgz, grad_dtype, qwz)
+            _register(ctx, self.numels, dtype, align, n_grad_slots, qgz, grad_dtype, qwz, alias_secondary)
             H.hpz_arena_alloc(ctx)
             H.hpz_set_timeout(ctx, timeout_s)
             self.ranks.append(RankCtx(ctx, r, world, node_size, self.numels))
@@ -117,7 +119,7 @@ class DistWorld:
     """This process's single rank of a torch.distributed world (one GPU per process)."""
 
     def __init__(self, numels, node_size, dtype="bf16", align=256, n_grad_slots=None, device=None,
-                 group=None, timeout_s=20.0, qgz=False, grad_dtype="f32", qwz=False):
+                 group=None, timeout_s=20.0, qgz=False, grad_dtype="f32", qwz=False, alias_secondary=True):
         import torch.distributed as dist
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
@@ -126,7 +128,8 @@ class DistWorld:
         self.numels = list(numels)
         dev = torch.cuda.current_device() if device is None else device
         ctx = H.hpz_init(self.world, node_size, self.rank, dev)
-        self.arena_bytes = _register(ctx, self.numels, dtype, align, n_grad_slots, qgz, grad_dtype, qwz)
+        self.arena_bytes = _register(ctx, self.numels, dtype, align, n_grad_slots, qgz, grad_dtype, qwz,
+                                     alias_secondary)
         handle = H.hpz_arena_alloc(ctx)
         H.hpz_set_timeout(ctx, timeout_s)
         virtual_nodes(self.world, node_size)         # validates the topology early

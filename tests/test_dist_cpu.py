@@ -93,7 +93,7 @@ def test_bench_reference_arm_without_launcher():
     import bench
     import argparse
     args = argparse.Namespace(model="falcon7b", order="fixed", verify="fingerprint", copy_engine="tma", overlap_bwd=0,
-                              qgz=False, grad_dtype="f32", qwz=False)
+                              qgz=False, grad_dtype="f32", qwz=False, graph=1)
     from paper_2407_01614_b200 import shapes
     n = shapes.numels("falcon7b")
     assert d["config"] == bench.make_config(args, 8, 4, len(n), sum(n), len(n))

@@ -20,7 +20,8 @@ def _train(order, steps=6, depth=1, h=512, L=4, T=256):
     from paper_2407_01614_b200.overlap import PrefetchTrainer
     from paper_2407_01614_b200.world import EmulatedWorld, buffer_view
     from synth import inputs as S
-    w = EmulatedWorld([h * h] * L, 1, 1, grad_dtype="bf16", timeout_s=10.0)
+    # stock needs a separate secondary to race on (at P' == P it is aliased to the primary)
+    w = EmulatedWorld([h * h] * L, 1, 1, grad_dtype="bf16", timeout_s=10.0, alias_secondary=order != "stock")
     try:
         rc = w.ranks[0]
         H.hpz_set_order(rc.ctx, order, stock_delay_us=5000 if order == "stock" else 0,
@@ -71,7 +72,8 @@ def _train_tf(order, steps=5, h=256, L=3, B=2, S=128, f=512, heads=4):
     from paper_2407_01614_b200.overlap import PrefetchTrainer, block_numel
     from paper_2407_01614_b200.world import EmulatedWorld
     from synth import inputs as S_
-    w = EmulatedWorld([block_numel(h, f)] * L, 1, 1, grad_dtype="bf16", timeout_s=10.0)
+    w = EmulatedWorld([block_numel(h, f)] * L, 1, 1, grad_dtype="bf16", timeout_s=10.0,
+                      alias_secondary=order != "stock")
     try:
         rc = w.ranks[0]
         H.hpz_set_order(rc.ctx, order, stock_delay_us=5000 if order == "stock" else 0,

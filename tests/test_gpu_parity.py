@@ -321,7 +321,7 @@ def test_missing_peer_times_out_instead_of_hanging():
     import time
     from paper_2407_01614_b200 import hpz as H
     from paper_2407_01614_b200.world import EmulatedWorld
-    w = EmulatedWorld([50_000], 2, 2, timeout_s=1.0)
+    w = EmulatedWorld([50_000], 4, 2, timeout_s=1.0)
     try:
         s = torch.cuda.current_stream()
         w0 = torch.from_numpy(S.layer_params(0, 50_000)).cuda()
@@ -508,3 +508,205 @@ def test_paper_order_with_one_reused_full_buffer():
                 assert np.array_equal(got.view(np.uint32), o.state[i][rc.rank].master.view(np.uint32)), (i, rc.rank)
     finally:
         w.close()
+
+
+# ---------------------------------------------------------------- a7: owner-emitted fingerprints
+def test_forward_fingerprint_checked_against_owners():
+    """FINGERPRINT mode compares every forward gather with the checksum its owners emitted
+    when they wrote the primaries (init, then every Adam): all checked, none differ."""
+    run = ParityRun(NUMELS, 4, 2, fused=True, verify="fingerprint")
+    try:
+        for _ in range(3):
+            _check_step(run, run.step())
+        c = run.counters()
+        assert c["fp_fwd_checked"] == 3 * len(NUMELS) * 4 and c["fp_fwd_mismatches"] == 0, c
+        assert c["fp_checked"] == 3 * len(NUMELS) * 4 and c["fp_mismatches"] == 0, c
+    finally:
+        run.close()
+
+
+def test_forward_fingerprint_qwz_and_unfused():
+    """Same with qwZ (the quantizer emits the dequantized words' checksum) and with the
+    unfused Adam kernel."""
+    for kw in (dict(qwz=True, fused=True), dict(fused=False), dict(fused=False, copy_engine="ldg")):
+        run = ParityRun(NUMELS, 4, 2, verify="fingerprint", **kw)
+        try:
+            for _ in range(2):
+                _check_step(run, run.step())
+            c = run.counters()
+            assert c["fp_fwd_checked"] == 2 * len(NUMELS) * 4 and c["fp_fwd_mismatches"] == 0, (kw, c)
+        finally:
+            run.close()
+
+
+def _sleep_ms(ms, stream):
+    with torch.cuda.stream(stream):
+        torch.cuda._sleep(int(ms * 2.0e6))     # ~2 GHz SM clock
+
+
+@pytest.mark.parametrize("fault", [0, 1])
+def test_fingerprint_catches_forward_read_before_adam(fault):
+    """E1 (PRIMARY_READY) removed on purpose (HPZ_FAULT_SKIP_E1): the owner's Adam of step 0
+    is held back on a side stream while the forward gathers of step 1 run — they read the
+    pre-step primary and the forward-vs-owner fingerprint fires.  With the edge in place
+    (fault 0) the same schedule waits and reads W_1: no mismatch.  Grids are capped so the
+    waiting kernels never fill the GPU (B200_PROFILING.md)."""
+    from paper_2407_01614_b200 import hpz as H
+    numels = [300_007, 65_536]
+    run = ParityRun(numels, 2, 1, fused=True, verify="fingerprint")
+    try:
+        for rc in run.w.ranks:
+            H.hpz_set_option(rc.ctx, "max_ctas", 32)
+        _check_step(run, run.step())
+        run.counters()                                   # reset
+        main, side = run.stream, torch.cuda.Stream()
+        bufs = run.fwd
+        for rc in run.w.ranks:
+            H.hpz_set_option(rc.ctx, "fault", H.FAULT_SKIP_E1 if fault else 0)
+        run._keep = []
+        L = len(numels)
+        for i in range(L):
+            for rc in run.w.ranks:
+                H.hpz_fwd_gather(rc.ctx, i, bufs[rc.rank][i].data_ptr(), main)
+        for i in reversed(range(L)):
+            for rc in run.w.ranks:
+                H.hpz_bwd_gather(rc.ctx, i, run.bwd[rc.rank][i].data_ptr(), main)
+            for rc in run.w.ranks:
+                run.grad_fn(rc, i)
+                H.hpz_grads_ready(rc.ctx, i, main)
+        side.wait_stream(main)
+        _sleep_ms(50, side)
+        for i in reversed(range(L)):
+            H.hpz_reduce_scatter_adam(run.w.ranks[0].ctx, i, run.adam, side)   # owner 0: late
+            H.hpz_reduce_scatter_adam(run.w.ranks[1].ctx, i, run.adam, main)
+        for i in range(L):                                                   # step 1 forward
+            for rc in run.w.ranks:
+                H.hpz_fwd_gather(rc.ctx, i, bufs[rc.rank][i].data_ptr(), main)
+        torch.cuda.synchronize()
+        c = run.counters()
+        assert c["timeouts"] == 0, c
+        if fault:
+            assert c["fp_fwd_mismatches"] > 0, c
+        else:
+            assert c["fp_fwd_mismatches"] == 0 and c["fp_fwd_checked"] == 2 * L * 2, c
+    finally:
+        run.close()
+
+
+@pytest.mark.parametrize("fault", [0, 2])
+def test_fingerprint_catches_adam_overwriting_a_read_primary(fault):
+    """E2 (FWD_DONE) removed on purpose (HPZ_FAULT_SKIP_E2): rank 1 publishes its step-1
+    gradients early (hpz_grads_ready) and its forward gathers of step 1 lag on another stream,
+    so nothing but E2 keeps owner 0's Adam from overwriting its primary with W_2 while rank 1
+    still has to read W_1.  Without E2 rank 1 gathers the wrong version and its forward
+    fingerprint differs from the owners'; with E2 (fault 0) the same schedule is safe."""
+    from paper_2407_01614_b200 import hpz as H
+    numels = [300_007, 65_536]
+    run = ParityRun(numels, 2, 1, fused=True, verify="fingerprint")
+    try:
+        for rc in run.w.ranks:
+            H.hpz_set_option(rc.ctx, "max_ctas", 32)
+        _check_step(run, run.step())
+        run.counters()                                   # reset
+        main, s1, sdelay = run.stream, torch.cuda.Stream(), torch.cuda.Stream()
+        r0, r1 = run.w.ranks
+        H.hpz_set_option(r0.ctx, "fault", fault)
+        L = len(numels)
+        gs = {(rc.rank, i): torch.from_numpy(S.layer_grads(i, run.t, rc.rank, lay.numel)).cuda()
+              for rc in run.w.ranks for i, lay in enumerate(run.o.layouts)}
+        torch.cuda.synchronize()
+        for i in reversed(range(L)):                     # rank 1: gradients first (early E5)
+            H.hpz_grad_upload(r1.ctx, i, gs[(1, i)].data_ptr(), numels[i], s1)
+            H.hpz_grads_ready(r1.ctx, i, s1)
+        _sleep_ms(50, sdelay)
+        for i in range(L):
+            H.hpz_fwd_gather(r0.ctx, i, run.fwd[0][i].data_ptr(), main)
+            H.hpz_fwd_gather(r1.ctx, i, run.fwd[1][i].data_ptr(), sdelay)     # rank 1 lags
+        for i in reversed(range(L)):
+            H.hpz_bwd_gather(r0.ctx, i, run.bwd[0][i].data_ptr(), main)
+            H.hpz_bwd_gather(r1.ctx, i, run.bwd[1][i].data_ptr(), sdelay)
+            H.hpz_grad_upload(r0.ctx, i, gs[(0, i)].data_ptr(), numels[i], main)
+            H.hpz_grads_ready(r0.ctx, i, main)
+            H.hpz_reduce_scatter_adam(r0.ctx, i, run.adam, main)
+            H.hpz_reduce_scatter_adam(r1.ctx, i, run.adam, sdelay)
+        torch.cuda.synchronize()
+        c1 = H.hpz_counters(r1.ctx)
+        c0 = H.hpz_counters(r0.ctx)
+        assert c0["timeouts"] == 0 and c1["timeouts"] == 0
+        if fault:
+            assert c1["fp_fwd_mismatches"] > 0, c1
+        else:
+            assert c1["fp_fwd_mismatches"] == 0 and c0["fp_fwd_mismatches"] == 0, (c0, c1)
+            assert c1["fp_fwd_checked"] == L and c0["fp_fwd_checked"] == L, (c0, c1)
+    finally:
+        run.close()
+
+
+# ---------------------------------------------------------------- device epochs + CUDA graphs
+@pytest.mark.parametrize("P,Pp,kw", [(4, 2, {}), (2, 2, {}), (4, 2, {"qgz": True}), (2, 1, {"grad_dtype": "bf16"}),
+                                     (1, 1, {})])
+def test_captured_step_replays_bit_exact(P, Pp, kw):
+    """with device-side epochs a whole training step (every rank's gathers,
+    gradient uploads, fused RS+Adam) is captured ONCE in a CUDA graph and replayed; each
+    replay is a new step — fresh flag epochs and Adam bias corrections from the device
+    counter — and matches the oracle bit for bit over 3 replays, then eager steps resume."""
+    from paper_2407_01614_b200 import hpz as H
+    run = ParityRun(NUMELS, P, Pp, fused=True, verify="fingerprint", **kw)
+    try:
+        for rc in run.w.ranks:
+            H.hpz_set_option(rc.ctx, "device_epoch", 1)
+        _check_step(run, run.step())                 # eager step 0 in device-epoch mode
+        L = len(NUMELS)
+        gdt = torch.bfloat16 if run.grad_dtype == "bf16" else torch.float32
+        gstatic = [[torch.zeros(run.o.layouts[i].numel, dtype=gdt, device="cuda") for i in range(L)]
+                   for _ in range(P)]
+
+        def fill(t):
+            for r in range(P):
+                for i, lay in enumerate(run.o.layouts):
+                    g = torch.from_numpy(S.layer_grads(i, t, r, lay.numel, kind=run.grad_kind)).cuda()
+                    gstatic[r][i].copy_(g.to(gdt))
+            torch.cuda.synchronize()
+
+        def grad_fn(rc, i):
+            H.hpz_grad_upload(rc.ctx, i, gstatic[rc.rank][i].data_ptr(), run.o.layouts[i].numel,
+                              torch.cuda.current_stream())
+
+        from paper_2407_01614_b200.world import run_step
+        graph = torch.cuda.CUDAGraph()
+        fill(1)
+        with torch.cuda.graph(graph):
+            run_step(run.w.ranks, [lambda i, r=r: run.fwd[r][i].data_ptr() for r in range(P)],
+                     [lambda i, r=r: run.bwd[r][i].data_ptr() for r in range(P)], run.adam,
+                     stream=torch.cuda.current_stream(), grad_fn=grad_fn, emulated=True, fused=True)
+        for k in range(3):                          # replays = steps 1, 2, 3
+            fill(1 + k)
+            graph.replay()
+            torch.cuda.synchronize()
+            run.t = 1 + k
+            rec = run.o.step()
+            run.t = 2 + k
+            _check_step(run, rec)
+        for rc in run.w.ranks:
+            H.hpz_resync_step(rc.ctx)
+            assert H.hpz_current_step(rc.ctx) == 4
+        _check_step(run, run.step())                 # eager step 4
+        c = run.counters()
+        assert c["timeouts"] == 0 and c["fp_mismatches"] == 0 and c["fp_fwd_mismatches"] == 0, c
+        assert c["fp_checked"] == 5 * L * P and c["fp_fwd_checked"] == 5 * L * P, c
+    finally:
+        run.close()
+
+
+def test_device_epoch_rejects_uncapturable_orders():
+    from paper_2407_01614_b200 import hpz as H
+    run = ParityRun(NUMELS, 2, 1, fused=True)
+    try:
+        for rc in run.w.ranks:
+            H.hpz_set_option(rc.ctx, "device_epoch", 1)
+            H.hpz_set_order(rc.ctx, "paper")
+        with pytest.raises(H.HpzError) as e:
+            H.hpz_fwd_gather(run.w.ranks[0].ctx, 0, run.fwd[0][0].data_ptr(), run.stream)
+        assert e.value.code == H.HPZ_ESTATE
+    finally:
+        run.close()

@@ -26,7 +26,9 @@ def run(order, args, world, rank, local, node_size, numels):
     from paper_2407_01614_b200 import hpz as H
     from paper_2407_01614_b200.world import DistWorld, EmulatedWorld, sum_over_ranks
     from synth import inputs as S
-    kw = dict(n_grad_slots=2, timeout_s=60.0, qgz=args.qgz, qwz=args.qwz, grad_dtype=args.grad_dtype)
+    # the stock race needs a secondary of its own (at P' == P it is aliased to the primary)
+    kw = dict(n_grad_slots=2, timeout_s=60.0, qgz=args.qgz, qwz=args.qwz, grad_dtype=args.grad_dtype,
+              alias_secondary=order != "stock")
     if world > 1:
         W = DistWorld(numels, node_size, device=local, **kw)
     else:

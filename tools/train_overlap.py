@@ -31,7 +31,8 @@ def run(order, depth, args, world, rank, local, node_size):
     per_layer = args.h * args.h if args.model == "mlp" else block_numel(args.h, args.ffn)
     numels = [per_layer] * args.layers
     # qgZ (the paper's Table 2 runs every hpZ variant with qgZ) quantizes fp32 gradients
-    kw = dict(n_grad_slots=len(numels), timeout_s=60.0, grad_dtype="f32" if args.qgz else "bf16", qgz=args.qgz)
+    kw = dict(n_grad_slots=len(numels), timeout_s=60.0, grad_dtype="f32" if args.qgz else "bf16", qgz=args.qgz,
+              alias_secondary=order not in ("stock", "paper"))   # the stock / paper copies need a secondary
     W = DistWorld(numels, node_size, device=local, **kw) if world > 1 else EmulatedWorld(numels, 1, 1, device=local, **kw)
     rc = W.ranks[0]
     H.hpz_set_order(rc.ctx, order, stock_delay_us=args.stock_delay_us if order == "stock" else 0,
