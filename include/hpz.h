@@ -247,6 +247,16 @@ HPZ_API int hpz_load_state(hpz_ctx* ctx, int layer, const float* master, const f
  * OFF: no secondary. */
 HPZ_API int hpz_fwd_gather(hpz_ctx* ctx, int layer, void* full_out, void* stream);
 
+/* ORDER_STOCK / ORDER_PAPER with HPZ_OPT_COPY_BY_CALLER: enqueue Alg. 1's "L_i,second <-
+ * empty(|L_i|/P'); Copy to L_i,second (Async MemcpyD2D)" for this step's
+ * forward-gathered full buffer of `layer`, on the context's side stream after the work
+ * already enqueued on `stream` (optional poison fill and delay first, hpz_set_order).  The
+ * copy reads that full buffer after the call returns; later hpz gathers into the same buffer
+ * wait for it, other writes by the caller must be ordered after it by the caller.  ESTATE
+ * outside those orders / without the option, before the layer's forward gather of the step,
+ * or twice in a step.  No-op when the secondary is aliased (P' = P). */
+HPZ_API int hpz_secondary_copy(hpz_ctx* ctx, int layer, void* stream);
+
 /* Backward gather of layer `layer` at step t (Alg. 1, AllGather(L_i, P')):
  * full_out[numel_pad] = concatenation of the P' secondaries of this rank's node.
  * FIXED: each source is read only after its owner released SEC_READY for step t — the
@@ -344,7 +354,7 @@ typedef enum {
                                     between steps with the device idle; bound arenas only. */
   HPZ_OPT_FAULT = 14,            /* TEST ONLY, 0 = off: HPZ_FAULT_* bits remove an ordering
                                     edge on purpose to prove the detector sees the violation */
-  HPZ_OPT_ALIAS_SECONDARY = 15   /* 1 (default) / 0, before hpz_register_flat_params.  With
+  HPZ_OPT_ALIAS_SECONDARY = 15,  /* 1 (default) / 0, before hpz_register_flat_params.  With
                                     P' = P (one node) the secondary slice of a rank IS its primary
                                     shard (Eq. (1) with P' = P): the arena stores no
                                     second copy, the forward gather writes no secondary and the
@@ -353,6 +363,11 @@ typedef enum {
                                     0 keeps a separate secondary at P' = P — needed only to
                                     reproduce the stock / paper copy on a one-node world.  No
                                     effect with qwZ (its secondary holds dequantized weights). */
+  HPZ_OPT_COPY_BY_CALLER = 16    /* 0 (default) / 1, ORDER_STOCK / ORDER_PAPER: hpz_fwd_gather
+                                    does not enqueue the secondary copy; the caller issues it with
+                                    hpz_secondary_copy where Alg. 1 does (after L_i.forward(),
+                                    PAPER.md:103-105) — e.g. to reproduce which backward gathers a
+                                    prefetching schedule races. */
 } hpz_option;
 #define HPZ_FAULT_SKIP_E1 1   /* forward gathers read primaries without acquiring PRIMARY_READY */
 #define HPZ_FAULT_SKIP_E2 2   /* Adam overwrites the primary without waiting for its readers   */

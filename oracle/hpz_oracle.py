@@ -375,7 +375,43 @@ def toy_batch(step: int, rank: int, batch: int = 64, dims=TOY_DIMS, identical: b
 # ----------------------------------------------------------------------------
 
 ORDERS = ("fixed", "stock", "off")
-STOCK_SCHEDULES = ("program", "adversarial_stale", "realloc", "half_written")
+STOCK_SCHEDULES = ("program", "adversarial_stale", "realloc", "half_written", "realistic")
+
+
+def prefetch_enqueue_order(n_layers: int, depth: int) -> list[tuple]:
+    """The operations Algorithm 1 enqueues in one step, in program order,
+    with ZeRO-3 prefetch of `depth` modules (reading R12).  Modules execute in the order
+    fwd L_1..L_N, bwd L_N..L_1.  For each module: "Ensure AllGather(L_i) finished" (an
+    AllGather not prefetched earlier is enqueued now, on demand), PrefetchAllGather() (the
+    AllGathers of the next `depth` modules not yet enqueued — forward ones over P, backward
+    ones over P'), the module's compute, and — after a forward — "L_i,second <- empty; Copy to
+    L_i,second (Async MemcpyD2D)".  Layers are 0-based.  Returns
+    [("gather", "fwd"|"bwd", i) | ("copy", i), ...]."""
+    modules = [("fwd", i) for i in range(n_layers)] + [("bwd", i) for i in reversed(range(n_layers))]
+    seq, enq = [], set()
+    for pos, m in enumerate(modules):
+        if m not in enq:                                   # Ensure AllGather(L_i) finished
+            enq.add(m)
+            seq.append(("gather",) + m)
+        for nxt in modules[pos + 1:pos + 1 + depth]:       # PrefetchAllGather()
+            if nxt not in enq:
+                enq.add(nxt)
+                seq.append(("gather",) + nxt)
+        if m[0] == "fwd":                                  # L_i.forward(); then the async copy
+            seq.append(("copy", m[1]))
+    return seq
+
+
+def realistic_racing_layers(n_layers: int, depth: int) -> set[int]:
+    """Layers whose backward AllGather(L_i, P') is ENQUEUED before their own secondary copy
+    under Alg. 1 with prefetch depth `depth`: without the fix (stock ZeRO++) nothing orders
+    the two, so the gather can read the secondary "still being partitioned" — the race of
+    PAPER.md:130-132, at the forward->backward turnaround of Fig. 1.  Every
+    other backward gather is enqueued after its copy (R13: in the realistic schedule those
+    read the fresh copy).  Pins: tests/test_oracle_step.py (closed form: the last
+    ceil(depth/2) layers, none without prefetch)."""
+    seq = prefetch_enqueue_order(n_layers, depth)
+    return {i for i in range(n_layers) if seq.index(("gather", "bwd", i)) < seq.index(("copy", i))}
 
 
 @dataclass
@@ -407,7 +443,9 @@ class HpzOracle:
     backward gather (R5, R13): "program" (copy lands first), "adversarial_stale"
     (every backward read happens before this step's copy: persistent buffer holds
     the previous step's slice, poison at t=0), "realloc" (fresh torch.empty each
-    step, read before the copy: poison), "half_written" (a seeded prefix refreshed).
+    step, read before the copy: poison), "half_written" (a seeded prefix refreshed),
+    "realistic" (only the layers `realistic_racing_layers(N, prefetch_depth)` read before
+    their copy — the previous step's slice, poison at t=0 — every other layer after it).
     """
     numels: list[int]
     world: int
@@ -422,6 +460,7 @@ class HpzOracle:
     grad_kind: str = "uniform"
     toy_identical_batches: bool = False
     half_seed: int = 1234
+    prefetch_depth: int = 1              # "realistic" stock schedule (R12)
     qgz: bool = False                    # f1: INT4 quantized gradient all-to-all (qgz_reduce_scatter)
     grad_dtype: str = "f32"              # f4: "bf16" = gradients stored/communicated as bf16 (RNE)
     qwz: bool = False                    # f2: INT8 blockwise weights in the forward AllGather
@@ -498,12 +537,15 @@ class HpzOracle:
             if self.order == "off":
                 continue
             # L_i,second <- empty(|L_i|/P'); async copy
+            racing = (realistic_racing_layers(L, self.prefetch_depth)
+                      if self.stock_schedule == "realistic" else set())
             for r in range(P):
                 st = self.state[i][r]
                 fresh = secondary_copy(F[r], lay, r)
-                if self.order == "fixed" or self.stock_schedule == "program":
+                if self.order == "fixed" or self.stock_schedule == "program" or \
+                        (self.stock_schedule == "realistic" and i not in racing):
                     st.sec = fresh                      # the wait orders it
-                elif self.stock_schedule == "adversarial_stale":
+                elif self.stock_schedule in ("adversarial_stale", "realistic"):
                     st.pending = fresh                  # lands only after the backward read
                 elif self.stock_schedule == "realloc":
                     st.sec = poison_like(lay.sec_shard, self.param_dtype)

@@ -33,6 +33,10 @@ struct Layer {
   // host bookkeeping of the step t the layer's ops were issued for (-1: never)
   int64_t fwd_t = -1, bwd_t = -1, rs_t = -1, step_t = -1;
   int64_t fpx_t = -1;    // step whose forward gather the owner's last fingerprint emission targets
+  char* fwd_out = nullptr;          // full buffer of the last forward gather
+  int64_t copy_t = -1;              // stock / paper: step of the last secondary copy issued
+  const char* copy_src = nullptr;   // ... its source range while it may still be pending
+  int64_t copy_bytes = 0;
 };
 
 }  // namespace
@@ -55,6 +59,7 @@ struct hpz_ctx {
   // (E1 acquire, E7 release).  Not with qwZ, whose secondary holds dequantized weights.
   bool alias_sec = false;
   bool alias_opt = true;                  // HPZ_OPT_ALIAS_SECONDARY
+  bool copy_by_caller = false;            // HPZ_OPT_COPY_BY_CALLER
   char* arena[kMaxWorld] = {};            // mapped arena base of every rank
   bool opened[kMaxWorld] = {};            // arena[j] was opened via IPC here
   int64_t t = 0;                          // current step (flag epochs)
@@ -681,6 +686,71 @@ int hpz_synth_master(hpz_ctx* c, int layer, uint64_t key, float scale, void* str
   return do_init_shard(c, layer, nullptr, key, scale, static_cast<cudaStream_t>(stream));
 }
 
+// Stock / paper secondary write (Alg. 1: "L_i,second <- empty(|L_i|/P');
+// Copy to L_i,second (Async MemcpyD2D)"): a copy from the layer's forward-gathered full
+// buffer on the context's side stream, after the work already on `s`.  STOCK: no edge to the
+// backward AllGather (the race).  PAPER: SEC_READY + a host-visible
+// "MemcpyD2D finished" event the backward gather waits for on the HOST (Alg. 1 blue lines).
+// The copy reads the caller's full buffer after this call returns: the next hpz gather into
+// the same buffer waits for it (the stream-side equivalent of record_stream on L_i).
+static int secondary_copy(hpz_ctx* c, int layer, cudaStream_t s) {
+  Layer& L = c->layers[layer];
+  const int nf = c->node_first();
+  char* sec = c->arena[c->rank] + L.off_secondary;
+  const int64_t sec_bytes = L.sec_shard * c->elem;
+  cudaError_t e;
+  HPZ_CUDA(c, cudaEventRecord(c->side_ev, s));
+  HPZ_CUDA(c, cudaStreamWaitEvent(c->side, c->side_ev, 0));
+  if (c->order == HPZ_ORDER_PAPER && c->t > 0) {
+    // E4 (P2P needs it; NCCL's rendezvous would cover it): node peers' step t-1 reads done
+    WaitList w{};
+    for (int q = 0; q < c->node_size; ++q) w.ptr[w.n++] = c->flag(c->rank, F_BWD_DONE, layer, nf + q);
+    w.target = c->lv(c->t);
+    e = launch_wait(w, c->sync(), c->side);
+    if (e != cudaSuccess) return fail(c, HPZ_ECUDA, "wait launch: %s", cudaGetErrorString(e));
+    c->launches += 1;
+  }
+  if (c->stock_poison) {
+    e = launch_fill_u32(sec, c->elem == 2 ? 0x7FC07FC0u : 0x7FC00000u, sec_bytes, grid_for(c, sec_bytes / 4096 + 1, 4), c->side);
+    if (e != cudaSuccess) return fail(c, HPZ_ECUDA, "poison launch: %s", cudaGetErrorString(e));
+    c->launches += 1;
+  }
+  if (c->stock_delay_us > 0) {
+    e = launch_delay(c->stock_delay_us, c->side);
+    if (e != cudaSuccess) return fail(c, HPZ_ECUDA, "delay launch: %s", cudaGetErrorString(e));
+    c->launches += 1;
+  }
+  e = launch_copy(sec, L.fwd_out + (int64_t)c->local() * sec_bytes, sec_bytes, grid_for(c, sec_bytes / 4096 + 1, 4), c->side);
+  if (e != cudaSuccess) return fail(c, HPZ_ECUDA, "stock copy launch: %s", cudaGetErrorString(e));
+  c->launches += 1;
+  if (c->order == HPZ_ORDER_PAPER) {
+    // publish SEC_READY to the node (what the collective's rendezvous does for NCCL)
+    ReleaseList r{};
+    for (int q = 0; q < c->node_size; ++q) r.ptr[r.n++] = c->flag(nf + q, F_SEC_READY, layer, c->rank);
+    r.value = c->lv(c->t + 1);
+    e = launch_release(r, c->sync(), c->side);
+    if (e != cudaSuccess) return fail(c, HPZ_ECUDA, "release launch: %s", cudaGetErrorString(e));
+    c->launches += 1;
+  }
+  HPZ_CUDA(c, cudaEventRecord(c->copy_ev[layer], c->side));
+  L.copy_t = c->t;
+  L.copy_src = L.fwd_out;
+  L.copy_bytes = L.numel_pad * c->elem;
+  return HPZ_OK;
+}
+
+// A gather about to write [out, out + bytes) waits for every pending stock / paper copy that
+// reads from that range (issued earlier on the side stream), then forgets it.
+static int wait_pending_copies(hpz_ctx* c, const char* out, int64_t bytes, cudaStream_t s) {
+  for (int i = 0; i < c->n_layers; ++i) {
+    Layer& L = c->layers[i];
+    if (!L.copy_src || L.copy_src >= out + bytes || L.copy_src + L.copy_bytes <= out) continue;
+    HPZ_CUDA(c, cudaStreamWaitEvent(s, c->copy_ev[i], 0));
+    L.copy_src = nullptr;
+  }
+  return HPZ_OK;
+}
+
 int hpz_fwd_gather(hpz_ctx* c, int layer, void* full_out, void* stream) {
   if (int rc = check_ready(c)) return rc;
   if (int rc = check_layer(c, layer)) return rc;
@@ -734,6 +804,7 @@ int hpz_fwd_gather(hpz_ctx* c, int layer, void* full_out, void* stream) {
   for (int j = 0; j < c->world; ++j) p.rel.ptr[p.rel.n++] = c->flag(j, F_FWD_DONE, layer, c->rank);            // E2
   p.rel.value = t1;
   p.sync = c->sync();
+  if (int rc = wait_pending_copies(c, p.out, L.numel_pad * c->elem, s)) return rc;
   cudaError_t e;
   if (c->qwz_bits) {
     // qwZ: pull every owner's INT8 codes + (min, scale) and dequantize (f2, R28)
@@ -748,54 +819,23 @@ int hpz_fwd_gather(hpz_ctx* c, int layer, void* full_out, void* stream) {
   }
   if (e != cudaSuccess) return fail(c, HPZ_ECUDA, "fwd gather launch: %s", cudaGetErrorString(e));
   c->launches += 1;
-  if ((c->order == HPZ_ORDER_STOCK || c->order == HPZ_ORDER_PAPER) && !c->alias_sec) {
-    // L_i,second <- empty(); async MemcpyD2D on another stream.  STOCK:
-    // no edge to the backward AllGather (the race).  PAPER: the copy is
-    // followed by an event the backward gather waits for on the HOST (Alg. 1 blue lines)
-    char* sec = c->arena[c->rank] + L.off_secondary;
-    const int64_t sec_bytes = L.sec_shard * c->elem;
-    HPZ_CUDA(c, cudaEventRecord(c->side_ev, s));
-    HPZ_CUDA(c, cudaStreamWaitEvent(c->side, c->side_ev, 0));
-    if (c->order == HPZ_ORDER_PAPER && c->t > 0) {
-      // E4 (P2P needs it; NCCL's rendezvous would cover it): node peers' step t-1 reads done
-      WaitList w{};
-      for (int q = 0; q < c->node_size; ++q) w.ptr[w.n++] = c->flag(c->rank, F_BWD_DONE, layer, nf + q);
-      w.target = c->lv(c->t);
-      e = launch_wait(w, c->sync(), c->side);
-      if (e != cudaSuccess) return fail(c, HPZ_ECUDA, "wait launch: %s", cudaGetErrorString(e));
-      c->launches += 1;
-    }
-    if (c->stock_poison) {
-      e = launch_fill_u32(sec, c->elem == 2 ? 0x7FC07FC0u : 0x7FC00000u, sec_bytes, grid_for(c, sec_bytes / 4096 + 1, 4), c->side);
-      if (e != cudaSuccess) return fail(c, HPZ_ECUDA, "poison launch: %s", cudaGetErrorString(e));
-      c->launches += 1;
-    }
-    if (c->stock_delay_us > 0) {
-      e = launch_delay(c->stock_delay_us, c->side);
-      if (e != cudaSuccess) return fail(c, HPZ_ECUDA, "delay launch: %s", cudaGetErrorString(e));
-      c->launches += 1;
-    }
-    e = launch_copy(sec, p.out + (int64_t)l * sec_bytes, sec_bytes, grid_for(c, sec_bytes / 4096 + 1, 4), c->side);
-    if (e != cudaSuccess) return fail(c, HPZ_ECUDA, "stock copy launch: %s", cudaGetErrorString(e));
-    c->launches += 1;
-    if (c->order == HPZ_ORDER_PAPER) {
-      // publish SEC_READY to the node (what the collective's rendezvous does for NCCL) and
-      // record the host-visible "MemcpyD2D finished" event
-      ReleaseList r{};
-      for (int q = 0; q < c->node_size; ++q) r.ptr[r.n++] = c->flag(nf + q, F_SEC_READY, layer, c->rank);
-      r.value = t1;
-      e = launch_release(r, c->sync(), c->side);
-      if (e != cudaSuccess) return fail(c, HPZ_ECUDA, "release launch: %s", cudaGetErrorString(e));
-      c->launches += 1;
-      HPZ_CUDA(c, cudaEventRecord(c->copy_ev[layer], c->side));
-      // the copy reads the caller's full buffer: later work on the caller's stream (e.g. the
-      // next gather into the same buffer) must not overwrite it first — the stream-side
-      // equivalent of the caching allocator's record_stream on L_i
-      HPZ_CUDA(c, cudaStreamWaitEvent(s, c->copy_ev[layer], 0));
-    }
-  }
   L.fwd_t = c->t;
+  L.fwd_out = p.out;
+  if ((c->order == HPZ_ORDER_STOCK || c->order == HPZ_ORDER_PAPER) && !c->alias_sec && !c->copy_by_caller)
+    return secondary_copy(c, layer, s);
   return HPZ_OK;
+}
+
+int hpz_secondary_copy(hpz_ctx* c, int layer, void* stream) {
+  if (int rc = check_ready(c)) return rc;
+  if (int rc = check_layer(c, layer)) return rc;
+  const Layer& L = c->layers[layer];
+  if (!c->copy_by_caller || (c->order != HPZ_ORDER_STOCK && c->order != HPZ_ORDER_PAPER))
+    return fail(c, HPZ_ESTATE, "hpz_secondary_copy: only with HPZ_OPT_COPY_BY_CALLER in ORDER_STOCK / ORDER_PAPER");
+  if (L.fwd_t != c->t) return fail(c, HPZ_ESTATE, "layer %d: secondary copy before its forward gather", layer);
+  if (L.copy_t == c->t) return fail(c, HPZ_ESTATE, "layer %d: secondary copy already issued at step %lld", layer, (long long)c->t);
+  if (c->alias_sec) return HPZ_OK;   // P' == P: the secondary is the primary, nothing to copy
+  return secondary_copy(c, layer, static_cast<cudaStream_t>(stream));
 }
 
 int hpz_bwd_gather(hpz_ctx* c, int layer, void* full_out, void* stream) {
@@ -805,8 +845,11 @@ int hpz_bwd_gather(hpz_ctx* c, int layer, void* full_out, void* stream) {
   Layer& L = c->layers[layer];
   if (L.fwd_t != c->t) return fail(c, HPZ_ESTATE, "layer %d: backward gather without its forward gather at step %lld", layer, (long long)c->t);
   if (L.bwd_t == c->t) return fail(c, HPZ_ESTATE, "layer %d already backward-gathered at step %lld", layer, (long long)c->t);
-  if (c->order == HPZ_ORDER_PAPER)   // Alg. 1: "Repeat wait Until MemcpyD2D on L_k,second finishes" (host)
+  if (c->order == HPZ_ORDER_PAPER && !c->alias_sec) {
+    // Alg. 1: "Repeat wait Until MemcpyD2D on L_k,second finishes" (host)
+    if (L.copy_t != c->t) return fail(c, HPZ_ESTATE, "layer %d: backward gather before its secondary copy (hpz_secondary_copy)", layer);
     HPZ_CUDA(c, cudaEventSynchronize(c->copy_ev[layer]));
+  }
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const uint32_t t1 = c->lv(c->t + 1);
   const int nf = c->node_first();
@@ -873,6 +916,7 @@ int hpz_bwd_gather(hpz_ctx* c, int layer, void* full_out, void* stream) {
       c->launches += 1;
     }
   }
+  if (int rc = wait_pending_copies(c, p.out, L.numel_pad * c->elem, s)) return rc;
   cudaError_t e = gather_launch(c, p, s, c->bwd_ctas);
   if (e != cudaSuccess) return fail(c, HPZ_ECUDA, "bwd gather launch: %s", cudaGetErrorString(e));
   c->launches += 1;
@@ -1209,6 +1253,10 @@ int hpz_set_option(hpz_ctx* c, int option, int64_t value) {
       if (c->registered) return fail(c, HPZ_ESTATE, "the secondary layout must be chosen before hpz_register_flat_params");
       if (value != 0 && value != 1) return fail(c, HPZ_EINVAL, "alias_secondary must be 0 or 1");
       c->alias_opt = value != 0;
+      return HPZ_OK;
+    case HPZ_OPT_COPY_BY_CALLER:
+      if (value != 0 && value != 1) return fail(c, HPZ_EINVAL, "copy_by_caller must be 0 or 1");
+      c->copy_by_caller = value != 0;
       return HPZ_OK;
     case HPZ_OPT_FAULT:
       if (value < 0 || value > (HPZ_FAULT_SKIP_E1 | HPZ_FAULT_SKIP_E2)) return fail(c, HPZ_EINVAL, "bad fault mask");

@@ -34,6 +34,9 @@ constexpr int kGatherChunk = 32768;     // bytes per gather stage (a 4..64 KiB, 
 constexpr int kGatherStages = 4;        // at N=1 and N=4 found no better geometry; profiles/README.md)
 constexpr int kFpWarps = 4;             // fingerprint consumer warps
 constexpr int kRsChunk = 1024;          // base shard elements per RS stage
+#ifndef HPZ_RS_P1_MUL
+#define HPZ_RS_P1_MUL 1                 // P = 1 (local, HBM-bound) chunk multiplier (A/B builds)
+#endif
 constexpr int kRsMaxConsumers = 512;    // up to 16 consumer warps (one float4 each per chunk)
 
 // ------------------------------------------------------------------ PTX wrappers
@@ -251,7 +254,7 @@ struct RsCfg {
   // per stage: P gradient slices (fp32, or qgZ int4 codes + (min, scale) per 64) (+ w, m, v);
   // qgZ chunks are longer so its small code/param copies stay >= 1 KiB / 256 B
   // P=1 (local, HBM-bound): 1024-element chunks keep 6 stages in flight; 2 <= P <= 8: 2048
-  static constexpr int kChunk = (P >= 2 && P <= 8 ? 2 : 1) * (QGZ ? 2 * kRsChunk : kRsChunk);
+  static constexpr int kChunk = (P >= 2 && P <= 8 ? 2 : (P == 1 ? HPZ_RS_P1_MUL : 1)) * (QGZ ? 2 * kRsChunk : kRsChunk);
   static constexpr int kGradBytes = MODE == RS_BF16 ? 2 : 4;
   static constexpr int kCodeBytes = kChunk / 2;
   static constexpr int kParamBytes = kChunk / kQgzBlock * 8;
@@ -267,17 +270,20 @@ struct RsCfg {
 };
 
 // Block = 1 producer warp + consumer warps.  Dynamic smem = kStages * kStageBytes.
-template <int P, bool ADAM, int MODE>
+// FP (with ADAM): the consumers also fingerprint the primary words they write (a7, E1/E2),
+// branch-free; a separate instantiation so the plain kernel keeps its code.
+template <int P, bool ADAM, int MODE, bool FP>
 __global__ void __launch_bounds__(RsCfg<P, ADAM, MODE>::kLead + RsCfg<P, ADAM, MODE>::kConsumers, 1)
     rs_tma_kernel(const __grid_constant__ RSParams r, const __grid_constant__ AdamParams a) {
   using C = RsCfg<P, ADAM, MODE>;
+  static_assert(ADAM || !FP, "fingerprints are emitted by the optimizer");
   constexpr bool QGZ = C::QGZ;
   constexpr bool BF16 = MODE == RS_BF16;
   static_assert(C::kStages >= 2, "stage ring too small");
   extern __shared__ __align__(1024) char smem[];
   __shared__ __align__(8) uint64_t full_bar[C::kStages];
   __shared__ __align__(8) uint64_t empty_bar[C::kStages];
-  uint64_t fp = 0;                 // consumers: fingerprint of the primary words written
+  uint64_t fp = 0;                 // consumers (FP): fingerprint of the primary words written
   const int64_t n = r.n_vec * 4;   // shard elements (multiple of 256)
   const int64_t total = (n + C::kChunk - 1) / C::kChunk;
   const int64_t nk = blockIdx.x < total ? (total - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
@@ -344,13 +350,9 @@ __global__ void __launch_bounds__(RsCfg<P, ADAM, MODE>::kLead + RsCfg<P, ADAM, M
       const char* stc = smem + (size_t)s * C::kStageBytes;
       const float4* wmv = reinterpret_cast<const float4*>(stc + C::kWmvOff);
       // one float4 `ct` of the chunk: fixed-order sum (R7) of the P slices, then Adam (R8);
-      // returns the fingerprint contribution of the primary word(s) written (warp-uniform
-      // call: `ok` false only computes nothing)
-      auto process = [&](const int ct, const bool ok) -> uint64_t {
-        uint2 pk = make_uint2(0u, 0u);
-        float4 w = make_float4(0.f, 0.f, 0.f, 0.f);
+      // w / pk: the new master and bf16 primary (for the fingerprint)
+      auto process = [&](const int ct, float4& w, uint2& pk) {
         const int64_t i = e0 / 4 + ct;   // float4 index in the shard
-        if (ok) {
         float4 x[P];
 #pragma unroll
         for (int j = 0; j < P; ++j) {
@@ -396,28 +398,53 @@ __global__ void __launch_bounds__(RsCfg<P, ADAM, MODE>::kLead + RsCfg<P, ADAM, M
             reinterpret_cast<float4*>(a.prim)[i] = w;
           }
         }
+      };
+      // fingerprint of the primary word(s) of float4 ct, branch-free and warp-uniform (the
+      // bf16 word of float4s 2k, 2k+1 is completed with the neighbour lane's half)
+      auto fingerprint = [&](const int ct, const bool ok, const float4& w, const uint2& pk) {
+        const int64_t i = e0 / 4 + ct;
+        uint64_t h;
+        if (a.prim_bf16) {
+          const uint32_t ox = __shfl_xor_sync(0xffffffffu, pk.x, 1);
+          const uint32_t oy = __shfl_xor_sync(0xffffffffu, pk.y, 1);
+          h = fp_word((uint32_t)(a.fpe.word_base + (i >> 1)), make_int4((int)pk.x, (int)pk.y, (int)ox, (int)oy));
+          h = (ok && !(i & 1)) ? h : 0ull;
+        } else {
+          h = fp_word((uint32_t)(a.fpe.word_base + i), make_int4(__float_as_int(w.x), __float_as_int(w.y),
+                                                                 __float_as_int(w.z), __float_as_int(w.w)));
+          h = ok ? h : 0ull;
         }
-        if (!ADAM || a.fpe.n_dst == 0) return 0ull;
-        return prim_word_fp(a.prim_bf16, ok, i, w, pk, a.fpe.word_base);
+        fp += h;
       };
       // consumer thread ct handles float4 ct of the chunk (and ct + kConsumers, ... when the
       // chunk holds more float4s than there are consumers).  The single-pass form is a
-      // separate branch: compiled as a loop it measured ~13% slower.
-      if constexpr (C::kConsumers * 4 == C::kChunk) {
+      // separate branch: compiled as a loop it measured ~13% slower.  The stage is released
+      // before the fingerprint work (registers only), which overlaps the next stage's wait.
+      constexpr int kIt = C::kChunk / (4 * C::kConsumers);
+      float4 w[kIt];
+      uint2 pk[kIt];
+      bool ok[kIt];
+      if constexpr (kIt == 1) {
         const int ct = threadIdx.x - C::kLead;
-        fp += process(ct, ct * 4 < cnt);
+        ok[0] = ct * 4 < cnt;
+        if (ok[0]) process(ct, w[0], pk[0]);
       } else {
 #pragma unroll
-        for (int it = 0; it < C::kChunk / (4 * C::kConsumers); ++it) {
+        for (int it = 0; it < kIt; ++it) {
           const int ct = threadIdx.x - C::kLead + it * C::kConsumers;
-          fp += process(ct, ct * 4 < cnt);
+          ok[it] = ct * 4 < cnt;
+          if (ok[it]) process(ct, w[it], pk[it]);
         }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty_bar[s]);
+      if constexpr (FP) {
+#pragma unroll
+        for (int it = 0; it < kIt; ++it) fingerprint(threadIdx.x - C::kLead + it * C::kConsumers, ok[it], w[it], pk[it]);
+      }
     }
   }
-  if (ADAM && a.fpe.n_dst > 0) emit_fp(fp, a.fpe, a.sync);
+  if constexpr (FP) emit_fp(fp, a.fpe, a.sync);
   if (last_cta(r.done_ctr)) {
     release_all(r.rel, r.sync);             // E6
     if (ADAM) release_all(a.rel, a.sync);   // E1 (t+1)
@@ -461,13 +488,19 @@ cudaError_t set_smem_attr(int smem) {
   return e;
 }
 
-template <int P, bool ADAM, int MODE>
+template <int P, bool ADAM, int MODE, bool FP = false>
 cudaError_t launch_rs_tma_t(const RSParams& r, const AdamParams& a, int grid, cudaStream_t s) {
   using C = RsCfg<P, ADAM, MODE>;
   const int smem = C::kStages * C::kStageBytes;
-  cudaError_t e = set_smem_attr<rs_tma_kernel<P, ADAM, MODE>>(smem);
+  cudaError_t e = set_smem_attr<rs_tma_kernel<P, ADAM, MODE, FP>>(smem);
   if (e != cudaSuccess) return e;
-  return launch_pdl(rs_tma_kernel<P, ADAM, MODE>, grid, C::kLead + C::kConsumers, smem, s, r, a);
+  return launch_pdl(rs_tma_kernel<P, ADAM, MODE, FP>, grid, C::kLead + C::kConsumers, smem, s, r, a);
+}
+
+template <int P, int MODE>
+cudaError_t launch_rs_adam_tma(const RSParams& r, const AdamParams& a, int grid, cudaStream_t s) {
+  return a.fpe.n_dst > 0 ? launch_rs_tma_t<P, true, MODE, true>(r, a, grid, s)
+                         : launch_rs_tma_t<P, true, MODE, false>(r, a, grid, s);
 }
 
 // qgZ quantizer: 4 threads per 64-element block, each holding 4 float4s (elements
@@ -789,9 +822,9 @@ template <int P>
 cudaError_t launch_rs_tma_p(const RSParams& r, const AdamParams* a, int grid, cudaStream_t s, int mode) {
   AdamParams none{};
   switch (mode) {
-    case RS_F32: return a ? launch_rs_tma_t<P, true, RS_F32>(r, *a, grid, s) : launch_rs_tma_t<P, false, RS_F32>(r, none, grid, s);
-    case RS_BF16: return a ? launch_rs_tma_t<P, true, RS_BF16>(r, *a, grid, s) : launch_rs_tma_t<P, false, RS_BF16>(r, none, grid, s);
-    case RS_QGZ: return a ? launch_rs_tma_t<P, true, RS_QGZ>(r, *a, grid, s) : launch_rs_tma_t<P, false, RS_QGZ>(r, none, grid, s);
+    case RS_F32: return a ? launch_rs_adam_tma<P, RS_F32>(r, *a, grid, s) : launch_rs_tma_t<P, false, RS_F32>(r, none, grid, s);
+    case RS_BF16: return a ? launch_rs_adam_tma<P, RS_BF16>(r, *a, grid, s) : launch_rs_tma_t<P, false, RS_BF16>(r, none, grid, s);
+    case RS_QGZ: return a ? launch_rs_adam_tma<P, RS_QGZ>(r, *a, grid, s) : launch_rs_tma_t<P, false, RS_QGZ>(r, none, grid, s);
     default: return cudaErrorInvalidValue;
   }
 }

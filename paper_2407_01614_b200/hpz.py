@@ -29,11 +29,11 @@ EXPORTED = [
     "hpz_set_timeout", "hpz_load_master", "hpz_synth_master", "hpz_fwd_gather", "hpz_bwd_gather",
     "hpz_grad_buffer", "hpz_grad_upload", "hpz_synth_grads", "hpz_grads_ready",
     "hpz_reduce_scatter", "hpz_step", "hpz_reduce_scatter_adam", "hpz_set_option", "hpz_load_state",
-    "hpz_resync_step",
+    "hpz_resync_step", "hpz_secondary_copy",
 ]
 OPT = {"store_grad_shard": 0, "ctas_per_sm": 1, "copy_engine": 2, "qgz": 3, "grad_dtype": 4, "qwz": 5, "max_ctas": 6,
        "bwd_ctas": 10, "rs_ctas": 11, "device_epoch": 13, "fault": 14,
-       "alias_secondary": 15}
+       "alias_secondary": 15, "copy_by_caller": 16}
 FAULT_SKIP_E1, FAULT_SKIP_E2 = 1, 2
 COPY = {"ldg": 0, "tma": 1}
 
@@ -81,6 +81,7 @@ def _load() -> ctypes.CDLL:
         "hpz_buffer": (c_int, [P, c_int, c_int, POINTER(c_void_p), POINTER(c_int64)]),
         "hpz_current_step": (c_int, [P, POINTER(c_int64)]),
         "hpz_resync_step": (c_int, [P]),
+        "hpz_secondary_copy": (c_int, [P, c_int, c_void_p]),
         "hpz_counters": (c_int, [P, POINTER(hpz_counters_t), c_int]),
         "hpz_last_error": (c_char_p, [P]),
         "hpz_set_order": (c_int, [P, c_int, c_int, c_int]),
@@ -230,6 +231,10 @@ def hpz_synth_master(ctx, layer: int, key: int, scale: float, stream=None):
 
 def hpz_fwd_gather(ctx, layer: int, full_out_ptr: int, stream=None):
     _check(ctx, "hpz_fwd_gather", LIB.hpz_fwd_gather(ctx, layer, c_void_p(full_out_ptr), _stream(stream)))
+
+
+def hpz_secondary_copy(ctx, layer: int, stream=None):
+    _check(ctx, "hpz_secondary_copy", LIB.hpz_secondary_copy(ctx, layer, _stream(stream)))
 
 
 def hpz_bwd_gather(ctx, layer: int, full_out_ptr: int, stream=None):

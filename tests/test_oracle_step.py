@@ -205,3 +205,47 @@ def test_sampled_trajectory_matches_full_sim():
     w, m, v, p = O.sampled_trajectory(0, 5000, 4, idx, 3, O.AdamHyper())
     assert np.array_equal(w, o.full_master(0)[idx])
     assert np.array_equal(p, o.full_primary(0)[idx])
+
+
+def test_realistic_racing_layers_closed_form():
+    """Alg. 1's enqueue order with prefetch depth d: the backward gathers
+    enqueued before their layer's secondary copy are exactly the last ceil(d/2) layers —
+    the forward->backward turnaround of Fig. 1 — and none without prefetch.
+    Derivation: bwd L_j (1-based) is module 2N+1-j, prefetched while module 2N+1-j-d runs;
+    its copy follows module j, so it races iff 2N+1-j-d <= j, i.e. j >= N - (d-1)/2."""
+    import math
+    for N in range(1, 8):
+        for d in range(0, 15):
+            k = min(N, math.ceil(d / 2))
+            assert O.realistic_racing_layers(N, d) == set(range(N - k, N)), (N, d)
+    # the program order itself: every gather is enqueued once, every copy after its forward
+    seq = O.prefetch_enqueue_order(4, 1)
+    assert sorted(x for x in seq if x[0] == "gather") == sorted(
+        [("gather", "fwd", i) for i in range(4)] + [("gather", "bwd", i) for i in range(4)])
+    assert seq.index(("gather", "fwd", 2)) < seq.index(("copy", 1)) < seq.index(("gather", "fwd", 3))
+    assert seq.index(("gather", "bwd", 3)) < seq.index(("copy", 3))        # the turnaround race
+
+
+@pytest.mark.parametrize("depth", [1, 3])
+def test_stock_realistic_closed_form(depth):
+    """Stock + realistic schedule: only the racing layers read stale data — poison at t=0
+    (every element NaN), W_{t-1} afterwards (mismatches = P * #{e: W_t[e] != W_{t-1}[e]});
+    every other layer reads its fresh copy (0 mismatches); fixed ordering reads nothing stale."""
+    P, Pp = 4, 2
+    numels = [3000, 2500, 4096, 77, 1234]
+    racing = O.realistic_racing_layers(len(numels), depth)
+    assert racing == ({4} if depth == 1 else {3, 4})
+    o = O.HpzOracle(numels, P, Pp, align=16, order="stock", stock_schedule="realistic", prefetch_depth=depth)
+    recs = o.run(3)
+    for t, rec in enumerate(recs):
+        for i, lay in enumerate(o.layouts):
+            if i not in racing:
+                assert rec.mismatches[i] == 0 and rec.nan_reads[i] == 0, (t, i)
+            elif t == 0:
+                assert rec.mismatches[i] == P * lay.numel == rec.nan_reads[i], (t, i)
+            else:
+                cur = O.param_bits(rec.W[i], "bf16")[:lay.numel]
+                prev = O.param_bits(recs[t - 1].W[i], "bf16")[:lay.numel]
+                assert rec.mismatches[i] == P * int(np.count_nonzero(cur != prev)) > 0, (t, i)
+    f = O.HpzOracle(numels, P, Pp, align=16, order="fixed", stock_schedule="realistic", prefetch_depth=depth)
+    assert all(sum(r.mismatches) == 0 for r in f.run(2))
