@@ -461,6 +461,11 @@ class HpzOracle:
     toy_identical_batches: bool = False
     half_seed: int = 1234
     prefetch_depth: int = 1              # "realistic" stock schedule (R12)
+    # test inputs other than the seeded generator (no arithmetic of the method): the full
+    # fp32 initial parameters of each layer, and a callable (t, rank, layer) -> the rank's
+    # full-length fp32 gradient of the layer at step t (e.g. what a real backward wrote)
+    init_params: list | None = None
+    grad_override: object = None
     qgz: bool = False                    # f1: INT4 quantized gradient all-to-all (qgz_reduce_scatter)
     grad_dtype: str = "f32"              # f4: "bf16" = gradients stored/communicated as bf16 (RNE)
     qwz: bool = False                    # f2: INT8 blockwise weights in the forward AllGather
@@ -483,6 +488,8 @@ class HpzOracle:
                 fan_in = d if i == 0 else h
                 w0[: lay.numel] = S.uniform(S.stream_key(S.SEED_PARAMS, i, 0, 0),
                                             np.arange(lay.numel), 2.0 ** -int(math.log2(fan_in) / 2 + 1))
+            elif self.init_params is not None:
+                w0 = pad_full(np.asarray(self.init_params[i], dtype=F32)[: lay.numel], lay)
             else:
                 w0 = S.layer_params(i, lay.numel, lay.numel_pad)
             ranks = []
@@ -508,6 +515,9 @@ class HpzOracle:
                 loss, gs = toy_loss_and_grads(f, b, x, y)
                 losses.append(loss)
                 G.append([pad_full(g.astype(F32), lay) for g, lay in zip(gs, self.layouts)])
+            elif self.grad_override is not None:
+                G.append([pad_full(np.asarray(self.grad_override(t, r, i), dtype=F32)[: lay.numel], lay)
+                          for i, lay in enumerate(self.layouts)])
             else:
                 G.append([S.layer_grads(i, t, r, lay.numel, lay.numel_pad, kind=self.grad_kind)
                           for i, lay in enumerate(self.layouts)])

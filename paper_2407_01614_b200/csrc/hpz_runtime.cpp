@@ -190,11 +190,15 @@ cudaError_t gather_launch(const hpz_ctx* c, const GatherParams& p, cudaStream_t 
   return launch_gather(p, grid_for(c, tiles, c->ctas_per_sm, cap > 0 ? cap * c->ctas_per_sm : 0), s);
 }
 
+#ifndef HPZ_RS_CTAS_PER_SM
+#define HPZ_RS_CTAS_PER_SM 1   // TMA reduce-scatter CTAs per SM (A/B builds; needs a smaller stage budget)
+#endif
 cudaError_t rs_launch(const hpz_ctx* c, const RSParams& r, const AdamParams* a, cudaStream_t s) {
+  const int per_sm = HPZ_RS_CTAS_PER_SM;
   if (c->qgz_bits || c->grad_bytes == 2)   // qgZ codes / bf16 gradients: TMA engine only
-    return launch_rs_tma(r, a, c->world, grid_for(c, (r.n_vec * 4 + 1023) / 1024, 1, c->rs_ctas), s, c->qgz_bits ? 2 : 1);
+    return launch_rs_tma(r, a, c->world, grid_for(c, (r.n_vec * 4 + 1023) / 1024, per_sm, c->rs_ctas), s, c->qgz_bits ? 2 : 1);
   if (c->copy_engine == HPZ_COPY_TMA)
-    return launch_rs_tma(r, a, c->world, grid_for(c, (r.n_vec * 4 + 1023) / 1024, 1, c->rs_ctas), s);
+    return launch_rs_tma(r, a, c->world, grid_for(c, (r.n_vec * 4 + 1023) / 1024, per_sm, c->rs_ctas), s);
   const int grid = grid_for(c, (r.n_vec + 511) / 512, c->ctas_per_sm, c->rs_ctas > 0 ? c->rs_ctas * c->ctas_per_sm : 0);
   return a ? launch_rs_adam(r, *a, c->world, grid, s) : launch_reduce_scatter(r, c->world, grid, s);
 }

@@ -37,6 +37,15 @@ constexpr int kRsChunk = 1024;          // base shard elements per RS stage
 #ifndef HPZ_RS_P1_MUL
 #define HPZ_RS_P1_MUL 1                 // P = 1 (local, HBM-bound) chunk multiplier (A/B builds)
 #endif
+#ifndef HPZ_RS_PN_MUL
+#define HPZ_RS_PN_MUL 2                 // 2 <= P <= 8 chunk multiplier (A/B builds)
+#endif
+#ifndef HPZ_RS_BUDGET_KB
+#define HPZ_RS_BUDGET_KB 200            // shared-memory stage budget per CTA (A/B builds)
+#endif
+#ifndef HPZ_RS_MAX_STAGES
+#define HPZ_RS_MAX_STAGES 6
+#endif
 constexpr int kRsMaxConsumers = 512;    // up to 16 consumer warps (one float4 each per chunk)
 
 // ------------------------------------------------------------------ PTX wrappers
@@ -248,34 +257,42 @@ __global__ void __launch_bounds__(32 * (1 + kFpWarps), 1)
 // ------------------------------------------------------------------ RS (+ Adam) (a5, a6)
 enum RsMode { RS_F32 = 0, RS_BF16 = 1, RS_QGZ = 2 };
 
-template <int P, bool ADAM, int MODE>
+template <int P, bool ADAM, int MODE, bool FP = false>
 struct RsCfg {
   static constexpr bool QGZ = MODE == RS_QGZ;
   // per stage: P gradient slices (fp32, or qgZ int4 codes + (min, scale) per 64) (+ w, m, v);
   // qgZ chunks are longer so its small code/param copies stay >= 1 KiB / 256 B
   // P=1 (local, HBM-bound): 1024-element chunks keep 6 stages in flight; 2 <= P <= 8: 2048
-  static constexpr int kChunk = (P >= 2 && P <= 8 ? 2 : (P == 1 ? HPZ_RS_P1_MUL : 1)) * (QGZ ? 2 * kRsChunk : kRsChunk);
+  static constexpr int kChunk = (P >= 2 && P <= 8 ? HPZ_RS_PN_MUL : (P == 1 ? HPZ_RS_P1_MUL : 1)) * (QGZ ? 2 * kRsChunk : kRsChunk);
   static constexpr int kGradBytes = MODE == RS_BF16 ? 2 : 4;
   static constexpr int kCodeBytes = kChunk / 2;
   static constexpr int kParamBytes = kChunk / kQgzBlock * 8;
   static constexpr int kSrcBytes = QGZ ? kCodeBytes + kParamBytes : kChunk * kGradBytes;
   static constexpr int kWmvOff = P * kSrcBytes;
-  static constexpr int kStageBytes = kWmvOff + (ADAM ? 3 * kChunk * 4 : 0);
-  static constexpr int kBudget = 200 * 1024;
-  static constexpr int kStages = kBudget / kStageBytes >= 6 ? 6 : kBudget / kStageBytes;
+  static constexpr int kPrimOff = kWmvOff + (ADAM ? 3 * kChunk * 4 : 0);
+  // FP: the new primaries of the chunk are staged in smem (fp32 size: the dtype is a runtime
+  // choice) for the fingerprint warp, which hashes them
+  static constexpr int kStageBytes = kPrimOff + (FP ? kChunk * 4 : 0);
+  static constexpr int kBudget = HPZ_RS_BUDGET_KB * 1024;
+  static constexpr int kStages = kBudget / kStageBytes >= HPZ_RS_MAX_STAGES ? HPZ_RS_MAX_STAGES : kBudget / kStageBytes;
   // consumer threads: one float4 per thread per chunk, at most 16 warps (idle polling
   // warps would steal issue slots from the working ones)
   static constexpr int kConsumers = kChunk / 4 < kRsMaxConsumers ? kChunk / 4 : kRsMaxConsumers;
   static constexpr int kLead = 32;   // producer warp
+  static constexpr int kThreads = kLead + kConsumers + (FP ? 32 : 0);   // (+ fingerprint warp, last)
 };
 
-// Block = 1 producer warp + consumer warps.  Dynamic smem = kStages * kStageBytes.
-// FP (with ADAM): the consumers also fingerprint the primary words they write (a7, E1/E2),
-// branch-free; a separate instantiation so the plain kernel keeps its code.
+// Block = 1 producer warp + consumer warps (+ FP: a fingerprint warp).  Dynamic smem =
+// kStages * kStageBytes.
+// FP (with ADAM): the owner-side fingerprint of the new primaries (a7, E1/E2).  Consumers
+// also copy each chunk's primaries into a smem staging area; the fingerprint warp hashes
+// them as whole 16-byte words (the words a forward gather will read), off the consumers'
+// critical path, and then frees the stage.  A separate instantiation, so the plain kernel
+// keeps its code.
 template <int P, bool ADAM, int MODE, bool FP>
-__global__ void __launch_bounds__(RsCfg<P, ADAM, MODE>::kLead + RsCfg<P, ADAM, MODE>::kConsumers, 1)
+__global__ void __launch_bounds__(RsCfg<P, ADAM, MODE, FP>::kThreads, 1)
     rs_tma_kernel(const __grid_constant__ RSParams r, const __grid_constant__ AdamParams a) {
-  using C = RsCfg<P, ADAM, MODE>;
+  using C = RsCfg<P, ADAM, MODE, FP>;
   static_assert(ADAM || !FP, "fingerprints are emitted by the optimizer");
   constexpr bool QGZ = C::QGZ;
   constexpr bool BF16 = MODE == RS_BF16;
@@ -283,7 +300,9 @@ __global__ void __launch_bounds__(RsCfg<P, ADAM, MODE>::kLead + RsCfg<P, ADAM, M
   extern __shared__ __align__(1024) char smem[];
   __shared__ __align__(8) uint64_t full_bar[C::kStages];
   __shared__ __align__(8) uint64_t empty_bar[C::kStages];
-  uint64_t fp = 0;                 // consumers (FP): fingerprint of the primary words written
+  __shared__ __align__(8) uint64_t prim_bar[FP ? C::kStages : 1];   // FP: a chunk's primaries staged
+  constexpr int kFpWarp = (C::kLead + C::kConsumers) / 32;
+  uint64_t fp = 0;                 // fingerprint warp: fingerprint of the primary words written
   const int64_t n = r.n_vec * 4;   // shard elements (multiple of 256)
   const int64_t total = (n + C::kChunk - 1) / C::kChunk;
   const int64_t nk = blockIdx.x < total ? (total - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
@@ -300,13 +319,31 @@ __global__ void __launch_bounds__(RsCfg<P, ADAM, MODE>::kLead + RsCfg<P, ADAM, M
     fence_proxy_async();
     for (int s = 0; s < C::kStages; ++s) {
       mbar_init(&full_bar[s], 1);
-      mbar_init(&empty_bar[s], C::kConsumers / 32);
+      mbar_init(&empty_bar[s], C::kConsumers / 32 + (FP ? 1 : 0));   // (+ the fingerprint warp)
+      if (FP) mbar_init(&prim_bar[s], C::kConsumers / 32);
     }
     fence_mbar_init();
   }
   __syncthreads();
 
-  if (warp == 0) {
+  if (FP && warp == kFpWarp) {
+    // fingerprint warp: per chunk, hash the staged primaries (16-byte words), then free
+    // the stage (its share of the empty barrier)
+    const int eb = a.prim_bf16 ? 2 : 4;
+    for (int64_t k = 0; k < nk; ++k) {
+      const int s = (int)(k % C::kStages);
+      mbar_wait(&prim_bar[s], (uint32_t)((k / C::kStages) & 1));
+      const int64_t e0 = (blockIdx.x + k * gridDim.x) * (int64_t)C::kChunk;
+      const int64_t rem = n - e0;
+      const int cnt = (int)(rem < C::kChunk ? rem : C::kChunk);
+      const int4* pw = reinterpret_cast<const int4*>(smem + (size_t)s * C::kStageBytes + C::kPrimOff);
+      const int nw = cnt * eb / 16;
+      const int64_t wb = a.fpe.word_base + e0 * eb / 16;
+      for (int v = lane; v < nw; v += 32) fp += fp_word((uint32_t)(wb + v), pw[v]);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty_bar[s]);
+    }
+  } else if (warp == 0) {
     if (lane == 0) {
       for (int64_t k = 0; k < nk; ++k) {
         const int s = (int)(k % C::kStages);
@@ -391,57 +428,34 @@ __global__ void __launch_bounds__(RsCfg<P, ADAM, MODE>::kLead + RsCfg<P, ADAM, M
           reinterpret_cast<float4*>(a.w)[i] = w;
           reinterpret_cast<float4*>(a.m)[i] = m;
           reinterpret_cast<float4*>(a.v)[i] = v;
+          char* stp = smem + (size_t)s * C::kStageBytes + C::kPrimOff;   // FP: staging area
           if (a.prim_bf16) {
             pk = pack_bf16x4(w);
             reinterpret_cast<uint2*>(a.prim)[i] = pk;
+            if constexpr (FP) reinterpret_cast<uint2*>(stp)[ct] = pk;
           } else {
             reinterpret_cast<float4*>(a.prim)[i] = w;
+            if constexpr (FP) reinterpret_cast<float4*>(stp)[ct] = w;
           }
         }
       };
-      // fingerprint of the primary word(s) of float4 ct, branch-free and warp-uniform (the
-      // bf16 word of float4s 2k, 2k+1 is completed with the neighbour lane's half)
-      auto fingerprint = [&](const int ct, const bool ok, const float4& w, const uint2& pk) {
-        const int64_t i = e0 / 4 + ct;
-        uint64_t h;
-        if (a.prim_bf16) {
-          const uint32_t ox = __shfl_xor_sync(0xffffffffu, pk.x, 1);
-          const uint32_t oy = __shfl_xor_sync(0xffffffffu, pk.y, 1);
-          h = fp_word((uint32_t)(a.fpe.word_base + (i >> 1)), make_int4((int)pk.x, (int)pk.y, (int)ox, (int)oy));
-          h = (ok && !(i & 1)) ? h : 0ull;
-        } else {
-          h = fp_word((uint32_t)(a.fpe.word_base + i), make_int4(__float_as_int(w.x), __float_as_int(w.y),
-                                                                 __float_as_int(w.z), __float_as_int(w.w)));
-          h = ok ? h : 0ull;
-        }
-        fp += h;
-      };
       // consumer thread ct handles float4 ct of the chunk (and ct + kConsumers, ... when the
       // chunk holds more float4s than there are consumers).  The single-pass form is a
-      // separate branch: compiled as a loop it measured ~13% slower.  The stage is released
-      // before the fingerprint work (registers only), which overlaps the next stage's wait.
-      constexpr int kIt = C::kChunk / (4 * C::kConsumers);
-      float4 w[kIt];
-      uint2 pk[kIt];
-      bool ok[kIt];
-      if constexpr (kIt == 1) {
+      // separate branch: compiled as a loop it measured ~13% slower.
+      float4 w;
+      uint2 pk;
+      if constexpr (C::kConsumers * 4 == C::kChunk) {
         const int ct = threadIdx.x - C::kLead;
-        ok[0] = ct * 4 < cnt;
-        if (ok[0]) process(ct, w[0], pk[0]);
+        if (ct * 4 < cnt) process(ct, w, pk);
       } else {
-#pragma unroll
-        for (int it = 0; it < kIt; ++it) {
-          const int ct = threadIdx.x - C::kLead + it * C::kConsumers;
-          ok[it] = ct * 4 < cnt;
-          if (ok[it]) process(ct, w[it], pk[it]);
-        }
+        for (int ct = threadIdx.x - C::kLead; ct * 4 < cnt; ct += C::kConsumers) process(ct, w, pk);
+      }
+      if constexpr (FP) {   // the chunk's primaries are staged (mbarrier arrive: release)
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&prim_bar[s]);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty_bar[s]);
-      if constexpr (FP) {
-#pragma unroll
-        for (int it = 0; it < kIt; ++it) fingerprint(threadIdx.x - C::kLead + it * C::kConsumers, ok[it], w[it], pk[it]);
-      }
     }
   }
   if constexpr (FP) emit_fp(fp, a.fpe, a.sync);
@@ -490,11 +504,11 @@ cudaError_t set_smem_attr(int smem) {
 
 template <int P, bool ADAM, int MODE, bool FP = false>
 cudaError_t launch_rs_tma_t(const RSParams& r, const AdamParams& a, int grid, cudaStream_t s) {
-  using C = RsCfg<P, ADAM, MODE>;
+  using C = RsCfg<P, ADAM, MODE, FP>;
   const int smem = C::kStages * C::kStageBytes;
   cudaError_t e = set_smem_attr<rs_tma_kernel<P, ADAM, MODE, FP>>(smem);
   if (e != cudaSuccess) return e;
-  return launch_pdl(rs_tma_kernel<P, ADAM, MODE, FP>, grid, C::kLead + C::kConsumers, smem, s, r, a);
+  return launch_pdl(rs_tma_kernel<P, ADAM, MODE, FP>, grid, C::kThreads, smem, s, r, a);
 }
 
 template <int P, int MODE>

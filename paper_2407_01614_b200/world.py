@@ -221,6 +221,7 @@ def save_checkpoint(rc: RankCtx, adam_steps_done: int) -> dict:
     shards of every layer (CPU tensors) + the Adam step count."""
     torch.cuda.synchronize()
     state = {"rank": rc.rank, "world": rc.world, "node_size": rc.node_size, "numels": list(rc.numels),
+             "shards": [int(x.shard) for x in rc.infos], "numel_pad": [int(x.numel_pad) for x in rc.infos],
              "adam_steps_done": int(adam_steps_done), "layers": []}
     for i in range(len(rc.numels)):
         state["layers"].append({k: buffer_view(rc, i, k, "f32").cpu().clone() for k in ("master", "m", "v")})
@@ -231,9 +232,17 @@ def load_checkpoint(rc: RankCtx, state: dict, stream=None):
     """Restore a save_checkpoint() state into a fresh context of the same layout/rank."""
     if state["rank"] != rc.rank or state["world"] != rc.world or list(state["numels"]) != list(rc.numels):
         raise ValueError("checkpoint was written for a different rank / world / model")
+    # the shard geometry (padding: align_elems) must match too — hpz_load_state copies
+    # `shard` fp32 elements per buffer from the given pointers
+    if list(state.get("shards", [])) != [int(x.shard) for x in rc.infos] or \
+            list(state.get("numel_pad", [])) != [int(x.numel_pad) for x in rc.infos]:
+        raise ValueError("checkpoint was written with a different shard layout (align_elems)")
     keep = []
     for i, L in enumerate(state["layers"]):
         ts = [L[k].contiguous().cuda() for k in ("master", "m", "v")]
+        for k, tk in zip(("master", "m", "v"), ts):
+            if tk.dtype != torch.float32 or tk.numel() != rc.infos[i].shard:
+                raise ValueError(f"checkpoint layer {i} {k}: expected {rc.infos[i].shard} fp32 elements")
         keep += ts
         H.hpz_load_state(rc.ctx, i, ts[0].data_ptr(), ts[1].data_ptr(), ts[2].data_ptr(),
                          state["adam_steps_done"], stream)

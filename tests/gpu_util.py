@@ -23,13 +23,25 @@ def oracle_prim_bits(x: np.ndarray, dtype: str) -> np.ndarray:
     return O.param_bits(x, dtype)
 
 
+def bits_equal(got: np.ndarray, want: np.ndarray, dtype: str) -> bool:
+    """Bitwise equality with NaNs compared by class, never by payload (reading R10: the GPU's
+    cvt / IEEE ops produce the canonical NaN, the oracle may keep an input's payload)."""
+    got, want = np.asarray(got), np.asarray(want)
+    if got.shape != want.shape:
+        return False
+    same = got == want
+    if same.all():
+        return True
+    return bool((same | (O.is_nan_bits(got, dtype) & O.is_nan_bits(want, dtype))).all())
+
+
 class ParityRun:
     """Drive an EmulatedWorld and an HpzOracle side by side on the same seeded inputs."""
 
     def __init__(self, numels, world, node_size, dtype="bf16", align=256, order="fixed",
                  verify="exact", grad_kind="uniform", n_grad_slots=None, stock_schedule="program",
                  fused=False, store_grad_shard=True, copy_engine="tma", qgz=False, grad_dtype="f32",
-                 qwz=False, load_initial=True):
+                 qwz=False, load_initial=True, init_params=None, grad_override=None):
         from paper_2407_01614_b200 import hpz as H
         from paper_2407_01614_b200.world import EmulatedWorld
         self.H = H
@@ -42,7 +54,8 @@ class ParityRun:
         self.o = O.HpzOracle(self.numels, world, node_size, align=align, param_dtype=dtype,
                              order="fixed" if order == "paper" else order,
                              stock_schedule=stock_schedule, grad_kind=grad_kind, qgz=qgz, grad_dtype=grad_dtype,
-                             qwz=qwz)
+                             qwz=qwz, init_params=init_params, grad_override=grad_override)
+        self.init_params, self.grad_override = init_params, grad_override
         self.stream = torch.cuda.current_stream()
         for rc in self.w.ranks:
             H.hpz_set_order(rc.ctx, order)
@@ -55,15 +68,23 @@ class ParityRun:
                     for rc in self.w.ranks]
         self.bwd = [[torch.zeros(rc.infos[i].numel_pad, dtype=tdt, device="cuda") for i in range(L)] for rc in self.w.ranks]
         for i, n in enumerate(self.numels if load_initial else []):
-            w0 = torch.from_numpy(S.layer_params(i, n)).cuda()
+            w0 = torch.from_numpy(np.ascontiguousarray(init_params[i][:n], dtype=np.float32) if init_params is not None
+                                  else S.layer_params(i, n)).cuda()
             for rc in self.w.ranks:
                 H.hpz_load_master(rc.ctx, i, w0.data_ptr(), self.stream)
         self.adam = H.make_adam()
         self.t = 0
 
+    def grads(self, i, t, r) -> np.ndarray:
+        """Rank r's full-length (padded) fp32 gradient of layer i at step t, as uploaded."""
+        lay = self.o.layouts[i]
+        if self.grad_override is not None:
+            return O.pad_full(np.asarray(self.grad_override(t, r, i), dtype=np.float32)[: lay.numel], lay)
+        return S.layer_grads(i, t, r, lay.numel, lay.numel_pad, kind=self.grad_kind)
+
     def grad_fn(self, rc, i):
         lay = self.o.layouts[i]
-        g = torch.from_numpy(S.layer_grads(i, self.t, rc.rank, lay.numel, kind=self.grad_kind)).cuda()
+        g = torch.from_numpy(np.ascontiguousarray(self.grads(i, self.t, rc.rank)[: lay.numel])).cuda()
         if self.grad_dtype == "bf16":
             g = g.to(torch.bfloat16)          # RNE, the same rounding as the oracle's bf16_rne
         self.H.hpz_grad_upload(rc.ctx, i, g.data_ptr(), lay.numel, self.stream)

@@ -14,7 +14,7 @@ import torch
 from oracle import hpz_oracle as O
 from synth import inputs as S
 
-from .gpu_util import ParityRun, bits_np, gpu_ok
+from .gpu_util import ParityRun, bits_equal, bits_np, gpu_ok
 
 pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not gpu_ok(), reason="needs a GPU")]
 
@@ -28,14 +28,14 @@ def _check_step(run: ParityRun, rec, check_all=True, check_secondary=True):
     for i, lay in enumerate(run.o.layouts):
         W = O.param_bits(rec.W[i], dtype)
         for r, rc in enumerate(run.w.ranks):
-            # a2: forward gather == W_t bitwise (incl. zero padding)
-            assert np.array_equal(bits_np(run.fwd[r][i], dtype), W), f"fwd layer {i} rank {r}"
+            # a2: forward gather == W_t bitwise (incl. zero padding; NaN by class, R10)
+            assert bits_equal(bits_np(run.fwd[r][i], dtype), W, dtype), f"fwd layer {i} rank {r}"
             # a4: backward gather == W_t bitwise
-            assert np.array_equal(bits_np(run.bwd[r][i], dtype), W), f"bwd layer {i} rank {r}"
+            assert bits_equal(bits_np(run.bwd[r][i], dtype), W, dtype), f"bwd layer {i} rank {r}"
         if not check_all:
             continue
         from paper_2407_01614_b200.world import buffer_view
-        grads = [S.layer_grads(i, run.t - 1, j, lay.numel, lay.numel_pad, kind=run.grad_kind) for j in range(P)]
+        grads = [run.grads(i, run.t - 1, j) for j in range(P)]
         if run.grad_dtype == "bf16":
             grads = [O.bf16_to_f32(O.bf16_rne(g)) for g in grads]
         for r, rc in enumerate(run.w.ranks):
@@ -46,20 +46,20 @@ def _check_step(run: ParityRun, rec, check_all=True, check_secondary=True):
             if run.o.order == "fixed" and check_secondary:   # (paper maps to fixed)
                 sec = bits_np(buffer_view(rc, i, "secondary", dtype), dtype)
                 want = st.prim if aliased else st.sec
-                assert np.array_equal(sec, O.param_bits(want, dtype)), f"secondary layer {i} rank {r}"
+                assert bits_equal(sec, O.param_bits(want, dtype), dtype), f"secondary layer {i} rank {r}"
             # a5 reduce-scatter bit-exact in the fixed order
             if run.store_grad_shard:
                 g_gpu = buffer_view(rc, i, "grad_shard", "f32").cpu().numpy()
                 g_ref = (O.qgz_reduce_scatter if run.qgz else O.reduce_scatter)(grads, lay, r)
-                assert np.array_equal(g_gpu.view(np.uint32), g_ref.view(np.uint32)), f"RS layer {i} rank {r}"
+                assert bits_equal(g_gpu.view(np.uint32), g_ref.view(np.uint32), "f32"), f"RS layer {i} rank {r}"
             # a6 Adam + bf16 refresh
             for kind, ref in (("master", st.master), ("m", st.m), ("v", st.v)):
                 got = buffer_view(rc, i, kind, "f32").cpu().numpy()
-                if not np.array_equal(got.view(np.uint32), ref.view(np.uint32)):
-                    rel = np.max(np.abs(got - ref) / np.maximum(np.abs(ref), 1e-30))
+                if not bits_equal(got.view(np.uint32), ref.view(np.uint32), "f32"):
+                    rel = np.nanmax(np.abs(got - ref) / np.maximum(np.abs(ref), 1e-30))
                     pytest.fail(f"{kind} layer {i} rank {r}: max rel err {rel:.3g}")
             prim = bits_np(buffer_view(rc, i, "primary", dtype), dtype)
-            assert np.array_equal(prim, O.param_bits(st.prim, dtype)), f"primary layer {i} rank {r}"
+            assert bits_equal(prim, O.param_bits(st.prim, dtype), dtype), f"primary layer {i} rank {r}"
 
 
 ENGINES = [("ldg", "exact"), ("tma", "fingerprint")]   # EXACT verification runs on the LDG kernel
@@ -710,3 +710,22 @@ def test_device_epoch_rejects_uncapturable_orders():
         assert e.value.code == H.HPZ_ESTATE
     finally:
         run.close()
+
+
+def test_checkpoint_rejects_a_different_shard_layout():
+    """A checkpoint written under another align_elems (another padding, so another shard
+    length) is rejected before any raw copy (hpz_load_state copies `shard` elements)."""
+    from paper_2407_01614_b200.world import load_checkpoint, save_checkpoint
+    a = ParityRun([100_003], 4, 2, fused=True, verify="none", align=256)
+    try:
+        a.step()
+        ck = save_checkpoint(a.w.ranks[1], 1)
+    finally:
+        a.close()
+    b = ParityRun([100_003], 4, 2, fused=True, verify="none", align=8, load_initial=False)
+    try:
+        assert b.w.ranks[1].infos[0].shard != ck["shards"][0]
+        with pytest.raises(ValueError):
+            load_checkpoint(b.w.ranks[1], ck, b.stream)
+    finally:
+        b.close()
