@@ -87,32 +87,36 @@ __device__ __forceinline__ bool last_cta(uint32_t* ctr) {
   return last;
 }
 
-// Order-independent 64-bit checksum contribution of one 16-byte word at global word
-// index gi (a7).  Not cryptographic: it detects stale/garbage words; EXACT mode counts
-// elements.
+// Fingerprint (a7): F(buffer) = sum over its 32-bit words x_q of x_q * M(q) mod 2^64, with
+// q the word's index in the full parameter buffer and M(q) = (q * 0x9E3779B1) | 1, an odd
+// position-dependent multiplier.  Additive, so CTAs, owners and gathers combine partial sums
+// in any order; one IMAD + one wide IMAD per word, so the optimizer can emit it in registers
+// almost for free.  It detects any single changed word exactly (an odd M(q) times a nonzero
+// 32-bit difference is never 0 mod 2^64); a multi-word change escapes only if the weighted
+// differences cancel mod 2^64 — a stale or garbage read does not do that by accident.  EXACT
+// mode counts elements.
+__device__ __forceinline__ uint64_t fp_u32(uint32_t q, uint32_t x) {
+  return (uint64_t)x * (uint64_t)((q * 0x9E3779B1u) | 1u);
+}
+// ... of one 16-byte word at 16-byte-word index gi (32-bit words 4gi .. 4gi+3)
 __device__ __forceinline__ uint64_t fp_word(uint32_t gi, const int4& w) {
-  uint32_t h = (uint32_t)w.x * 0x85EBCA6Bu ^ (uint32_t)w.y * 0xC2B2AE35u ^ (uint32_t)w.z * 0x27D4EB2Fu ^
-               (uint32_t)w.w * 0x165667B1u ^ gi * 0x9E3779B1u;
-  h ^= h >> 15;
-  h *= 0x2C1B3C6Du;
-  h ^= h >> 12;
-  uint32_t h2 = h * 0x297A2D39u;
-  h2 ^= h2 >> 16;
-  return ((uint64_t)h2 << 32) | h;
+  const uint32_t q = gi * 4u;
+  return fp_u32(q, (uint32_t)w.x) + fp_u32(q + 1u, (uint32_t)w.y) + fp_u32(q + 2u, (uint32_t)w.z) +
+         fp_u32(q + 3u, (uint32_t)w.w);
 }
 
 // Fingerprint contribution of the primary elements a thread of an Adam kernel just wrote:
-// float4 index i of the shard.  fp32 primary: the float4 is one 16-byte word.  bf16
-// primary: the 8-byte halves of word i/2 are held by lanes i and i^1 of one warp, which
-// must both call this (warp-uniform: `valid` false contributes nothing but still shuffles).
-__device__ __forceinline__ uint64_t prim_word_fp(bool bf16, bool valid, int64_t i, const float4& w, const uint2& pk,
+// float4 index i of the shard (bf16: the 8 bytes pk, 32-bit words 2i, 2i+1 of the shard;
+// fp32: the 16 bytes w, words 4i .. 4i+3).  word_base = the shard's first 16-byte word in
+// the full buffer.  Per thread, no cross-lane work.
+__device__ __forceinline__ uint64_t prim_word_fp(bool bf16, int64_t i, const float4& w, const uint2& pk,
                                                  int64_t word_base) {
-  if (!bf16) return valid ? fp_word((uint32_t)(word_base + i), *reinterpret_cast<const int4*>(&w)) : 0ull;
-  const uint32_t ox = __shfl_xor_sync(0xffffffffu, pk.x, 1);
-  const uint32_t oy = __shfl_xor_sync(0xffffffffu, pk.y, 1);
-  if (!valid || (i & 1)) return 0ull;
-  const int4 word = make_int4((int)pk.x, (int)pk.y, (int)ox, (int)oy);
-  return fp_word((uint32_t)(word_base + i / 2), word);
+  if (bf16) {
+    const uint32_t q = (uint32_t)(word_base * 4 + 2 * i);
+    return fp_u32(q, pk.x) + fp_u32(q + 1u, pk.y);
+  }
+  return fp_word((uint32_t)(word_base + i), make_int4(__float_as_int(w.x), __float_as_int(w.y),
+                                                       __float_as_int(w.z), __float_as_int(w.w)));
 }
 
 // Block-wide sum of per-thread fingerprints, added (thread 0) into every reader's slot of

@@ -255,7 +255,7 @@ __global__ void __launch_bounds__(kThreads) adam_kernel(const __grid_constant__ 
         reinterpret_cast<float4*>(p.v)[i] = v[u];
         pk = store_prim(p.prim, p.prim_bf16, i, w[u]);
       }
-      if (emit) fp += prim_word_fp(p.prim_bf16, ok, i, w[u], pk, p.fpe.word_base);
+      if (emit && ok) fp += prim_word_fp(p.prim_bf16, i, w[u], pk, p.fpe.word_base);
     }
   }
   if (emit) emit_fp(fp, p.fpe, p.sync);
@@ -320,7 +320,7 @@ __global__ void __launch_bounds__(kThreads) rs_adam_kernel(const __grid_constant
         reinterpret_cast<float4*>(a.v)[i] = v[u];
         pk = store_prim(a.prim, a.prim_bf16, i, w[u]);
       }
-      if (emit) fp += prim_word_fp(a.prim_bf16, ok, i, w[u], pk, a.fpe.word_base);
+      if (emit && ok) fp += prim_word_fp(a.prim_bf16, i, w[u], pk, a.fpe.word_base);
     }
   }
   if (emit) emit_fp(fp, a.fpe, a.sync);

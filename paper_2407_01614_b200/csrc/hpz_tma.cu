@@ -270,25 +270,23 @@ struct RsCfg {
   static constexpr int kSrcBytes = QGZ ? kCodeBytes + kParamBytes : kChunk * kGradBytes;
   static constexpr int kWmvOff = P * kSrcBytes;
   static constexpr int kPrimOff = kWmvOff + (ADAM ? 3 * kChunk * 4 : 0);
-  // FP: the new primaries of the chunk are staged in smem (fp32 size: the dtype is a runtime
-  // choice) for the fingerprint warp, which hashes them
-  static constexpr int kStageBytes = kPrimOff + (FP ? kChunk * 4 : 0);
+  static constexpr int kStageBytes = kPrimOff;
   static constexpr int kBudget = HPZ_RS_BUDGET_KB * 1024;
-  static constexpr int kStages = kBudget / kStageBytes >= HPZ_RS_MAX_STAGES ? HPZ_RS_MAX_STAGES : kBudget / kStageBytes;
+  static constexpr int kFit = kBudget / kStageBytes;
+  static constexpr int kStages = kFit >= HPZ_RS_MAX_STAGES ? HPZ_RS_MAX_STAGES : (kFit < 2 ? 2 : kFit);
   // consumer threads: one float4 per thread per chunk, at most 16 warps (idle polling
   // warps would steal issue slots from the working ones)
   static constexpr int kConsumers = kChunk / 4 < kRsMaxConsumers ? kChunk / 4 : kRsMaxConsumers;
   static constexpr int kLead = 32;   // producer warp
-  static constexpr int kThreads = kLead + kConsumers + (FP ? 32 : 0);   // (+ fingerprint warp, last)
+  static constexpr int kThreads = kLead + kConsumers;
 };
 
-// Block = 1 producer warp + consumer warps (+ FP: a fingerprint warp).  Dynamic smem =
-// kStages * kStageBytes.
-// FP (with ADAM): the owner-side fingerprint of the new primaries (a7, E1/E2).  Consumers
-// also copy each chunk's primaries into a smem staging area; the fingerprint warp hashes
-// them as whole 16-byte words (the words a forward gather will read), off the consumers'
-// critical path, and then frees the stage.  A separate instantiation, so the plain kernel
-// keeps its code.
+// Block = 1 producer warp + consumer warps.  Dynamic smem = kStages * kStageBytes.
+// FP (with ADAM): the consumers also fingerprint the primary words they write (a7, E1/E2;
+// a few integer ops per thread, prim_word_fp).  A separate instantiation, so the plain
+// kernel keeps its code.  (Measured: a dedicated fingerprint warp fed through smem was
+// slower — this kernel's time tracks the consumers' instruction stream, and a polling warp
+// steals their issue slots.)
 template <int P, bool ADAM, int MODE, bool FP>
 __global__ void __launch_bounds__(RsCfg<P, ADAM, MODE, FP>::kThreads, 1)
     rs_tma_kernel(const __grid_constant__ RSParams r, const __grid_constant__ AdamParams a) {
@@ -300,9 +298,7 @@ __global__ void __launch_bounds__(RsCfg<P, ADAM, MODE, FP>::kThreads, 1)
   extern __shared__ __align__(1024) char smem[];
   __shared__ __align__(8) uint64_t full_bar[C::kStages];
   __shared__ __align__(8) uint64_t empty_bar[C::kStages];
-  __shared__ __align__(8) uint64_t prim_bar[FP ? C::kStages : 1];   // FP: a chunk's primaries staged
-  constexpr int kFpWarp = (C::kLead + C::kConsumers) / 32;
-  uint64_t fp = 0;                 // fingerprint warp: fingerprint of the primary words written
+  uint64_t fp = 0;                 // FP consumers: fingerprint of the primary words written
   const int64_t n = r.n_vec * 4;   // shard elements (multiple of 256)
   const int64_t total = (n + C::kChunk - 1) / C::kChunk;
   const int64_t nk = blockIdx.x < total ? (total - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
@@ -319,31 +315,13 @@ __global__ void __launch_bounds__(RsCfg<P, ADAM, MODE, FP>::kThreads, 1)
     fence_proxy_async();
     for (int s = 0; s < C::kStages; ++s) {
       mbar_init(&full_bar[s], 1);
-      mbar_init(&empty_bar[s], C::kConsumers / 32 + (FP ? 1 : 0));   // (+ the fingerprint warp)
-      if (FP) mbar_init(&prim_bar[s], C::kConsumers / 32);
+      mbar_init(&empty_bar[s], C::kConsumers / 32);
     }
     fence_mbar_init();
   }
   __syncthreads();
 
-  if (FP && warp == kFpWarp) {
-    // fingerprint warp: per chunk, hash the staged primaries (16-byte words), then free
-    // the stage (its share of the empty barrier)
-    const int eb = a.prim_bf16 ? 2 : 4;
-    for (int64_t k = 0; k < nk; ++k) {
-      const int s = (int)(k % C::kStages);
-      mbar_wait(&prim_bar[s], (uint32_t)((k / C::kStages) & 1));
-      const int64_t e0 = (blockIdx.x + k * gridDim.x) * (int64_t)C::kChunk;
-      const int64_t rem = n - e0;
-      const int cnt = (int)(rem < C::kChunk ? rem : C::kChunk);
-      const int4* pw = reinterpret_cast<const int4*>(smem + (size_t)s * C::kStageBytes + C::kPrimOff);
-      const int nw = cnt * eb / 16;
-      const int64_t wb = a.fpe.word_base + e0 * eb / 16;
-      for (int v = lane; v < nw; v += 32) fp += fp_word((uint32_t)(wb + v), pw[v]);
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty_bar[s]);
-    }
-  } else if (warp == 0) {
+  if (warp == 0) {
     if (lane == 0) {
       for (int64_t k = 0; k < nk; ++k) {
         const int s = (int)(k % C::kStages);
@@ -428,15 +406,13 @@ __global__ void __launch_bounds__(RsCfg<P, ADAM, MODE, FP>::kThreads, 1)
           reinterpret_cast<float4*>(a.w)[i] = w;
           reinterpret_cast<float4*>(a.m)[i] = m;
           reinterpret_cast<float4*>(a.v)[i] = v;
-          char* stp = smem + (size_t)s * C::kStageBytes + C::kPrimOff;   // FP: staging area
           if (a.prim_bf16) {
             pk = pack_bf16x4(w);
             reinterpret_cast<uint2*>(a.prim)[i] = pk;
-            if constexpr (FP) reinterpret_cast<uint2*>(stp)[ct] = pk;
           } else {
             reinterpret_cast<float4*>(a.prim)[i] = w;
-            if constexpr (FP) reinterpret_cast<float4*>(stp)[ct] = w;
           }
+          if constexpr (FP) fp += prim_word_fp(a.prim_bf16, i, w, pk, a.fpe.word_base);
         }
       };
       // consumer thread ct handles float4 ct of the chunk (and ct + kConsumers, ... when the
@@ -449,10 +425,6 @@ __global__ void __launch_bounds__(RsCfg<P, ADAM, MODE, FP>::kThreads, 1)
         if (ct * 4 < cnt) process(ct, w, pk);
       } else {
         for (int ct = threadIdx.x - C::kLead; ct * 4 < cnt; ct += C::kConsumers) process(ct, w, pk);
-      }
-      if constexpr (FP) {   // the chunk's primaries are staged (mbarrier arrive: release)
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&prim_bar[s]);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty_bar[s]);
