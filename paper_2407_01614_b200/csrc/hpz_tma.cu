@@ -30,8 +30,11 @@ namespace hpz {
 
 namespace {
 
+#ifndef HPZ_GATHER_STAGES
+#define HPZ_GATHER_STAGES 4
+#endif
 constexpr int kGatherChunk = 32768;     // bytes per gather stage (a 4..64 KiB, 1..3 CTA/SM sweep
-constexpr int kGatherStages = 4;        // at N=1 and N=4 found no better geometry; profiles/README.md)
+constexpr int kGatherStages = HPZ_GATHER_STAGES;   // at N=1 and N=4 found no better geometry; profiles/README.md)
 constexpr int kFpWarps = 4;             // fingerprint consumer warps
 constexpr int kRsChunk = 1024;          // base shard elements per RS stage
 #ifndef HPZ_RS_P1_MUL

@@ -46,7 +46,8 @@ def main():
     numels = [int(x) for x in args.numels.split(",")]
     P, r = dist.get_world_size(), dist.get_rank()
     W = DistWorld(numels, args.node_size, timeout_s=20.0, qgz=bool(args.qgz), grad_dtype=args.grad_dtype,
-                  qwz=bool(args.qwz), n_grad_slots=args.grad_slots or None)
+                  qwz=bool(args.qwz), n_grad_slots=args.grad_slots or None,
+                  alias_secondary=args.order != "stock")     # the stock race needs a real secondary
     rc = W.ranks[0]
     s = torch.cuda.current_stream()
     H.hpz_set_order(rc.ctx, args.order, stock_delay_us=args.stock_delay_us, stock_poison=args.order == "stock")
@@ -87,8 +88,10 @@ def main():
             assert np.array_equal(got_b, W_t), f"rank {r} step {t} layer {i}: bwd gather"
             st = o.state[i][r]
             if args.order == "fixed":
+                # P' == P: the secondary is aliased to the primary, which holds W_{t+1}
+                want = st.prim if (args.node_size == P and not args.qwz) else st.sec
                 sec = buffer_view(rc, i, "secondary", "bf16").cpu().numpy().view(np.uint16)
-                assert np.array_equal(sec, O.param_bits(st.sec, "bf16")), f"rank {r} layer {i}: secondary"
+                assert np.array_equal(sec, O.param_bits(want, "bf16")), f"rank {r} layer {i}: secondary"
             g = buffer_view(rc, i, "grad_shard", "f32").cpu().numpy()
             rs = O.qgz_reduce_scatter if args.qgz else O.reduce_scatter
             Gs = [S.layer_grads(i, t, j, lay.numel, lay.numel_pad) for j in range(P)]
