@@ -33,7 +33,10 @@ namespace {
 #ifndef HPZ_GATHER_STAGES
 #define HPZ_GATHER_STAGES 4
 #endif
-constexpr int kGatherChunk = 32768;     // bytes per gather stage (a 4..64 KiB, 1..3 CTA/SM sweep
+#ifndef HPZ_GATHER_CHUNK
+#define HPZ_GATHER_CHUNK 32768
+#endif
+constexpr int kGatherChunk = HPZ_GATHER_CHUNK;   // bytes per gather stage (a 4..64 KiB, 1..3 CTA/SM sweep
 constexpr int kGatherStages = HPZ_GATHER_STAGES;   // at N=1 and N=4 found no better geometry; profiles/README.md)
 constexpr int kFpWarps = 4;             // fingerprint consumer warps
 constexpr int kRsChunk = 1024;          // base shard elements per RS stage
@@ -44,11 +47,15 @@ constexpr int kRsChunk = 1024;          // base shard elements per RS stage
 #define HPZ_RS_PN_MUL 2                 // 2 <= P <= 8 chunk multiplier (A/B builds)
 #endif
 #ifndef HPZ_RS_BUDGET_KB
-#define HPZ_RS_BUDGET_KB 200            // shared-memory stage budget per CTA (A/B builds)
+#define HPZ_RS_BUDGET_KB 224            // shared-memory stage budget per CTA: 4 stages at P = 4
+                                        // (0.820 vs 0.814 of 770 GB/s with 200 KiB, N=4 A/B)
 #endif
 #ifndef HPZ_RS_MAX_STAGES
 #define HPZ_RS_MAX_STAGES 6
 #endif
+#ifndef HPZ_RS_WMV_LDG
+#define HPZ_RS_WMV_LDG 0                // P >= 2: consumers load master/m/v with LDG (prefetched
+#endif                                  // one chunk ahead) so the smem ring holds only peer data
 constexpr int kRsMaxConsumers = 512;    // up to 16 consumer warps (one float4 each per chunk)
 
 // ------------------------------------------------------------------ PTX wrappers
@@ -272,7 +279,8 @@ struct RsCfg {
   static constexpr int kParamBytes = kChunk / kQgzBlock * 8;
   static constexpr int kSrcBytes = QGZ ? kCodeBytes + kParamBytes : kChunk * kGradBytes;
   static constexpr int kWmvOff = P * kSrcBytes;
-  static constexpr int kPrimOff = kWmvOff + (ADAM ? 3 * kChunk * 4 : 0);
+  static constexpr bool kWmvLdg = ADAM && HPZ_RS_WMV_LDG && P >= 2 && kChunk / 4 <= kRsMaxConsumers;
+  static constexpr int kPrimOff = kWmvOff + (ADAM && !kWmvLdg ? 3 * kChunk * 4 : 0);
   static constexpr int kStageBytes = kPrimOff;
   static constexpr int kBudget = HPZ_RS_BUDGET_KB * 1024;
   static constexpr int kFit = kBudget / kStageBytes;
@@ -335,7 +343,7 @@ __global__ void __launch_bounds__(RsCfg<P, ADAM, MODE, FP>::kThreads, 1)
         const uint32_t bytes = cnt * 4;
         char* st = smem + (size_t)s * C::kStageBytes;
         const uint32_t src_bytes = QGZ ? cnt / 2 + cnt / kQgzBlock * 8 : (BF16 ? cnt * 2 : bytes);
-        mbar_expect_tx(&full_bar[s], src_bytes * P + (ADAM ? 3 * bytes : 0));
+        mbar_expect_tx(&full_bar[s], src_bytes * P + (ADAM && !C::kWmvLdg ? 3 * bytes : 0));
 #pragma unroll
         for (int j = 0; j < P; ++j) {
           char* dst = st + j * C::kSrcBytes;
@@ -348,7 +356,7 @@ __global__ void __launch_bounds__(RsCfg<P, ADAM, MODE, FP>::kThreads, 1)
             tma_load(dst, r.src[j] + e0, bytes, &full_bar[s]);
           }
         }
-        if (ADAM) {
+        if (ADAM && !C::kWmvLdg) {
           float* wmv = reinterpret_cast<float*>(st + C::kWmvOff);
           tma_load(wmv + 0 * C::kChunk, a.w + e0, bytes, &full_bar[s]);
           tma_load(wmv + 1 * C::kChunk, a.m + e0, bytes, &full_bar[s]);
@@ -359,6 +367,20 @@ __global__ void __launch_bounds__(RsCfg<P, ADAM, MODE, FP>::kThreads, 1)
     }
   } else {
     const float2 sc = ADAM ? adam_scalars(a) : make_float2(0.f, 0.f);
+    // kWmvLdg: this thread's master/m/v float4s of the next chunk, loaded one chunk ahead
+    float4 nw = make_float4(0.f, 0.f, 0.f, 0.f), nm = nw, nv = nw;
+    auto load_wmv = [&](int64_t kk) {
+      const int64_t e0k = (blockIdx.x + kk * gridDim.x) * (int64_t)C::kChunk;
+      const int ct0 = threadIdx.x - C::kLead;
+      if (e0k + ct0 * 4 < n) {
+        const int64_t ii = e0k / 4 + ct0;
+        nw = __ldcs(reinterpret_cast<const float4*>(a.w) + ii);
+        nm = __ldcs(reinterpret_cast<const float4*>(a.m) + ii);
+        nv = __ldcs(reinterpret_cast<const float4*>(a.v) + ii);
+      }
+    };
+    static_assert(!C::kWmvLdg || C::kConsumers * 4 == C::kChunk, "LDG master/m/v: one float4 per consumer");
+    if constexpr (C::kWmvLdg) if (nk > 0) load_wmv(0);
     for (int64_t k = 0; k < nk; ++k) {
       const int s = (int)(k % C::kStages);
       mbar_wait(&full_bar[s], (uint32_t)((k / C::kStages) & 1));
@@ -367,6 +389,8 @@ __global__ void __launch_bounds__(RsCfg<P, ADAM, MODE, FP>::kThreads, 1)
       const int cnt = (int)(rem < C::kChunk ? rem : C::kChunk);
       const char* stc = smem + (size_t)s * C::kStageBytes;
       const float4* wmv = reinterpret_cast<const float4*>(stc + C::kWmvOff);
+      float4 cw = nw, cm = nm, cv = nv;   // kWmvLdg: this chunk's master/m/v
+      if constexpr (C::kWmvLdg) if (k + 1 < nk) load_wmv(k + 1);
       // one float4 `ct` of the chunk: fixed-order sum (R7) of the P slices, then Adam (R8);
       // w / pk: the new master and bf16 primary (for the fingerprint)
       auto process = [&](const int ct, float4& w, uint2& pk) {
@@ -399,9 +423,16 @@ __global__ void __launch_bounds__(RsCfg<P, ADAM, MODE, FP>::kThreads, 1)
         g.w = __fmul_rn(g.w, r.inv_p);
         if (r.out) reinterpret_cast<float4*>(r.out)[i] = g;
         if (ADAM) {
-          w = wmv[0 * (C::kChunk / 4) + ct];
-          float4 m = wmv[1 * (C::kChunk / 4) + ct];
-          float4 v = wmv[2 * (C::kChunk / 4) + ct];
+          float4 m, v;
+          if constexpr (C::kWmvLdg) {
+            w = cw;
+            m = cm;
+            v = cv;
+          } else {
+            w = wmv[0 * (C::kChunk / 4) + ct];
+            m = wmv[1 * (C::kChunk / 4) + ct];
+            v = wmv[2 * (C::kChunk / 4) + ct];
+          }
           adam1(w.x, m.x, v.x, g.x, a, sc);
           adam1(w.y, m.y, v.y, g.y, a, sc);
           adam1(w.z, m.z, v.z, g.z, a, sc);
