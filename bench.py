@@ -68,6 +68,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-nccl", action="store_true")
+    ap.add_argument("--no-p2p-ceiling", action="store_true")
     ap.add_argument("--oracle-numel", type=int, default=0,
                     help="elements of the oracle's sample (0: 2^25/P; tests use small samples)")
     return ap.parse_args()
@@ -620,6 +621,14 @@ def main():
     nccl = None
     if world > 1 and not args.no_nccl:
         nccl = nccl_baseline(infos, e, node_size, dev, tdt, args)
+    ceiling = None
+    if world > 1 and not args.no_p2p_ceiling:
+        torch.cuda.synchronize()
+        dist.barrier()
+        ceiling = p2p_ceiling(world, rank)
+        if ceiling:
+            for k in kernels.values():
+                k["nvlink_frac_of_measured_ceiling"] = round(k["nvlink_GBps"] / ceiling["pull_tma_GBps_per_gpu_avg"], 4)
 
     W.close()
     if rank == 0:
@@ -652,6 +661,7 @@ def main():
             "roofline": roofline, "kernels": kernels,
             "cpu_baseline": cpu,
             "nccl_baseline": nccl,
+            "p2p_ceiling": ceiling,
             "e2e": e2e,
             "gpu_launches": int(stats[5]),
             "clocks": clk,
@@ -660,6 +670,33 @@ def main():
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def p2p_ceiling(world, rank):
+    """The fabric's measured all-to-all pull ceiling: after the timed work,
+    rank 0 runs tools/p2p_probe (every GPU TMA-pulls 512 MiB from every peer at once, the
+    traffic pattern of these collectives) while the other ranks wait on the host (TCP store,
+    no GPU work).  Returns {per-GPU ingress GB/s} or None."""
+    import re
+    import torch.distributed as dist
+    store = dist.distributed_c10d._get_default_store()
+    res = None
+    if rank == 0:
+        exe = os.path.join(ROOT, "tools", "p2p_probe")
+        try:
+            out = subprocess.run([exe, str(world), "pull_tma", "512", "1", "32768"], capture_output=True, text=True,
+                                 timeout=120).stdout
+            m = re.search(r"per-GPU GB/s: min ([0-9.]+) avg ([0-9.]+)", out)
+            if m:
+                res = {"pull_tma_GBps_per_gpu_min": float(m.group(1)), "pull_tma_GBps_per_gpu_avg": float(m.group(2)),
+                       "how": f"tools/p2p_probe {world} pull_tma 512 1 32768: all {world} GPUs TMA-pull 512 MiB from "
+                              f"every peer concurrently (bulk copies through smem, 1 CTA/SM), per-GPU ingress"}
+        except (OSError, subprocess.TimeoutExpired):
+            res = None
+        store.set("hpz_p2p_probe_done", "1")
+    else:
+        store.wait(["hpz_p2p_probe_done"])
+    return res
 
 
 def nccl_baseline(infos, e, node_size, dev, tdt, args):
