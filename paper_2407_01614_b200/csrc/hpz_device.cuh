@@ -95,28 +95,44 @@ __device__ __forceinline__ bool last_cta(uint32_t* ctr) {
 // 32-bit difference is never 0 mod 2^64); a multi-word change escapes only if the weighted
 // differences cancel mod 2^64 — a stale or garbage read does not do that by accident.  EXACT
 // mode counts elements.
+constexpr uint32_t kFpMul = 0x9E3779B1u;
+// acc += x * (qm | 1) with qm = q * kFpMul, as ONE 32x32->64 multiply-add (mad.wide.u32)
+__device__ __forceinline__ void fp_mad(uint64_t& acc, uint32_t qm, uint32_t x) {
+  asm("mad.wide.u32 %0, %1, %2, %0;" : "+l"(acc) : "r"(x), "r"(qm | 1u));
+}
 __device__ __forceinline__ uint64_t fp_u32(uint32_t q, uint32_t x) {
-  return (uint64_t)x * (uint64_t)((q * 0x9E3779B1u) | 1u);
+  uint64_t acc = 0;
+  fp_mad(acc, q * kFpMul, x);
+  return acc;
 }
 // ... of one 16-byte word at 16-byte-word index gi (32-bit words 4gi .. 4gi+3)
 __device__ __forceinline__ uint64_t fp_word(uint32_t gi, const int4& w) {
-  const uint32_t q = gi * 4u;
-  return fp_u32(q, (uint32_t)w.x) + fp_u32(q + 1u, (uint32_t)w.y) + fp_u32(q + 2u, (uint32_t)w.z) +
-         fp_u32(q + 3u, (uint32_t)w.w);
+  const uint32_t qm = gi * (4u * kFpMul);
+  uint64_t acc = 0;
+  fp_mad(acc, qm, (uint32_t)w.x);
+  fp_mad(acc, qm + kFpMul, (uint32_t)w.y);
+  fp_mad(acc, qm + 2u * kFpMul, (uint32_t)w.z);
+  fp_mad(acc, qm + 3u * kFpMul, (uint32_t)w.w);
+  return acc;
 }
 
 // Fingerprint contribution of the primary elements a thread of an Adam kernel just wrote:
 // float4 index i of the shard (bf16: the 8 bytes pk, 32-bit words 2i, 2i+1 of the shard;
 // fp32: the 16 bytes w, words 4i .. 4i+3).  word_base = the shard's first 16-byte word in
 // the full buffer.  Per thread, no cross-lane work.
-__device__ __forceinline__ uint64_t prim_word_fp(bool bf16, int64_t i, const float4& w, const uint2& pk,
-                                                 int64_t word_base) {
+__device__ __forceinline__ void prim_word_fp(uint64_t& acc, bool bf16, int64_t i, const float4& w, const uint2& pk,
+                                             int64_t word_base) {
   if (bf16) {
-    const uint32_t q = (uint32_t)(word_base * 4 + 2 * i);
-    return fp_u32(q, pk.x) + fp_u32(q + 1u, pk.y);
+    const uint32_t qm = (uint32_t)(word_base * 4 + 2 * i) * kFpMul;
+    fp_mad(acc, qm, pk.x);
+    fp_mad(acc, qm + kFpMul, pk.y);
+  } else {
+    const uint32_t qm = (uint32_t)(word_base * 4 + 4 * i) * kFpMul;
+    fp_mad(acc, qm, __float_as_uint(w.x));
+    fp_mad(acc, qm + kFpMul, __float_as_uint(w.y));
+    fp_mad(acc, qm + 2u * kFpMul, __float_as_uint(w.z));
+    fp_mad(acc, qm + 3u * kFpMul, __float_as_uint(w.w));
   }
-  return fp_word((uint32_t)(word_base + i), make_int4(__float_as_int(w.x), __float_as_int(w.y),
-                                                       __float_as_int(w.z), __float_as_int(w.w)));
 }
 
 // Block-wide sum of per-thread fingerprints, added (thread 0) into every reader's slot of

@@ -218,7 +218,7 @@ __device__ __forceinline__ uint2 store_prim(void* prim, int bf16, int64_t i, con
 }
 
 // Grid-stride loops below run a warp-uniform trip count (per-lane predicate `ok`) so the
-// fingerprint shuffle of prim_word_fp always has the whole warp.
+// loop shape of the fingerprinting kernels is the same whatever the lane.
 __global__ void __launch_bounds__(kThreads) adam_kernel(const __grid_constant__ AdamParams p) {
   if (threadIdx.x == 0) wait_all(p.wait, p.sync);   // E2: peers finished reading my primary
   __syncthreads();
@@ -255,7 +255,7 @@ __global__ void __launch_bounds__(kThreads) adam_kernel(const __grid_constant__ 
         reinterpret_cast<float4*>(p.v)[i] = v[u];
         pk = store_prim(p.prim, p.prim_bf16, i, w[u]);
       }
-      if (emit && ok) fp += prim_word_fp(p.prim_bf16, i, w[u], pk, p.fpe.word_base);
+      if (emit && ok) prim_word_fp(fp, p.prim_bf16, i, w[u], pk, p.fpe.word_base);
     }
   }
   if (emit) emit_fp(fp, p.fpe, p.sync);
@@ -320,7 +320,7 @@ __global__ void __launch_bounds__(kThreads) rs_adam_kernel(const __grid_constant
         reinterpret_cast<float4*>(a.v)[i] = v[u];
         pk = store_prim(a.prim, a.prim_bf16, i, w[u]);
       }
-      if (emit && ok) fp += prim_word_fp(a.prim_bf16, i, w[u], pk, a.fpe.word_base);
+      if (emit && ok) prim_word_fp(fp, a.prim_bf16, i, w[u], pk, a.fpe.word_base);
     }
   }
   if (emit) emit_fp(fp, a.fpe, a.sync);

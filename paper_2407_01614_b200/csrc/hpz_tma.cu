@@ -446,7 +446,7 @@ __global__ void __launch_bounds__(RsCfg<P, ADAM, MODE, FP>::kThreads, 1)
           } else {
             reinterpret_cast<float4*>(a.prim)[i] = w;
           }
-          if constexpr (FP) fp += prim_word_fp(a.prim_bf16, i, w, pk, a.fpe.word_base);
+          if constexpr (FP) prim_word_fp(fp, a.prim_bf16, i, w, pk, a.fpe.word_base);
         }
       };
       // consumer thread ct handles float4 ct of the chunk (and ct + kConsumers, ... when the
