@@ -36,8 +36,15 @@ namespace {
 #ifndef HPZ_GATHER_CHUNK
 #define HPZ_GATHER_CHUNK 32768
 #endif
-constexpr int kGatherChunk = HPZ_GATHER_CHUNK;   // bytes per gather stage (a 4..64 KiB, 1..3 CTA/SM sweep
-constexpr int kGatherStages = HPZ_GATHER_STAGES;   // at N=1 and N=4 found no better geometry; profiles/README.md)
+// Gather stage geometry, two instantiations (both 128 KiB of smem): sources over NVLink
+// pull 32 KiB chunks through 4 stages; a single local source (P = 1, or P' = 1 backward) is
+// a device-local copy and streams 16 KiB chunks through 8 stages (measured at N = 1: fwd /
+// bwd gathers at 0.91 of the HBM copy peak vs 0.85-0.87 with 32 KiB; at N = 4 the 16 KiB
+// geometry loses 2-5% on NVLink pulls, 8 KiB loses 10-20% everywhere).
+constexpr int kGatherChunk = HPZ_GATHER_CHUNK;   // bytes per gather stage (remote sources)
+constexpr int kGatherStages = HPZ_GATHER_STAGES;
+constexpr int kGatherChunkLocal = 16384;
+constexpr int kGatherStagesLocal = 8;
 constexpr int kFpWarps = 4;             // fingerprint consumer warps
 constexpr int kRsChunk = 1024;          // base shard elements per RS stage
 #ifndef HPZ_RS_P1_MUL
@@ -151,7 +158,7 @@ __device__ __forceinline__ void fence_mbar_init() {
 // ------------------------------------------------------------------ gather (a2, a4)
 // Block = 1 producer warp (+ kFpWarps fingerprint warps when FP).  Dynamic smem =
 // kGatherStages * kGatherChunk bytes.
-template <bool FP>
+template <bool FP, int kGatherChunk, int kGatherStages>
 __global__ void __launch_bounds__(32 * (1 + kFpWarps), 1)
     gather_tma_kernel(const __grid_constant__ GatherParams p) {
   extern __shared__ __align__(1024) char smem[];
@@ -811,13 +818,21 @@ __global__ void __launch_bounds__(32 + kQwConsumers, 1) gather_qwz_kernel(const 
 
 }  // namespace
 
-cudaError_t launch_gather_tma(const GatherParams& p, int grid, cudaStream_t s) {
-  const int smem = kGatherStages * kGatherChunk;
+template <int CHUNK, int STAGES>
+cudaError_t launch_gather_tma_t(const GatherParams& p, int grid, cudaStream_t s) {
+  const int smem = STAGES * CHUNK;
   const bool fp = p.fp_acc != nullptr;
-  cudaError_t e = fp ? set_smem_attr<gather_tma_kernel<true>>(smem) : set_smem_attr<gather_tma_kernel<false>>(smem);
+  cudaError_t e = fp ? set_smem_attr<gather_tma_kernel<true, CHUNK, STAGES>>(smem)
+                     : set_smem_attr<gather_tma_kernel<false, CHUNK, STAGES>>(smem);
   if (e != cudaSuccess) return e;
-  return fp ? launch_pdl(gather_tma_kernel<true>, grid, 32 * (1 + kFpWarps), smem, s, p)
-            : launch_pdl(gather_tma_kernel<false>, grid, 32, smem, s, p);
+  return fp ? launch_pdl(gather_tma_kernel<true, CHUNK, STAGES>, grid, 32 * (1 + kFpWarps), smem, s, p)
+            : launch_pdl(gather_tma_kernel<false, CHUNK, STAGES>, grid, 32, smem, s, p);
+}
+
+cudaError_t launch_gather_tma(const GatherParams& p, int grid, cudaStream_t s) {
+  // one source = this rank's own arena (P = 1, or the P' = 1 backward): a local copy
+  return p.n_src == 1 ? launch_gather_tma_t<kGatherChunkLocal, kGatherStagesLocal>(p, grid, s)
+                      : launch_gather_tma_t<kGatherChunk, kGatherStages>(p, grid, s);
 }
 
 cudaError_t launch_qwz_quantize(const QwzQuantParams& q, int grid, cudaStream_t s) {
