@@ -61,12 +61,13 @@ def run(order, args, world, rank, local, node_size, numels):
     torch.cuda.synchronize()
     secs = time.time() - t0
     c = H.hpz_counters(ctx)
-    tot = sum_over_ranks([c["mismatches"], c["nan_reads"], c["fp_mismatches"], c["fp_checked"], c["timeouts"]],
-                         device=torch.device("cuda", local))
+    tot = sum_over_ranks([c["mismatches"], c["nan_reads"], c["fp_mismatches"], c["fp_checked"], c["timeouts"],
+                          c["fp_fwd_mismatches"], c["fp_fwd_checked"]], device=torch.device("cuda", local))
     W.close()
     return {"order": order, "steps": steps, "wall_s": round(secs, 1), "mismatched_elements": int(tot[0]),
             "nan_reads": int(tot[1]), "fingerprint_mismatched_layers": int(tot[2]),
-            "layer_gathers_checked": int(tot[3]), "timeouts": int(tot[4])}
+            "layer_gathers_checked": int(tot[3]), "timeouts": int(tot[4]),
+            "fwd_vs_owner_fingerprint_mismatched_layers": int(tot[5]), "fwd_layer_gathers_checked": int(tot[6])}
 
 
 def main():
@@ -99,7 +100,7 @@ def main():
                "options": {"qgz": args.qgz, "qwz": args.qwz, "grad_dtype": args.grad_dtype},
                "runs": res,
                "pass": res[0]["mismatched_elements"] == 0 and res[0]["fingerprint_mismatched_layers"] == 0
-               and res[0]["timeouts"] == 0
+               and res[0]["fwd_vs_owner_fingerprint_mismatched_layers"] == 0 and res[0]["timeouts"] == 0
                and (len(res) < 2 or res[1]["mismatched_elements"] > 0 or res[1]["fingerprint_mismatched_layers"] > 0)}
         print(json.dumps(out), flush=True)
     if world > 1:
