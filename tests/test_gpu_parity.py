@@ -729,3 +729,49 @@ def test_checkpoint_rejects_a_different_shard_layout():
             load_checkpoint(b.w.ranks[1], ck, b.stream)
     finally:
         b.close()
+
+
+# ---------------------------------------------------------------- ranks on concurrent streams
+@pytest.mark.parametrize("P,Pp,kw", [(4, 2, {}), (2, 2, {}), (8, 4, {"qgz": True}), (4, 1, {"grad_dtype": "bf16"}),
+                                     (4, 2, {"device_epoch": True})])
+def test_emulated_ranks_on_concurrent_streams(P, Pp, kw):
+    """Single-GPU emulation with one stream PER RANK: every rank issues its own step program
+    (forward gathers, backward gathers + gradient upload + fused RS+Adam) on its own stream, so
+    the ranks' kernels run concurrently and every cross-rank flag wait (E1-E7) is a real race
+    between kernels, not satisfied by stream order as in the one-stream emulation.  Grids are
+    capped (HPZ_OPT_MAX_CTAS) so all ranks' waiting kernels fit on the GPU at once.  3 steps,
+    bit-exact vs the oracle, all fingerprints checked."""
+    from paper_2407_01614_b200 import hpz as H
+    kw = dict(kw)
+    dev_epoch = kw.pop("device_epoch", False)
+    run = ParityRun(NUMELS, P, Pp, fused=True, verify="fingerprint", **kw)
+    try:
+        streams = [torch.cuda.Stream() for _ in range(P)]
+        for rc in run.w.ranks:
+            H.hpz_set_option(rc.ctx, "max_ctas", 144 // P)
+            if dev_epoch:
+                H.hpz_set_option(rc.ctx, "device_epoch", 1)
+        L = len(NUMELS)
+        for t in range(3):
+            grads = {(r, i): torch.from_numpy(np.ascontiguousarray(run.grads(i, t, r)[:run.o.layouts[i].numel])).cuda()
+                     for r in range(P) for i in range(L)}
+            if run.grad_dtype == "bf16":
+                grads = {k: v.to(torch.bfloat16) for k, v in grads.items()}
+            torch.cuda.synchronize()
+            for rc in run.w.ranks:            # each rank's whole step on its own stream
+                s = streams[rc.rank]
+                for i in range(L):
+                    H.hpz_fwd_gather(rc.ctx, i, run.fwd[rc.rank][i].data_ptr(), s)
+                for i in reversed(range(L)):
+                    H.hpz_bwd_gather(rc.ctx, i, run.bwd[rc.rank][i].data_ptr(), s)
+                    H.hpz_grad_upload(rc.ctx, i, grads[(rc.rank, i)].data_ptr(), run.o.layouts[i].numel, s)
+                    H.hpz_reduce_scatter_adam(rc.ctx, i, run.adam, s)
+            torch.cuda.synchronize()
+            rec = run.o.step()
+            run.t = t + 1
+            _check_step(run, rec)
+        c = run.counters()
+        assert c["timeouts"] == 0 and c["fp_mismatches"] == 0 and c["fp_fwd_mismatches"] == 0, c
+        assert c["fp_checked"] == 3 * L * P and c["fp_fwd_checked"] == 3 * L * P, c
+    finally:
+        run.close()
