@@ -66,7 +66,9 @@ typedef enum {
   HPZ_EINVAL = -1,    /* bad argument (SPEC invalid-argument)                       */
   HPZ_ESTATE = -2,    /* call out of lifecycle order (SPEC lifecycle/invalid-program) */
   HPZ_ECUDA = -3,     /* a CUDA runtime call failed; message names it              */
-  HPZ_ETIMEOUT = -4,  /* a device-side flag wait timed out (peer missing / deadlock) */
+  HPZ_ETIMEOUT = -4,  /* a device-side flag wait timed out (peer missing / deadlock); the
+                         message names the first flag that timed out (edge, layer or
+                         gradient slot, source rank, value seen vs needed) */
   HPZ_ENOMEM = -5     /* arena allocation failed                                    */
 } hpz_status;
 

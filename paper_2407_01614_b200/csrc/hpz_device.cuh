@@ -38,6 +38,9 @@ __device__ __forceinline__ bool wait_geq(const uint32_t* flag, uint32_t target, 
       if (*(volatile uint32_t*)s.abort_flag) return false;
       if (globaltimer() - t0 > s.timeout_ns) {
         atomicAdd(s.timeouts, 1ull);
+        if (s.timeout_info != nullptr &&
+            atomicCAS(s.timeout_info, 0ull, (unsigned long long)(uintptr_t)flag) == 0ull)   // first timeout: which edge
+          s.timeout_info[1] = ((unsigned long long)target << 32) | ld_acquire_sys(flag);
         atomicExch(s.abort_flag, 1u);
         *s.host_err = 1u;
         __threadfence_system();

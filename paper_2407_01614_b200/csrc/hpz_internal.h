@@ -24,6 +24,7 @@ struct SyncCommon {
   unsigned long long* timeouts;        // local arena counter
   volatile uint32_t* host_err;         // host-mapped pinned word polled by the runtime
   const uint32_t* epoch;               // device step counter (device-epoch mode) or nullptr
+  unsigned long long* timeout_info;    // [0] address of the first flag that timed out, [1] target<<32 | seen
 };
 
 // A list of flags to release (st.release.sys of value + mul * epoch), possibly in peer arenas.

@@ -125,6 +125,7 @@ struct hpz_ctx {
     s.timeouts = stat(4);
     s.host_err = host_err_dev;
     s.epoch = dev_epoch ? epoch_word() : nullptr;
+    s.timeout_info = stat(8);
     return s;
   }
   // Flag value for the absolute epoch x of a layer flag: absolute (host epochs) or relative
@@ -157,11 +158,46 @@ int fail(hpz_ctx* c, int code, const char* fmt, ...) {
     if (e_ != cudaSuccess) return fail(c, HPZ_ECUDA, "%s: %s", #call, cudaGetErrorString(e_)); \
   } while (0)
 
+// Which ordering edge a flag address belongs to (for the timeout message).
+std::string describe_flag(const hpz_ctx* c, uint64_t addr) {
+  static const char* kLayerKinds[] = {"PRIM_READY (E1)", "FWD_DONE (E2)", "SEC_READY (E3)", "BWD_DONE (E4)",
+                                      "BWDP_DONE (E7)"};
+  static const char* kSlotKinds[] = {"GRAD_READY (E5)", "RS_DONE (E6)"};
+  char buf[160];
+  for (int r = 0; r < c->world; ++r) {
+    const uint64_t base = reinterpret_cast<uint64_t>(c->arena[r] + c->off_flags);
+    const uint64_t n_layer = (uint64_t)F_NUM_LAYER_KINDS * c->n_layers * c->world;
+    const uint64_t n_all = n_layer + (uint64_t)S_NUM * c->n_slots * c->world;
+    if (addr < base || addr >= base + n_all * 4) continue;
+    uint64_t idx = (addr - base) / 4;
+    if (idx < n_layer) {
+      const uint64_t src = idx % c->world, layer = (idx / c->world) % c->n_layers, kind = idx / c->world / c->n_layers;
+      snprintf(buf, sizeof buf, "%s of layer %llu from rank %llu (flag in rank %d's arena)", kLayerKinds[kind],
+               (unsigned long long)layer, (unsigned long long)src, r);
+    } else {
+      idx -= n_layer;
+      const uint64_t src = idx % c->world, slot = (idx / c->world) % c->n_slots, kind = idx / c->world / c->n_slots;
+      snprintf(buf, sizeof buf, "%s of gradient slot %llu from rank %llu (flag in rank %d's arena)", kSlotKinds[kind],
+               (unsigned long long)slot, (unsigned long long)src, r);
+    }
+    return buf;
+  }
+  snprintf(buf, sizeof buf, "flag at %#llx", (unsigned long long)addr);
+  return buf;
+}
+
 int check_ready(hpz_ctx* c) {
   if (!c) return HPZ_EINVAL;
   if (!c->registered || !c->bound) return fail(c, HPZ_ESTATE, "context not registered/bound");
-  if (c->host_err && *(volatile uint32_t*)c->host_err)
+  if (c->host_err && *(volatile uint32_t*)c->host_err) {
+    unsigned long long info[2] = {0, 0};
+    cudaMemcpy(info, c->stat(8), sizeof info, cudaMemcpyDeviceToHost);   // the waits have returned
+    cudaGetLastError();
+    if (info[0])
+      return fail(c, HPZ_ETIMEOUT, "a device-side flag wait timed out: %s stayed at %u, needed >= %u",
+                  describe_flag(c, info[0]).c_str(), (unsigned)(info[1] & 0xffffffffu), (unsigned)(info[1] >> 32));
     return fail(c, HPZ_ETIMEOUT, "a device-side flag wait timed out (a peer never released)");
+  }
   return HPZ_OK;
 }
 
@@ -388,7 +424,7 @@ int hpz_register_flat_params(hpz_ctx* c, int n_layers, const int64_t* numel, int
   c->off_fp = off;
   off = align_up(off + (uint64_t)n_layers * 4 * 8, 256);
   c->off_stats = off;
-  off = align_up(off + 8 * 8, 256);
+  off = align_up(off + 16 * 8, 256);
   c->off_fpx = off;
   off = align_up(off + (uint64_t)n_layers * 2 * 8, 256);
   c->off_epoch = off;

@@ -339,6 +339,8 @@ def test_missing_peer_times_out_instead_of_hanging():
         with pytest.raises(H.HpzError) as e:
             H.hpz_grad_buffer(r0, 0, s)
         assert e.value.code == H.HPZ_ETIMEOUT
+        # the error names the edge that never arrived (first timed-out flag, decoded)
+        assert "SEC_READY (E3) of layer 0 from rank 1" in str(e.value), str(e.value)
     finally:
         w.close()
 
@@ -735,12 +737,16 @@ def test_checkpoint_rejects_a_different_shard_layout():
 @pytest.mark.parametrize("P,Pp,kw", [(4, 2, {}), (2, 2, {}), (8, 4, {"qgz": True}), (4, 1, {"grad_dtype": "bf16"}),
                                      (4, 2, {"device_epoch": True})])
 def test_emulated_ranks_on_concurrent_streams(P, Pp, kw):
-    """Single-GPU emulation with one stream PER RANK: every rank issues its own step program
-    (forward gathers, backward gathers + gradient upload + fused RS+Adam) on its own stream, so
-    the ranks' kernels run concurrently and every cross-rank flag wait (E1-E7) is a real race
-    between kernels, not satisfied by stream order as in the one-stream emulation.  Grids are
-    capped (HPZ_OPT_MAX_CTAS) so all ranks' waiting kernels fit on the GPU at once.  3 steps,
-    bit-exact vs the oracle, all fingerprints checked."""
+    """Single-GPU emulation with one stream PER RANK: each rank's calls go to its own stream,
+    so the ranks' kernels run concurrently and every cross-rank flag wait (E1-E7) is a real
+    race between running kernels, not satisfied by stream order as in the one-stream
+    emulation.  Two rules keep mutually-waiting kernels on one GPU deadlock-free (a
+    multi-process world with one GPU per rank needs neither): calls are submitted in SPMD
+    phase order across ranks (every kernel is submitted after the kernels whose flags it
+    waits for — the driver may serialize several streams in one hardware queue, measured: a
+    rank-by-rank submission deadlocked on E3 with 36-CTA grids), and grids are capped so all
+    ranks' waiting kernels fit on the GPU at once.  3 steps, bit-exact vs the oracle, all
+    fingerprints checked."""
     from paper_2407_01614_b200 import hpz as H
     kw = dict(kw)
     dev_epoch = kw.pop("device_epoch", False)
@@ -752,20 +758,25 @@ def test_emulated_ranks_on_concurrent_streams(P, Pp, kw):
             if dev_epoch:
                 H.hpz_set_option(rc.ctx, "device_epoch", 1)
         L = len(NUMELS)
+        ranks = run.w.ranks
         for t in range(3):
             grads = {(r, i): torch.from_numpy(np.ascontiguousarray(run.grads(i, t, r)[:run.o.layouts[i].numel])).cuda()
                      for r in range(P) for i in range(L)}
             if run.grad_dtype == "bf16":
                 grads = {k: v.to(torch.bfloat16) for k, v in grads.items()}
             torch.cuda.synchronize()
-            for rc in run.w.ranks:            # each rank's whole step on its own stream
-                s = streams[rc.rank]
-                for i in range(L):
-                    H.hpz_fwd_gather(rc.ctx, i, run.fwd[rc.rank][i].data_ptr(), s)
-                for i in reversed(range(L)):
-                    H.hpz_bwd_gather(rc.ctx, i, run.bwd[rc.rank][i].data_ptr(), s)
-                    H.hpz_grad_upload(rc.ctx, i, grads[(rc.rank, i)].data_ptr(), run.o.layouts[i].numel, s)
-                    H.hpz_reduce_scatter_adam(rc.ctx, i, run.adam, s)
+            for i in range(L):
+                for rc in ranks:
+                    H.hpz_fwd_gather(rc.ctx, i, run.fwd[rc.rank][i].data_ptr(), streams[rc.rank])
+            for i in reversed(range(L)):
+                for rc in ranks:
+                    H.hpz_bwd_gather(rc.ctx, i, run.bwd[rc.rank][i].data_ptr(), streams[rc.rank])
+                for rc in ranks:
+                    H.hpz_grad_upload(rc.ctx, i, grads[(rc.rank, i)].data_ptr(), run.o.layouts[i].numel,
+                                      streams[rc.rank])
+                    H.hpz_grads_ready(rc.ctx, i, streams[rc.rank])
+                for rc in ranks:
+                    H.hpz_reduce_scatter_adam(rc.ctx, i, run.adam, streams[rc.rank])
             torch.cuda.synchronize()
             rec = run.o.step()
             run.t = t + 1
