@@ -558,6 +558,8 @@ def main():
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if bound == "hbm" else
                 "B200_PROFILING.md measured peer copy 770 GB/s per direction (900 nominal)",
                 "alg_bytes_per_step": alg, "launches_per_step": L, "ms_per_step": round(share[dom], 4),
+                "timing": f"CUDA events around every call of the {KB} instrumented steps run right after the "
+                          f"timed region (same config, eager issue), on the stream the kernels run on",
                 "share_of_step": round(share[dom] / max(fwd_ms + bwd_ms + rs_ms + adam_ms + q_ms + g_ms, 1e-9), 4)}
 
     # per-kernel table (north_star: per-step gather / reduce-scatter time, NVLink GB/s

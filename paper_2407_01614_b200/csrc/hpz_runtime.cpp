@@ -219,7 +219,7 @@ int grid_for(const hpz_ctx* c, int64_t work_items, int per_sm, int cap = 0) {
 // verification, or when selected with HPZ_OPT_COPY_ENGINE).
 cudaError_t gather_launch(const hpz_ctx* c, const GatherParams& p, cudaStream_t s, int cap = 0) {
   if (c->copy_engine == HPZ_COPY_TMA && p.mism == nullptr) {
-    const int64_t cb = p.n_src == 1 ? 16384 : 32768;   // launch_gather_tma's chunk for this case
+    const int64_t cb = p.n_src == 1 ? 16384 : 32768;   // launch_gather_tma's chunk for this case (grid sizing only)
     const int64_t chunks = (p.src_bytes + cb - 1) / cb * p.n_src;
     return launch_gather_tma(p, grid_for(c, chunks, 1, cap), s);
   }

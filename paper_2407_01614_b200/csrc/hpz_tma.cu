@@ -43,8 +43,14 @@ namespace {
 // geometry loses 2-5% on NVLink pulls, 8 KiB loses 10-20% everywhere).
 constexpr int kGatherChunk = HPZ_GATHER_CHUNK;   // bytes per gather stage (remote sources)
 constexpr int kGatherStages = HPZ_GATHER_STAGES;
-constexpr int kGatherChunkLocal = 16384;
-constexpr int kGatherStagesLocal = 8;
+#ifndef HPZ_GATHER_LOCAL_CHUNK
+#define HPZ_GATHER_LOCAL_CHUNK 16384
+#endif
+#ifndef HPZ_GATHER_LOCAL_STAGES
+#define HPZ_GATHER_LOCAL_STAGES 8
+#endif
+constexpr int kGatherChunkLocal = HPZ_GATHER_LOCAL_CHUNK;
+constexpr int kGatherStagesLocal = HPZ_GATHER_LOCAL_STAGES;
 constexpr int kFpWarps = 4;             // fingerprint consumer warps
 constexpr int kRsChunk = 1024;          // base shard elements per RS stage
 #ifndef HPZ_RS_P1_MUL
