@@ -1282,6 +1282,8 @@ int hpz_set_option(hpz_ctx* c, int option, int64_t value) {
     case HPZ_OPT_DEVICE_EPOCH: {
       if (value != 0 && value != 1) return fail(c, HPZ_EINVAL, "device_epoch must be 0 or 1");
       if (!c->bound) return fail(c, HPZ_ESTATE, "device epochs need a bound arena");
+      if (c->dev_epoch && value == 0)   // back to host epochs: take over the device's step count first
+        if (int rc = hpz_resync_step(c)) return rc;
       // between steps, device idle: the device counter starts at the host's step
       HPZ_CUDA(c, cudaSetDevice(c->device));
       HPZ_CUDA(c, cudaDeviceSynchronize());
