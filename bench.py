@@ -65,6 +65,9 @@ def parse():
     ap.add_argument("--graph", type=int, default=1,
                     help="1: device-side epochs, one whole step captured in a CUDA graph and replayed each timed "
                          "step (fixed/off orders); 0: every call issued eagerly")
+    ap.add_argument("--graph-events", type=int, default=1,
+                    help="graph mode: 1 = per-call timing events inside the captured (timed) graph; 0 = a plain "
+                         "graph, per-call times from eager steps after the timed region")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-nccl", action="store_true")
@@ -155,6 +158,35 @@ def host_mem_available():
     except OSError:
         pass
     return 8 << 30
+
+
+class ExtEvent:
+    """A timing event recorded as an EXTERNAL event-record node when the stream is being
+    captured (cuEventRecordWithFlags(..., CU_EVENT_RECORD_EXTERNAL)): its timestamp is taken
+    every time the graph replays, so per-call device times can be read from inside a
+    CUDA-graph replay.  Same elapsed_time() interface as torch.cuda.Event."""
+    _lib = None
+
+    def __init__(self):
+        import ctypes
+        if ExtEvent._lib is None:
+            ExtEvent._lib = ctypes.CDLL("libcuda.so.1")
+        self._ct = ctypes
+        self.h = ctypes.c_void_p()
+        self._check(ExtEvent._lib.cuEventCreate(ctypes.byref(self.h), 0), "cuEventCreate")
+
+    def _check(self, rc, what):
+        if rc != 0:
+            raise RuntimeError(f"{what} failed: CUresult {rc}")
+
+    def record(self, stream):
+        self._check(ExtEvent._lib.cuEventRecordWithFlags(self.h, self._ct.c_void_p(stream.cuda_stream), 1),
+                    "cuEventRecordWithFlags")
+
+    def elapsed_time(self, other):
+        ms = self._ct.c_float()
+        self._check(ExtEvent._lib.cuEventElapsedTime(self._ct.byref(ms), self.h, other.h), "cuEventElapsedTime")
+        return ms.value
 
 
 # ----------------------------------------------------------------------------- oracle legs
@@ -372,7 +404,7 @@ def main():
         waiting only for its own layer's upload."""
         def rec(k, st=None, layer=None):
             if ev is not None:
-                x = torch.cuda.Event(enable_timing=True)
+                x = ExtEvent() if torch.cuda.is_current_stream_capturing() else torch.cuda.Event(enable_timing=True)
                 x.record(stream if st is None else st)
                 ev[k].append(x)
                 if k.endswith("0"):
@@ -431,17 +463,24 @@ def main():
 
     for _ in range(args.warmup):
         one_step()
+    K = args.steps
     graph = None
+    evs = {k: [] for k in ("fwd0", "fwd1", "bwd0", "bwd1", "rs0", "rs1", "adam0", "adam1", "q0", "q1", "g0", "g1")}
+    evs.update({"_layer_" + k: [] for k in ("fwd", "bwd", "rs", "adam", "q", "g")})
     if use_graph:
-        # capture ONE whole step (every layer's gathers and fused RS+Adam); each replay is
-        # a new step: flag epochs and Adam scalars come from the device step counter
+        # capture the K timed steps (every layer's gathers and fused RS+Adam, K times) as ONE
+        # CUDA graph with an external timing event around every call: each step reads its
+        # flag epochs and Adam scalars from the device step counter, and the per-call device
+        # times come from inside the timed replay itself
         torch.cuda.synchronize()
         l0 = H.hpz_counters(ctx)["launches"]
         graph = torch.cuda.CUDAGraph()
+        t_ref = ExtEvent()
         with torch.cuda.graph(graph, stream=stream):
-            one_step()
+            t_ref.record(stream)
+            for _ in range(K):
+                one_step(evs if args.graph_events else None)
         graph_launches = H.hpz_counters(ctx)["launches"] - l0
-        graph.replay()            # one more warm-up step (the captured one)
         torch.cuda.synchronize()
     H.hpz_counters(ctx, reset=True)
     launches0 = H.hpz_counters(ctx)["launches"]
@@ -449,36 +488,35 @@ def main():
     barrier()
     if rank == 0:
         clocks.start()
-    # timed region: K whole steps bracketed by two events only (per-call events between the
-    # kernels would break programmatic dependent launch and inflate the step)
+    # timed region: K whole steps bracketed by two events (graph mode: one replay of the K-step
+    # graph; eager mode: K steps without per-call events)
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
     t_start.record(stream)
-    for _ in range(args.steps):
-        if graph is not None:
-            graph.replay()
-        else:
+    if graph is not None:
+        graph.replay()
+    else:
+        for _ in range(args.steps):
             one_step()
     t_end.record(stream)
     barrier()
     clk = clocks.stop() if rank == 0 else None
     barrier()        # rank 0 spent ~0.25 s stopping the sampler: realign before the breakdown steps
     cnt = H.hpz_counters(ctx)
-    K = args.steps
-    launches = graph_launches * K if graph is not None else cnt["launches"] - launches0
+    launches = graph_launches if graph is not None else cnt["launches"] - launches0
     if graph is not None:
         H.hpz_resync_step(ctx)    # host bookkeeping = the device step counter, for the eager steps below
     step_ms = t_start.elapsed_time(t_end) / K
-    # per-kernel breakdown: extra instrumented steps (events around every call), after the
-    # timed region; used for the breakdown and the roofline's per-kernel durations
-    KB = max(1, min(K, 5))
-    evs = {k: [] for k in ("fwd0", "fwd1", "bwd0", "bwd1", "rs0", "rs1", "adam0", "adam1", "q0", "q1", "g0", "g1")}
-    evs.update({"_layer_" + k: [] for k in ("fwd", "bwd", "rs", "adam", "q", "g")})
-    t_ref = torch.cuda.Event(enable_timing=True)
-    t_ref.record(stream)
-    for _ in range(KB):
-        one_step(evs)
-    barrier()
+    if graph is not None and args.graph_events:
+        KB = K                    # per-call times of the timed steps themselves
+    else:
+        # eager mode: extra instrumented steps (events around every call) after the timed region
+        KB = max(1, min(K, 5))
+        t_ref = torch.cuda.Event(enable_timing=True)
+        t_ref.record(stream)
+        for _ in range(KB):
+            one_step(evs)
+        barrier()
     if args.trace:
         # JSONL op trace of the instrumented steps (one line per call; SURVEY §5 tracing)
         names = {"fwd": "hpz_fwd_gather", "bwd": "hpz_bwd_gather", "rs": "hpz_reduce_scatter" + ("_adam" if fused else ""),
@@ -558,8 +596,11 @@ def main():
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if bound == "hbm" else
                 "B200_PROFILING.md measured peer copy 770 GB/s per direction (900 nominal)",
                 "alg_bytes_per_step": alg, "launches_per_step": L, "ms_per_step": round(share[dom], 4),
-                "timing": f"CUDA events around every call of the {KB} instrumented steps run right after the "
-                          f"timed region (same config, eager issue), on the stream the kernels run on",
+                "timing": (f"external CUDA events around every call inside the captured graph, read from the timed "
+                           f"replay itself ({KB} steps), on the stream the kernels run on"
+                           if graph is not None and args.graph_events else
+                           f"CUDA events around every call of {KB} instrumented steps run right after the timed "
+                           f"region (same config, eager issue), on the stream the kernels run on"),
                 "share_of_step": round(share[dom] / max(fwd_ms + bwd_ms + rs_ms + adam_ms + q_ms + g_ms, 1e-9), 4)}
 
     # per-kernel table (north_star: per-step gather / reduce-scatter time, NVLink GB/s
