@@ -66,6 +66,9 @@ constexpr int kRsChunk = 1024;          // base shard elements per RS stage
 #ifndef HPZ_RS_MAX_STAGES
 #define HPZ_RS_MAX_STAGES 6
 #endif
+#ifndef HPZ_RS_ROTATE
+#define HPZ_RS_ROTATE 0                 // A/B: rotate the order of the P slice loads per CTA and chunk
+#endif
 #ifndef HPZ_RS_WMV_LDG
 #define HPZ_RS_WMV_LDG 0                // P >= 2: consumers load master/m/v with LDG (prefetched
 #endif                                  // one chunk ahead) so the smem ring holds only peer data
@@ -358,7 +361,9 @@ __global__ void __launch_bounds__(RsCfg<P, ADAM, MODE, FP>::kThreads, 1)
         const uint32_t src_bytes = QGZ ? cnt / 2 + cnt / kQgzBlock * 8 : (BF16 ? cnt * 2 : bytes);
         mbar_expect_tx(&full_bar[s], src_bytes * P + (ADAM && !C::kWmvLdg ? 3 * bytes : 0));
 #pragma unroll
-        for (int j = 0; j < P; ++j) {
+        for (int jj = 0; jj < P; ++jj) {
+          // HPZ_RS_ROTATE: each CTA starts its chunk's loads at a different source rank
+          const int j = HPZ_RS_ROTATE ? (int)((jj + blockIdx.x + k) % P) : jj;
           char* dst = st + j * C::kSrcBytes;
           if (QGZ) {
             tma_load(dst, r.qcodes[j] + e0 / 2, cnt / 2, &full_bar[s]);
