@@ -36,8 +36,9 @@
  *     library's flags order every cross-GPU hazard, and the caller's streams order
  *     the library against its own compute.
  *   - Ownership: the library allocates exactly one device arena per context
- *     (hpz_arena_alloc) or borrows a caller-provided one (hpz_bind); full_out
- *     buffers always belong to the caller.
+ *     (hpz_arena_alloc) or borrows a caller-provided one (hpz_bind), plus — with
+ *     HPZ_OPT_DEVICE_EPOCH only — a small table of Adam scalars; full_out buffers
+ *     always belong to the caller.
  */
 #ifndef HPZ_H
 #define HPZ_H
