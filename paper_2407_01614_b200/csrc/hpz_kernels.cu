@@ -222,7 +222,7 @@ __device__ __forceinline__ uint2 store_prim(void* prim, int bf16, int64_t i, con
 __global__ void __launch_bounds__(kThreads) adam_kernel(const __grid_constant__ AdamParams p) {
   if (threadIdx.x == 0) wait_all(p.wait, p.sync);   // E2: peers finished reading my primary
   __syncthreads();
-  const float2 sc = adam_scalars(p);
+  const float4 sc = adam_scalars(p);
   const bool emit = p.fpe.n_dst > 0;
   uint64_t fp = 0;
   const int64_t stride = (int64_t)gridDim.x * kThreads * kAdamUnroll;
@@ -279,7 +279,7 @@ __global__ void __launch_bounds__(kThreads) rs_adam_kernel(const __grid_constant
     wait_all(a.wait, a.sync);                // E2 (+E7): nobody still reads my primary
   }
   __syncthreads();
-  const float2 sc = adam_scalars(a);
+  const float4 sc = adam_scalars(a);
   const bool emit = a.fpe.n_dst > 0;
   uint64_t fp = 0;
   const int64_t stride = (int64_t)gridDim.x * kThreads * U;
