@@ -183,6 +183,13 @@ class ExtEvent:
         self._check(ExtEvent._lib.cuEventRecordWithFlags(self.h, self._ct.c_void_p(stream.cuda_stream), 1),
                     "cuEventRecordWithFlags")
 
+    def __del__(self):
+        try:
+            if ExtEvent._lib is not None and self.h:
+                ExtEvent._lib.cuEventDestroy_v2(self.h)
+        except Exception:          # noqa: BLE001  (interpreter shutdown)
+            pass
+
     def elapsed_time(self, other):
         ms = self._ct.c_float()
         self._check(ExtEvent._lib.cuEventElapsedTime(self._ct.byref(ms), self.h, other.h), "cuEventElapsedTime")
