@@ -66,6 +66,10 @@ constexpr int kRsChunk = 1024;          // base shard elements per RS stage
 #ifndef HPZ_RS_MAX_STAGES
 #define HPZ_RS_MAX_STAGES 6
 #endif
+#ifndef HPZ_GATHER_ROTATE
+#define HPZ_GATHER_ROTATE 0             // 1: rotate each gather CTA through the sources (chunk_of);
+                                        // measured slower (local copies -23%, N=4 bwd -1%), kept off
+#endif
 #ifndef HPZ_RS_ROTATE
 #define HPZ_RS_ROTATE 1                 // rotate the order of the P slice loads per CTA and chunk
                                         // (N=4 RS+Adam 0.817 vs 0.799-0.811 of 770 GB/s; N=2 equal)
@@ -179,7 +183,14 @@ __global__ void __launch_bounds__(32 * (1 + kFpWarps), 1)
   const int n_src = p.n_src;
   const int64_t chunks_per_src = (p.src_bytes + kGatherChunk - 1) / kGatherChunk;
   const int64_t total = chunks_per_src * n_src;
-  const int64_t nk = blockIdx.x < total ? (total - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  // HPZ_GATHER_ROTATE: round k hands CTA b item k*G + (b + k) % G (a permutation inside each
+  // round of G items), so every CTA rotates through the sources instead of pinning one
+  // (G % n_src == 0 would give CTA b source b % n_src for good: the CTAs of the local source
+  // finish early and the NVLink pulls run on the rest of the SMs).
+  const int64_t G = gridDim.x;
+  const int64_t nk = HPZ_GATHER_ROTATE
+      ? total / G + (((int64_t)blockIdx.x + total / G) % G < total % G ? 1 : 0)
+      : (blockIdx.x < total ? (total - blockIdx.x + G - 1) / G : 0);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
@@ -192,7 +203,7 @@ __global__ void __launch_bounds__(32 * (1 + kFpWarps), 1)
   __syncthreads();
 
   auto chunk_of = [&](int64_t k, int& j, int64_t& off, uint32_t& bytes) {
-    const int64_t w = blockIdx.x + k * gridDim.x;
+    const int64_t w = HPZ_GATHER_ROTATE ? k * G + ((int64_t)blockIdx.x + k) % G : blockIdx.x + k * G;
     j = (int)(w % n_src);
     off = (w / n_src) * kGatherChunk;
     const int64_t rem = p.src_bytes - off;
@@ -721,7 +732,10 @@ __global__ void __launch_bounds__(32 + kQwConsumers, 1) gather_qwz_kernel(const 
   const int64_t n_el = p.src_bytes;                     // codes: 1 byte per element
   const int64_t chunks_per_src = (n_el + kQwChunk - 1) / kQwChunk;
   const int64_t total = chunks_per_src * n_src;
-  const int64_t nk = blockIdx.x < total ? (total - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  const int64_t G = gridDim.x;   // HPZ_GATHER_ROTATE schedule: see gather_tma_kernel
+  const int64_t nk = HPZ_GATHER_ROTATE
+      ? total / G + (((int64_t)blockIdx.x + total / G) % G < total % G ? 1 : 0)
+      : (blockIdx.x < total ? (total - blockIdx.x + G - 1) / G : 0);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int eb = p.elem_bytes;
   if (threadIdx.x == 0) {
@@ -733,7 +747,7 @@ __global__ void __launch_bounds__(32 + kQwConsumers, 1) gather_qwz_kernel(const 
   }
   __syncthreads();
   auto chunk_of = [&](int64_t k, int& j, int64_t& off, uint32_t& cnt) {
-    const int64_t w = blockIdx.x + k * gridDim.x;
+    const int64_t w = HPZ_GATHER_ROTATE ? k * G + ((int64_t)blockIdx.x + k) % G : blockIdx.x + k * G;
     j = (int)(w % n_src);
     off = (w / n_src) * kQwChunk;
     const int64_t rem = n_el - off;
