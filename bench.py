@@ -72,6 +72,10 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-nccl", action="store_true")
     ap.add_argument("--no-p2p-ceiling", action="store_true")
+    ap.add_argument("--share-gpus", action="store_true",
+                    help="FUNCTIONAL CHECK ONLY, not a measurement: rank r runs on GPU r %% device_count "
+                         "(several time-sliced processes per GPU, gloo control plane, no NCCL baseline / "
+                         "p2p ceiling), so the N-rank path runs on a box with fewer than N GPUs")
     ap.add_argument("--oracle-numel", type=int, default=0,
                     help="elements of the oracle's sample (0: 2^25/P; tests use small samples)")
     return ap.parse_args()
@@ -301,7 +305,9 @@ def relaunch(n):
 
 def make_config(args, world, node_size, n_layers, n_params, n_slots):
     """The workload this line measures (identical for both arms)."""
-    return {"workload": f"{args.model}-shaped flat parameter buffers ({n_layers} layers, "
+    extra = {"share_gpus": "FUNCTIONAL CHECK: ranks time-slice shared GPUs; the timings are not "
+                           "measurements"} if getattr(args, "share_gpus", False) else {}
+    return {**extra, "workload": f"{args.model}-shaped flat parameter buffers ({n_layers} layers, "
                         f"{n_params} params), bf16 params + fp32 master/Adam",
             "world": world, "node_size": node_size, "virtual_nodes": world // node_size,
             "parallelism": f"hpZ dp{world} (P={world}, P'={node_size})", "order": args.order,
@@ -347,10 +353,16 @@ def main():
     from paper_2407_01614_b200.world import DistWorld, EmulatedWorld, max_over_ranks, sum_over_ranks
     from synth import inputs as S
 
+    if args.share_gpus:
+        local_rank %= torch.cuda.device_count()
+        args.no_nccl = args.no_p2p_ceiling = True
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.share_gpus:
+            dist.init_process_group("gloo")      # NCCL refuses two ranks on one device
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     numels = shapes.numels(args.model)
     dtype = shapes.PARAM_DTYPE.get(args.model, "bf16")
     e = 2 if dtype == "bf16" else 4

@@ -56,12 +56,18 @@ def exchange_handles(handle: bytes, group=None) -> list[bytes]:
     return [bytes(h) for h in handles]
 
 
+def _reduce_device(device):
+    """Where a host-scalar reduction runs: the given device on NCCL, the host on gloo."""
+    import torch.distributed as dist
+    return "cpu" if dist.get_backend() == "gloo" else device
+
+
 def max_over_ranks(values: list[float], device=None) -> list[float]:
     """Element-wise max over all ranks (timing rule: max over ranks); identity without a PG."""
     import torch.distributed as dist
     if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
         return list(values)
-    t = torch.tensor(values, dtype=torch.float64, device=device)
+    t = torch.tensor(values, dtype=torch.float64, device=_reduce_device(device))
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return t.tolist()
 
@@ -70,7 +76,7 @@ def sum_over_ranks(values: list[float], device=None) -> list[float]:
     import torch.distributed as dist
     if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
         return list(values)
-    t = torch.tensor(values, dtype=torch.float64, device=device)
+    t = torch.tensor(values, dtype=torch.float64, device=_reduce_device(device))
     dist.all_reduce(t, op=dist.ReduceOp.SUM)
     return t.tolist()
 

@@ -36,10 +36,19 @@ def main():
     ap.add_argument("--grad-dtype", default="f32")
     ap.add_argument("--qwz", type=int, default=0)
     ap.add_argument("--grad-slots", type=int, default=0)
+    ap.add_argument("--share-gpus", type=int, default=0,
+                    help="1: rank r runs on GPU r %% device_count (several processes per GPU, time-sliced; "
+                         "gloo control plane, since NCCL refuses two ranks on one device)")
     args = ap.parse_args()
     local = int(os.environ["LOCAL_RANK"])
-    torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if args.share_gpus:
+        local %= torch.cuda.device_count()
+        torch.cuda.set_device(local)
+        dist.init_process_group("gloo")
+    else:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    red_dev = "cpu" if args.share_gpus else "cuda"
     from paper_2407_01614_b200 import hpz as H
     from paper_2407_01614_b200.world import DistWorld, buffer_view, run_step
 
@@ -107,7 +116,7 @@ def main():
         keep.clear()
     c = H.hpz_counters(rc.ctx)
     tot = torch.tensor([c["mismatches"], c["nan_reads"], c["timeouts"], c["fp_mismatches"]],
-                       dtype=torch.int64, device="cuda")
+                       dtype=torch.int64, device=red_dev)
     dist.all_reduce(tot)
     tot = tot.tolist()
     if r == 0:
