@@ -606,12 +606,21 @@ def main():
         "not captured: ncu replays a kernel ~40 times, which a kernel waiting on peer GPUs' flags cannot "
         "survive (single-GPU captures only); see the N=1 capture and profiles/README.md")
     tr = ncu_traffic().get(f"P{world}_{dom}")
+    if tr and tr.get("node_size", node_size) != node_size:
+        tr = None                                       # captured on another (P, P')
+    nvl_rx = None
     if tr and not (args.qgz or args.qwz or args.grad_dtype != "f32"):
-        # DRAM bytes of ONE captured launch (ncu --set full) next to that launch's algorithmic bytes
+        # DRAM bytes of ONE captured launch (ncu) next to that launch's algorithmic bytes
         traffic, traffic_alg, traffic_src = tr["dram_bytes_per_launch"], tr["launch_alg_bytes"], tr["source"]
+        if "nvlink_rx_bytes_per_launch" in tr:          # N > 1: the same capture's NVLink ingress
+            nvl_rx = {"nvlink_rx_bytes_per_launch": tr["nvlink_rx_bytes_per_launch"],
+                      "nvlink_alg_ingress_bytes": tr["nvlink_alg_ingress_bytes"],
+                      "rx_over_alg": round(tr["nvlink_rx_bytes_per_launch"] / tr["nvlink_alg_ingress_bytes"], 4),
+                      "traffic_is": tr["alg_bytes_are"]}
     roofline = {"bound": bound, "kernel": dom, "achieved": round(achieved, 1), "peak": peak, "unit": unit,
                 "frac": round(achieved / peak, 4), "traffic": traffic,
                 "traffic_launch_alg_bytes": traffic_alg, "traffic_source": traffic_src,
+                **({"traffic_nvlink": nvl_rx} if nvl_rx else {}),
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if bound == "hbm" else
                 "B200_PROFILING.md measured peer copy 770 GB/s per direction (900 nominal)",
                 "alg_bytes_per_step": alg, "launches_per_step": L, "ms_per_step": round(share[dom], 4),

@@ -44,6 +44,8 @@ def main():
     ap.add_argument("--node-size", type=int, default=1)
     ap.add_argument("--steps", type=int, default=2)
     ap.add_argument("--model", default="falcon7b_block")
+    ap.add_argument("--verify", default="fingerprint", choices=["none", "fingerprint"],
+                    help="the bench's default is fingerprint")
     args = ap.parse_args()
     import torch
     from paper_2407_01614_b200 import hpz as H
@@ -60,7 +62,8 @@ def main():
         ctx = H.hpz_init(P, Pp, r, r)
         H.hpz_register_flat_params(ctx, numels)
         H.hpz_arena_alloc(ctx)
-        H.hpz_set_verify(ctx, "none")
+        H.hpz_set_verify(ctx, args.verify)
+        H.hpz_set_option(ctx, "store_grad_shard", 0)   # the bench's fused RS+Adam stores no gradient shard
         ctxs.append(ctx)
     ptrs = [H.hpz_arena_ptr(c, r) for r, c in enumerate(ctxs)]
     for r, c in enumerate(ctxs):
@@ -91,11 +94,17 @@ def main():
         torch.cuda.synchronize(r)
     cnt = [H.hpz_counters(c) for c in ctxs]
     e = 2
+    # this GPU's own DRAM bytes per launch (its peers idle under ncu): own shard / secondary
+    # read, full buffer (+ secondary) written; RS+Adam: own gradient slice read, master/m/v
+    # read + written, bf16 primary written
+    hbm = {"fwd_gather": [x.shard * e + x.numel_pad * e + (x.sec_shard * e if Pp < P else 0) for x in infos],
+           "bwd_gather": [x.sec_shard * e + x.numel_pad * e for x in infos],
+           "reduce_scatter+adam": [x.shard * (4 + 12 + 12 + e) for x in infos]}
     alg = {"fwd_gather": [x.numel_pad * e * (P - 1) // P for x in infos],
            "bwd_gather": [x.numel_pad * e * (Pp - 1) // Pp for x in infos],
            "reduce_scatter+adam": [x.numel_pad * 4 * (P - 1) // P for x in infos]}
     print(json.dumps({"world": P, "node_size": Pp, "model": args.model, "numel_pad": [x.numel_pad for x in infos],
-                      "nvlink_ingress_alg_bytes_per_launch": alg,
+                      "nvlink_ingress_alg_bytes_per_launch": alg, "local_hbm_alg_bytes_per_launch": hbm,
                       "timeouts": sum(x["timeouts"] for x in cnt)}), flush=True)
     for c in ctxs:
         H.hpz_finalize(c)
