@@ -603,8 +603,9 @@ def main():
     achieved = alg / (share[dom] * 1e-3) / 1e9          # per-launch bytes / per-launch time, summed over L launches
     traffic = traffic_alg = None
     traffic_src = None if world == 1 else (
-        "not captured: ncu replays a kernel ~40 times, which a kernel waiting on peer GPUs' flags cannot "
-        "survive (single-GPU captures only); see the N=1 capture and profiles/README.md")
+        f"not captured for world {world} (P'={node_size}): the capture drives all P GPUs from one process under "
+        f"ncu (tools/nvlink_bytes.py; ncu must not wrap the multi-rank bench) and exists for N = 2, 4 "
+        f"(profiles/ncu_traffic.json)")
     tr = ncu_traffic().get(f"P{world}_{dom}")
     if tr and tr.get("node_size", node_size) != node_size:
         tr = None                                       # captured on another (P, P')
