@@ -5,6 +5,7 @@ oracle computed one element at a time (oracle.sampled_trajectory).
 
     python tests/full_size_worker.py                      # N=1 (P=1)
     torchrun --nproc-per-node N tests/full_size_worker.py # P=N, P'=N/2
+    HPZ_SHARE_GPUS=1 HPZ_FULL_MODEL=falcon7b_block torchrun --nproc-per-node 8 ...  # 8 ranks, any #GPUs
 Prints FULL_SIZE_OK on success (rank 0)."""
 import os
 import sys
@@ -28,9 +29,15 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    share = os.environ.get("HPZ_SHARE_GPUS") == "1"   # rank r on GPU r % #GPUs (time-sliced processes)
+    if share:
+        local %= torch.cuda.device_count()
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if share:
+            dist.init_process_group("gloo")             # NCCL refuses two ranks on one device
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     node = world // 2 if world >= 2 else 1
     numels = shapes.numels(model)
     L = len(numels)
@@ -48,7 +55,7 @@ def main():
     fwd = torch.empty(nmax, dtype=torch.bfloat16, device="cuda")
     bwd = torch.empty(nmax, dtype=torch.bfloat16, device="cuda")
     adam = H.make_adam()
-    check_layers = sorted({0, 1, L - 1})
+    check_layers = sorted({i for i in (0, 1, L - 1) if i < L})
     rng = np.random.default_rng(11)
     samples = {i: np.unique(np.concatenate([rng.integers(0, numels[i], 3000),
                                             [0, numels[i] - 1, rc.infos[i].numel_pad - 1]]))

@@ -26,3 +26,14 @@ def test_full_size_falcon7b_multiproc():
            "--master-addr", "127.0.0.1", "--master-port=30111", os.path.join(ROOT, "tests", "full_size_worker.py")]
     res = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
     assert res.returncode == 0 and "FULL_SIZE_OK" in res.stdout, res.stdout[-2000:] + res.stderr[-2000:]
+
+
+def test_full_size_block_eight_processes_sharing_gpus():
+    """One full-size Falcon-7B decoder block (207M elements: every CTA wraps its ring many
+    times) at the north_star's 2x4 topology, 8 separate processes on min(8, #GPUs) devices
+    (a 1-GPU box included), sampled elements vs the oracle, in the bench's configuration."""
+    env = dict(os.environ, HPZ_SHARE_GPUS="1", HPZ_FULL_MODEL="falcon7b_block")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=8",
+           "--master-addr", "127.0.0.1", "--master-port=30131", os.path.join(ROOT, "tests", "full_size_worker.py")]
+    res = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
+    assert res.returncode == 0 and "FULL_SIZE_OK" in res.stdout, res.stdout[-2000:] + res.stderr[-2000:]
