@@ -80,23 +80,33 @@ def main():
     ap.add_argument("--qwz", action="store_true")
     ap.add_argument("--grad-dtype", default="f32")
     ap.add_argument("--verify", default="exact", choices=["exact", "fingerprint"])
+    ap.add_argument("--node-size", type=int, default=0, help="P' (default N/2)")
+    ap.add_argument("--share-gpus", action="store_true",
+                    help="rank r on GPU r %% #GPUs (e.g. the 8-rank topologies on a 4-GPU box; gloo control plane)")
     args = ap.parse_args()
     import torch
     import torch.distributed as dist
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.share_gpus:
+        local %= torch.cuda.device_count()
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    node_size = world // 2 if world >= 2 else 1
+        if args.share_gpus:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    node_size = args.node_size or (world // 2 if world >= 2 else 1)
     from paper_2407_01614_b200 import shapes
     numels = shapes.numels(args.model)
     res = [run("fixed", args, world, rank, local, node_size, numels)]
     if args.stock_steps > 0:
         res.append(run("stock", args, world, rank, local, node_size, numels))
     if rank == 0:
-        out = {"config": f"C5 stress: {args.model} ({len(numels)} x {numels[0]} elements), P={world}, P'={node_size}",
+        out = {"config": f"C5 stress: {args.model} ({len(numels)} x {numels[0]} elements), P={world}, P'={node_size}"
+                         + (f", {world} processes sharing {torch.cuda.device_count()} GPU(s) (time-sliced)"
+                            if args.share_gpus else ""),
                "options": {"qgz": args.qgz, "qwz": args.qwz, "grad_dtype": args.grad_dtype},
                "runs": res,
                "pass": res[0]["mismatched_elements"] == 0 and res[0]["fingerprint_mismatched_layers"] == 0
