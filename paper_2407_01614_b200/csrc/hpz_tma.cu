@@ -31,16 +31,18 @@ namespace hpz {
 namespace {
 
 #ifndef HPZ_GATHER_STAGES
-#define HPZ_GATHER_STAGES 4
+#define HPZ_GATHER_STAGES 3
 #endif
 #ifndef HPZ_GATHER_CHUNK
 #define HPZ_GATHER_CHUNK 32768
 #endif
-// Gather stage geometry, two instantiations (both 128 KiB of smem): sources over NVLink
-// pull 32 KiB chunks through 4 stages; a single local source (P = 1, or P' = 1 backward) is
-// a device-local copy and streams 16 KiB chunks through 8 stages (measured at N = 1: fwd /
-// bwd gathers at 0.91 of the HBM copy peak vs 0.85-0.87 with 32 KiB; at N = 4 the 16 KiB
-// geometry loses 2-5% on NVLink pulls, 8 KiB loses 10-20% everywhere).
+// Gather stage geometry, two instantiations: sources over NVLink pull 32 KiB chunks through
+// 3 stages (96 KiB in flight per SM: at N = 4 the gathers reach 0.81 of 770 GB/s vs 0.79
+// with 4 stages and 0.74 with 2; N = 2 equal; r02_ab_remote_gather.jsonl); a single local
+// source (P = 1, or P' = 1 backward) is a device-local copy and streams 16 KiB chunks
+// through 8 stages (measured at N = 1: fwd / bwd gathers at 0.91 of the HBM copy peak vs
+// 0.85-0.87 with 32 KiB; at N = 4 the 16 KiB geometry loses 2-5% on NVLink pulls, 8 KiB
+// loses 10-20% everywhere).
 constexpr int kGatherChunk = HPZ_GATHER_CHUNK;   // bytes per gather stage (remote sources)
 constexpr int kGatherStages = HPZ_GATHER_STAGES;
 #ifndef HPZ_GATHER_LOCAL_CHUNK
@@ -65,6 +67,11 @@ constexpr int kRsChunk = 1024;          // base shard elements per RS stage
 #endif
 #ifndef HPZ_RS_MAX_STAGES
 #define HPZ_RS_MAX_STAGES 6
+#endif
+#ifndef HPZ_RS_STAGES_P4PLUS
+#define HPZ_RS_STAGES_P4PLUS 2          // stage cap for P >= 4 (0 = none): less peer data in flight per
+                                        // SM measured faster in the all-to-all (P=4: 2 stages 1.2%
+                                        // faster than 4; r02_ab_rs_stages.jsonl); P = 8 fits 2 anyway
 #endif
 #ifndef HPZ_GATHER_ROTATE
 #define HPZ_GATHER_ROTATE 0             // 1: rotate each gather CTA through the sources (chunk_of);
@@ -312,7 +319,8 @@ struct RsCfg {
   static constexpr int kStageBytes = kPrimOff;
   static constexpr int kBudget = HPZ_RS_BUDGET_KB * 1024;
   static constexpr int kFit = kBudget / kStageBytes;
-  static constexpr int kStages = kFit >= HPZ_RS_MAX_STAGES ? HPZ_RS_MAX_STAGES : (kFit < 2 ? 2 : kFit);
+  static constexpr int kMax = (P >= 4 && HPZ_RS_STAGES_P4PLUS > 0) ? HPZ_RS_STAGES_P4PLUS : HPZ_RS_MAX_STAGES;
+  static constexpr int kStages = kFit >= kMax ? kMax : (kFit < 2 ? 2 : kFit);
   // consumer threads: one float4 per thread per chunk, at most 16 warps (idle polling
   // warps would steal issue slots from the working ones)
   static constexpr int kConsumers = kChunk / 4 < kRsMaxConsumers ? kChunk / 4 : kRsMaxConsumers;
