@@ -756,13 +756,20 @@ def p2p_ceiling(world, rank):
     if rank == 0:
         exe = os.path.join(ROOT, "tools", "p2p_probe")
         try:
-            out = subprocess.run([exe, str(world), "pull_tma", "512", "1", "32768"], capture_output=True, text=True,
-                                 timeout=120).stdout
-            m = re.search(r"per-GPU GB/s: min ([0-9.]+) avg ([0-9.]+)", out)
-            if m:
-                res = {"pull_tma_GBps_per_gpu_min": float(m.group(1)), "pull_tma_GBps_per_gpu_avg": float(m.group(2)),
-                       "how": f"tools/p2p_probe {world} pull_tma 512 1 32768: all {world} GPUs TMA-pull 512 MiB from "
-                              f"every peer concurrently (bulk copies through smem, 1 CTA/SM), per-GPU ingress"}
+            by_depth = {}
+            for depth in (2, 3, 4):           # the ceiling: the best stage-ring depth
+                out = subprocess.run([exe, str(world), "pull_tma", "512", "1", "32768", "0", "50", str(depth)],
+                                     capture_output=True, text=True, timeout=120).stdout
+                m = re.search(r"per-GPU GB/s: min ([0-9.]+) avg ([0-9.]+)", out)
+                if m:
+                    by_depth[depth] = (float(m.group(1)), float(m.group(2)))
+            if by_depth:
+                best = max(by_depth, key=lambda d: by_depth[d][1])
+                res = {"pull_tma_GBps_per_gpu_min": by_depth[best][0], "pull_tma_GBps_per_gpu_avg": by_depth[best][1],
+                       "avg_by_stage_depth": {str(d): v[1] for d, v in by_depth.items()},
+                       "how": f"tools/p2p_probe {world} pull_tma 512 1 32768 0 50 DEPTH: all {world} GPUs TMA-pull "
+                              f"512 MiB from every peer concurrently (bulk copies through a DEPTH x 32 KiB smem ring, "
+                              f"1 CTA/SM), per-GPU ingress; best depth of 2, 3, 4 ({best})"}
         except Exception:          # noqa: BLE001  (a missing or failing probe only drops this field)
             res = None
         finally:

@@ -151,6 +151,10 @@ int main(int argc, char** argv) {
   // streams: does mixing the two request paths exceed either alone?
   const bool mix = strstr(mode, "mix") != nullptr;
   const int mix_pct = argc > 7 ? atoi(argv[7]) : 50;
+  // TMA stage ring depth (argv[8], default 4): the ceiling is the best over depths
+  const int stages = argc > 8 ? atoi(argv[8]) : 4;
+  void (*tma_k)(const Ptrs, int) = stages == 2 ? copy_tma<2> : stages == 3 ? copy_tma<3> : stages == 6 ? copy_tma<6> : copy_tma<4>;
+  const int n_stages = (stages == 2 || stages == 3 || stages == 6) ? stages : 4;
   cudaStream_t st[kMaxG], st2[kMaxG];
   cudaEvent_t e0[kMaxG], e1[kMaxG], e2[kMaxG];
   Ptrs P[kMaxG], PA[kMaxG], PB[kMaxG];
@@ -176,8 +180,8 @@ int main(int argc, char** argv) {
       p.n++;
     }
     if (tma || mix) {
-      int smem = 4 * chunk;
-      CK(cudaFuncSetAttribute(copy_tma<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      int smem = n_stages * chunk;
+      CK(cudaFuncSetAttribute(tma_k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     }
     if (mix) {   // split every peer buffer: [0, a) by TMA, [a, bytes) by LDG/STG
       const int64_t a = (bytes * mix_pct / 100) / 4096 * 4096;
@@ -197,12 +201,12 @@ int main(int argc, char** argv) {
       CK(cudaEventRecord(e0[g], st[g]));
       if (mix) {
         CK(cudaStreamWaitEvent(st2[g], e0[g], 0));
-        copy_tma<4><<<sms, 32, 4 * chunk, st[g]>>>(PA[g], chunk);
+        tma_k<<<sms, 32, n_stages * chunk, st[g]>>>(PA[g], chunk);
         copy_ldg<8><<<sms * ctas_per_sm, 256, 0, st2[g]>>>(PB[g]);
         CK(cudaEventRecord(e2[g], st2[g]));
         CK(cudaStreamWaitEvent(st[g], e2[g], 0));
       } else if (tma)
-        copy_tma<4><<<sms * ctas_per_sm, 32, 4 * chunk, st[g]>>>(P[g], chunk);
+        tma_k<<<sms * ctas_per_sm, 32, n_stages * chunk, st[g]>>>(P[g], chunk);
       else
         copy_ldg<8><<<sms * ctas_per_sm, 256, 0, st[g]>>>(P[g]);
       CK(cudaGetLastError());
@@ -219,8 +223,8 @@ int main(int argc, char** argv) {
       sum += gbs;
     }
     if (it == 3)
-      printf("mode=%s G=%d MB/peer=%lld ctas/sm=%d chunk=%d  per-GPU GB/s: min %.1f avg %.1f\n", mode, G,
-             (long long)mb, ctas_per_sm, chunk, worst, sum / G);
+      printf("mode=%s G=%d MB/peer=%lld ctas/sm=%d chunk=%d stages=%d  per-GPU GB/s: min %.1f avg %.1f\n", mode, G,
+             (long long)mb, ctas_per_sm, chunk, n_stages, worst, sum / G);
   }
   // verify one region
   CK(cudaSetDevice(0));
