@@ -320,7 +320,7 @@ struct RsCfg {
   static constexpr int kBudget = HPZ_RS_BUDGET_KB * 1024;
   static constexpr int kFit = kBudget / kStageBytes;
   // the P >= 4 cap was measured on the fp32 RS only: qgZ / bf16 gradients keep the budget rule
-  static constexpr int kMax = (P >= 4 && MODE == 0 && HPZ_RS_STAGES_P4PLUS > 0) ? HPZ_RS_STAGES_P4PLUS
+  static constexpr int kMax = (P >= 4 && MODE == RS_F32 && HPZ_RS_STAGES_P4PLUS > 0) ? HPZ_RS_STAGES_P4PLUS
                                                                                  : HPZ_RS_MAX_STAGES;
   static constexpr int kStages = kFit >= kMax ? kMax : (kFit < 2 ? 2 : kFit);
   // consumer threads: one float4 per thread per chunk, at most 16 warps (idle polling
