@@ -293,6 +293,42 @@ __global__ void __launch_bounds__(T) ldg_wide_fp(const int4* src, int4* dst, int
   }
 }
 
+// persistent warps, each taking runs of R warp-tiles (32 lanes x U int4) from a counter with
+// the next run's counter read issued ahead; copy through registers + register fingerprint
+template <int U, int R>
+__global__ void __launch_bounds__(256) ldg_dyn_fp(const int4* src, int4* dst, int64_t n, unsigned* ctr,
+                                                  unsigned long long* fp_out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t tiles = (n + 32 * U - 1) / (32 * U);
+  unsigned nxt = 0;
+  if (lane == 0) nxt = atomicAdd(ctr, (unsigned)R);
+  unsigned long long acc = 0;
+  for (;;) {
+    const int64_t run = (int64_t)__shfl_sync(0xffffffffu, nxt, 0);
+    if (run >= tiles) break;
+    if (lane == 0) nxt = atomicAdd(ctr, (unsigned)R);
+    for (int t = 0; t < R && run + t < tiles; ++t) {
+      const int64_t base = (run + t) * 32 * U + lane;
+      int4 r[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (base + u * 32 < n) r[u] = src[base + u * 32];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (base + u * 32 < n) {
+          dst[base + u * 32] = r[u];
+          const uint32_t q = (uint32_t)(base + u * 32) * 4u * 0x9E3779B1u;
+          acc += (unsigned long long)(uint32_t)r[u].x * (q | 1u) + (unsigned long long)(uint32_t)r[u].y * ((q + 0x9E3779B1u) | 1u) +
+                 (unsigned long long)(uint32_t)r[u].z * ((q + 2u * 0x9E3779B1u) | 1u) +
+                 (unsigned long long)(uint32_t)r[u].w * ((q + 3u * 0x9E3779B1u) | 1u);
+        }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0 && acc) atomicAdd(fp_out, acc);
+}
+
 __global__ void __launch_bounds__(32) tma_wide(const char* src, char* dst, int64_t bytes, int tile) {
   extern __shared__ __align__(1024) char smem[];
   __shared__ __align__(8) uint64_t full;
@@ -428,6 +464,16 @@ int main(int argc, char** argv) {
   LDG_WF(8, 512)
   LDG_WF(4, 512)
   LDG_WF(16, 256)
+#define LDG_DF(U, R, C)                                                                                   \
+  printf("ldg_dyn_fp U=%d R=%d %d CTA/SM  %.1f GB/s\n", U, R, C, timeit([&] {                               \
+           CK(cudaMemsetAsync(ctr, 0, 8));                                                                  \
+           ldg_dyn_fp<U, R><<<sms * C, 256>>>((const int4*)src, (int4*)dst, n16, (unsigned*)ctr, fpo);      \
+         }, bytes));
+  LDG_DF(8, 4, 8)
+  LDG_DF(8, 8, 8)
+  LDG_DF(8, 4, 4)
+  LDG_DF(4, 8, 8)
+  LDG_DF(16, 4, 4)
   TMA_W(16384)
   TMA_W(32768)
   TMA_W(65536)
