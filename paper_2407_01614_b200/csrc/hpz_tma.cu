@@ -62,7 +62,7 @@ constexpr int kRsChunk = 1024;          // base shard elements per RS stage
 #define HPZ_RS_PN_MUL 2                 // 2 <= P <= 8 chunk multiplier (A/B builds)
 #endif
 #ifndef HPZ_RS_BUDGET_KB
-#define HPZ_RS_BUDGET_KB 224            // shared-memory stage budget per CTA: 4 stages at P = 4
+#define HPZ_RS_BUDGET_KB 224            // shared-memory stage budget per CTA (4 stages at P = 4 under the budget alone; fp32 RS is capped, HPZ_RS_STAGES_P4PLUS)
                                         // (0.820 vs 0.814 of 770 GB/s with 200 KiB, N=4 A/B)
 #endif
 #ifndef HPZ_RS_MAX_STAGES
