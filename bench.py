@@ -303,6 +303,40 @@ def relaunch(n):
     return p.wait()
 
 
+def step_bytes(numel_pad, shard, P, Pp, e, grad_dtype="f32", qgz=False, qwz=False, fused=True):
+    """Algorithmic bytes per rank per step (SURVEY §8(d) per padded model
+    element: forward gather 2(P-1)/P, backward 2(P'-1)/P', RS 4(P-1)/P of NVLink ingress,
+    fused Adam 30/P of HBM).  numel_pad / shard: per layer.  Returns
+      ag      AllGather output bytes (N̂·e), coll = 2·ag + fp32 RS input (the `value` bytes),
+      rs_in   RS input bytes in the slot dtype, adam = the optimizer's HBM bytes,
+      nvlink  per kernel: NVLink ingress (busbw convention; qgZ / qwZ: wire bytes),
+      hbm     per kernel: every byte it reads or writes in this GPU's memory, incl. what it
+              serves to peers,
+      hbm_p1  per kernel at P = 1: the local copy / update bytes (the N = 1 roofline)."""
+    N, S = sum(numel_pad), sum(shard)
+    ag = N * e
+    coll = 2 * ag + N * 4
+    rs_in = N * (2 if grad_dtype == "bf16" else 4)
+    rs_wire = rs_in * (0.625 / 4 if qgz else 1.0)          # qgZ: int4 codes + (min, scale) per 64
+    fwd_wire = ag * ((1 + 8 / 256) / e if qwz else 1.0)     # qwZ: int8 codes + (min, scale) per 256
+    adam = S * (30 if e == 2 else 32)
+    sec = 0 if (Pp == P and not qwz) else ag / Pp           # P' == P: secondary is the primary (SPEC.md:133)
+    rs_name = "reduce_scatter+adam" if fused else "reduce_scatter"
+    nvlink = {"fwd_gather": fwd_wire * (P - 1) / P, "bwd_gather": ag * (Pp - 1) / Pp,
+              "reduce_scatter": rs_wire * (P - 1) / P, "reduce_scatter+adam": rs_wire * (P - 1) / P, "adam": adam}
+    hbm = {"fwd_gather": 2 * ag + sec,                      # serve primary; write out (+ secondary)
+           "bwd_gather": 2 * ag,                            # serve secondary; write out
+           # RS: my slot is read once in total (by its owners); fused Adam: w, m, v read +
+           # written (24 B) and the primary refreshed (e); unfused: the fp32 shard written
+           rs_name: rs_in + (S * (24 + e) if fused else S * 4)}
+    hbm_p1 = {"fwd_gather": 2 * ag + sec, "bwd_gather": 2 * ag, "reduce_scatter": 2 * rs_in, "adam": adam,
+              # fused at P=1: read grad slot 4 + w,m,v 12; write w,m,v 12 + primary e
+              "reduce_scatter+adam": S * (28 + e)}
+    ingress = nvlink["fwd_gather"] + nvlink["bwd_gather"] + nvlink["reduce_scatter"]
+    return {"ag": ag, "coll": coll, "rs_in": rs_in, "adam": adam, "sec": sec, "nvlink": nvlink, "hbm": hbm,
+            "hbm_p1": hbm_p1, "ingress": ingress}
+
+
 def make_config(args, world, node_size, n_layers, n_params, n_slots):
     """The workload this line measures (identical for both arms)."""
     extra = {"share_gpus": "FUNCTIONAL CHECK: ranks time-slice shared GPUs; the timings are not "
@@ -552,18 +586,10 @@ def main():
                 f.write(json.dumps(r) + "\n")
     tot = {k: sum(a.elapsed_time(b) for a, b in zip(evs[k + "0"], evs[k + "1"])) / KB
            for k in ("fwd", "bwd", "rs", "adam", "q", "g")}
-    # bytes per rank per step (algbw: AG output bytes, RS input bytes)
-    ag_bytes = sum(x.numel_pad for x in infos) * e
-    rs_bytes = sum(x.numel_pad for x in infos) * 4
-    coll_bytes = 2 * ag_bytes + rs_bytes
-    # NVLink ingress per rank per step (busbw convention)
     P, Pp = world, node_size
-    gsz = 2 if args.grad_dtype == "bf16" else 4
-    rs_bytes = sum(x.numel_pad for x in infos) * gsz      # RS input bytes in the slot dtype
-    rs_wire = rs_bytes * (0.625 / 4 if args.qgz else 1.0)
-    fwd_wire = ag_bytes * ((1 + 8 / 256) / e if args.qwz else 1.0)
-    ingress = fwd_wire * (P - 1) / P + ag_bytes * (Pp - 1) / Pp + rs_wire * (P - 1) / P
-    adam_bytes = sum(x.shard for x in infos) * (30 if dtype == "bf16" else 32)
+    B = step_bytes([x.numel_pad for x in infos], [x.shard for x in infos], P, Pp, e, args.grad_dtype,
+                   args.qgz, args.qwz, fused)
+    ag_bytes, coll_bytes, rs_bytes, adam_bytes = B["ag"], B["coll"], B["rs_in"], B["adam"]
 
     vals = max_over_ranks([step_ms, tot["fwd"], tot["bwd"], tot["rs"], tot["adam"],
                            tot["fwd"] + tot["bwd"] + tot["rs"] + tot["q"], tot["q"], tot["g"]], device=dev)
@@ -582,20 +608,11 @@ def main():
     if not fused:
         share["adam"] = adam_ms
     dom = max(share, key=share.get)
-    # P' == P: the secondary is the primary (no secondary store)
-    sec_bytes = 0 if (node_size == world and not args.qwz) else ag_bytes / node_size
     if world == 1:
-        hbm_alg = {"fwd_gather": 2 * ag_bytes + sec_bytes,   # read primary, write full out (+ secondary)
-                   "bwd_gather": 2 * ag_bytes, "reduce_scatter": 2 * rs_bytes, "adam": adam_bytes,
-                   # fused at P=1: read grad slot 4 + w,m,v 12; write w,m,v 12 + primary e
-                   "reduce_scatter+adam": sum(x.shard for x in infos) * (28 + e)}
-        alg = hbm_alg[dom]
+        alg = B["hbm_p1"][dom]
         bound, peak, unit = "hbm", hbm_peak, "GB/s"
     else:
-        nv_alg = {"fwd_gather": fwd_wire * (P - 1) / P, "bwd_gather": ag_bytes * (Pp - 1) / Pp,
-                  "reduce_scatter": rs_wire * (P - 1) / P, "adam": adam_bytes,
-                  "reduce_scatter+adam": rs_wire * (P - 1) / P}
-        alg = nv_alg[dom]
+        alg = B["nvlink"][dom]
         if dom == "adam":
             bound, peak, unit = "hbm", hbm_peak, "GB/s"
         else:
@@ -636,14 +653,7 @@ def main():
     # against 900 per direction, HBM GB/s against the measured copy peak); algorithmic bytes
     # per rank and step: NVLink ingress as above; HBM = every byte each kernel must read or
     # write in this GPU's memory (incl. the shards it serves to peers)
-    shard_sum = sum(x.shard for x in infos)
-    hbm_k = {"fwd_gather": ag_bytes + ag_bytes + sec_bytes,          # serve primary; write out (+ secondary)
-             "bwd_gather": ag_bytes + ag_bytes,                       # serve secondary; write out
-             # RS: my slot is read once in total (by its owners); fused Adam: w, m, v read +
-             # written (24 B) and the primary refreshed (e); unfused: the fp32 shard written
-             rs_name: rs_bytes + (shard_sum * (24 + e) if fused else shard_sum * 4)}
-    nv_k = {"fwd_gather": fwd_wire * (P - 1) / P, "bwd_gather": ag_bytes * (Pp - 1) / Pp,
-            rs_name: rs_wire * (P - 1) / P}
+    hbm_k, nv_k = B["hbm"], B["nvlink"]
     kernels = {}
     for k, ms in (("fwd_gather", fwd_ms), ("bwd_gather", bwd_ms), (rs_name, rs_ms)):
         if ms <= 0:
@@ -683,7 +693,8 @@ def main():
         barrier()
         e2e_ms = max_over_ranks([a.elapsed_time(b) / args.e2e_steps], device=dev)[0]
         e2e = {"value": round(world * coll_bytes / (e2e_ms * 1e-3) / 1e9, 2), "unit": "GB/s",
-               "h2d_bytes_per_step": sum(x.numel for x in infos) * gsz, "d2h_bytes_per_step": 5 * 8,
+               "h2d_bytes_per_step": sum(x.numel for x in infos) * (2 if args.grad_dtype == "bf16" else 4),
+               "d2h_bytes_per_step": 5 * 8,
                "ms_per_step": round(e2e_ms, 3),
                "note": "through the C ABI: every layer's gradient uploaded from pinned host memory "
                        "(hpz_grad_upload, on a copy stream overlapping the gathers) inside the timed "
@@ -727,8 +738,8 @@ def main():
                                       "qgz_quantize": round(q_ms, 3), "grad_synth": round(g_ms, 3),
                                       "collectives": round(coll_ms, 3)},
             "fused_rs_adam": fused,
-            "nvlink_ingress_GBps_per_gpu": round(ingress / (step_ms * 1e-3) / 1e9, 2) if world > 1 else None,
-            "nvlink_frac_of_900": round(ingress / (step_ms * 1e-3) / 1e9 / 900, 4) if world > 1 else None,
+            "nvlink_ingress_GBps_per_gpu": round(B["ingress"] / (step_ms * 1e-3) / 1e9, 2) if world > 1 else None,
+            "nvlink_frac_of_900": round(B["ingress"] / (step_ms * 1e-3) / 1e9 / 900, 4) if world > 1 else None,
             "collectives_only_GBps": round(world * coll_bytes / (coll_ms * 1e-3) / 1e9, 2),
             "roofline": roofline, "kernels": kernels,
             "cpu_baseline": cpu,

@@ -38,3 +38,30 @@ def test_n1_traffic_within_algorithmic_bytes():
     t = json.load(open(P("ncu_traffic.json")))
     for k in ("P1_fwd_gather", "P1_bwd_gather", "P1_reduce_scatter+adam"):
         assert t[k]["dram_bytes_per_launch"] <= t[k]["launch_alg_bytes"], k
+
+
+def test_bench_algorithmic_bytes_match_survey_c2():
+    """bench.step_bytes (the roofline's and the per-kernel table's denominators) on the C2
+    configuration — Falcon-7B, P = 8, P' = 4 and 2, layout from the ORACLE (independent of
+    the library) — reproduces SURVEY §8's per-step figures: forward-gather ingress 12.11 GB
+    (a2), backward 10.38 / 6.92 GB (a4), RS 24.23 GB (a5), fused Adam 25.96 GB of HBM (a6)."""
+    sys.path.insert(0, ROOT)
+    import bench
+    from oracle import hpz_oracle as O
+    from paper_2407_01614_b200 import shapes
+    numels = shapes.numels("falcon7b")
+    for Pp, bwd in ((4, 10.38), (2, 6.92)):
+        lays = [O.LayerLayout(n, 8, Pp, 256) for n in numels]
+        B = bench.step_bytes([x.numel_pad for x in lays], [x.shard for x in lays], 8, Pp, 2)
+        assert round(B["nvlink"]["fwd_gather"] / 1e9, 2) == 12.11
+        assert round(B["nvlink"]["bwd_gather"] / 1e9, 2) == bwd
+        assert round(B["nvlink"]["reduce_scatter+adam"] / 1e9, 2) == 24.23
+        assert round(B["adam"] / 1e9, 2) == 25.96
+        # per padded element: 2(P-1)/P, 2(P'-1)/P', 4(P-1)/P, 30/P (SURVEY §8(d))
+        N = sum(x.numel_pad for x in lays)
+        assert B["nvlink"]["fwd_gather"] == N * 2 * 7 / 8 and B["nvlink"]["bwd_gather"] == N * 2 * (Pp - 1) / Pp
+        assert B["hbm_p1"]["reduce_scatter+adam"] == sum(x.shard for x in lays) * 30
+    # P' = P: no secondary bytes (SPEC.md:133); qwZ keeps one
+    lays = [O.LayerLayout(n, 4, 4, 256) for n in numels]
+    assert bench.step_bytes([x.numel_pad for x in lays], [x.shard for x in lays], 4, 4, 2)["sec"] == 0
+    assert bench.step_bytes([x.numel_pad for x in lays], [x.shard for x in lays], 4, 4, 2, qwz=True)["sec"] > 0
