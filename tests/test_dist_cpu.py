@@ -23,6 +23,9 @@ def _worker(rank, world, port, q):
     got = exchange_handles(h)
     mx = max_over_ranks([float(rank), 10.0 - rank])
     sm = sum_over_ranks([1.0, float(rank)])
+    # gloo (the --share-gpus control plane): a CUDA device argument reduces on the host
+    assert max_over_ranks([float(rank)], device="cuda") == [1.0]
+    assert sum_over_ranks([1.0], device=torch.device("cuda", 0)) == [2.0]
     groups = virtual_nodes(world, 1)
     subg = [dist.new_group(g) for g in groups]
     mine = subg[rank]
@@ -97,3 +100,16 @@ def test_bench_reference_arm_without_launcher():
     from paper_2407_01614_b200 import shapes
     n = shapes.numels("falcon7b")
     assert d["config"] == bench.make_config(args, 8, 4, len(n), sum(n), len(n))
+
+
+def test_share_gpus_config_is_labelled():
+    """`bench.py --share-gpus` lines say they are functional checks, not measurements."""
+    import argparse
+    sys.path.insert(0, ROOT)
+    import bench
+    args = argparse.Namespace(model="falcon7b_block", order="fixed", verify="fingerprint", copy_engine="tma",
+                              overlap_bwd=0, qgz=False, grad_dtype="f32", qwz=False, graph=1, share_gpus=True)
+    cfg = bench.make_config(args, 8, 4, 1, 207070080, 1)
+    assert "FUNCTIONAL CHECK" in cfg["share_gpus"] and cfg["parallelism"] == "hpZ dp8 (P=8, P'=4)"
+    args.share_gpus = False
+    assert "share_gpus" not in bench.make_config(args, 8, 4, 1, 207070080, 1)
